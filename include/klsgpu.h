@@ -1,0 +1,123 @@
+/*
+ * klsgpu.h — C-ABI of libklsgpu.so, the sm_100a kernels behind the
+ * DCGS2 / CGS2 Arnoldi-QR hot path of arXiv 2104.01253.
+ *
+ * Every entry point takes plain device pointers, sizes, leading dimensions
+ * and a cudaStream_t passed as void*.  Nothing allocates: workspaces are
+ * caller-owned (size them with kls_workspace_bytes and zero them once).
+ * Return value: 0 on success, <0 on error (KLS_EINVAL bad argument,
+ * KLS_ECUDA CUDA error, KLS_ENOSPC workspace too small); the message is in
+ * kls_last_error() (thread-local).  Numerical breakdowns are not errors at
+ * this level: the host decides them from the reduced scalars and raises the
+ * reference's exceptions (errors.py:4-39).
+ *
+ * Layout: a basis block Q is column-major with leading dimension ldq (even;
+ * the Python host pads it to a multiple of 32 doubles).  Vectors are fp64
+ * arrays of m rows, 16-byte aligned.  Reductions are deterministic (fixed
+ * summation order, no fp64 atomics); results are bitwise reproducible for a
+ * fixed device.
+ *
+ * Each declaration cites the reference interface it replaces
+ * (/root/reference/pkg/src/kls/<file>:<line>).
+ */
+#ifndef KLSGPU_H
+#define KLSGPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KLS_OK 0
+#define KLS_EINVAL (-1)
+#define KLS_ECUDA (-2)
+#define KLS_ENOSPC (-3)
+
+/* Library ABI version (1). */
+int kls_version(void);
+/* Message of the last failing call on this thread. */
+const char* kls_last_error(void);
+/* SM count of the current device (grid sizing). */
+int kls_device_sm_count(void);
+
+/* Bytes of reduction workspace that cover any call with <= kmax basis
+ * columns on the current device.  Zero it once before first use; every
+ * reducing kernel leaves its ticket at zero again. */
+size_t kls_workspace_bytes(int64_t m, int32_t kmax);
+
+/* Fused block inner products — kernels.mv_trans_mv (kernels.py:44-60):
+ *   out = [Q(:, 0:k), bext]^T [x0 (, x1)]      column-major,
+ *         (k + (bext != NULL)) rows x nx columns (nx = 1 or 2),
+ *   then out[rows*nx] = x_last . x_last when xnorm != 0.
+ * bext == NULL drops the extra left column; k == 0 is allowed (the empty
+ * basis block still reduces, kernels.py:5-9).  One pass over Q. */
+int kls_mv_trans_mv(const double* Q, int64_t ldq, int64_t m, int32_t k, const double* bext,
+                    const double* x0, const double* x1, int32_t nx, int32_t xnorm, double* out,
+                    void* ws, size_t ws_bytes, void* stream);
+
+/* The single fused reduction of a DCGS2 Arnoldi step — replaces
+ *   g = mv_trans_mv(np.hstack([Q, w]), np.column_stack([w, aw]))
+ * (arnoldi.py:362-370) plus the guard norm ||aw|| (arnoldi.py:414):
+ *   out[0:j]   = c = Q^T w      out[j]     = beta  = w.w
+ *   out[j+1:2j+1] = s = Q^T aw  out[2j+1]  = s_piv = w.aw
+ *   out[2j+2]  = aw.aw
+ * 2j+3 doubles: the payload of the one allreduce per step. */
+int kls_gram_dcgs2(const double* Q, int64_t ldq, int64_t m, int32_t j, const double* w,
+                   const double* aw, double* out, void* ws, size_t ws_bytes, void* stream);
+
+/* Fused DCGS2 update — the two MvTimesMatAddMv of a step
+ * (arnoldi.py:389-391 and 415-420; QR form ortho.py:371-375, 396-398):
+ *   u = w - Q(:,0:j) c;  Q(:, j) = u / alpha;
+ *   w = (divide ? aw / alpha : aw) - (Q(:,0:j) t(0:j) + Q(:,j) t_j)
+ * coef (device) = [c(0:j), t(0:j+1)], 2j+1 doubles.  One pass over Q. */
+int kls_dcgs2_update(double* Q, int64_t ldq, int64_t m, int32_t j, double* w, const double* aw,
+                     const double* coef, double alpha, int32_t divide, void* stream);
+
+/* Y(:,0:l) <- scale*Y + sign*B(:,0:k) S — kernels.mv_times_mat_add_mv
+ * (kernels.py:63-84) for l = 1 or 2; S is k x l column-major on the device.
+ * nrm_out (optional, device) receives ||Y(:, l-1)||^2 of the result, fusing
+ * the norm2 that follows a projection (ortho.py:153-154, arnoldi.py:433-434). */
+int kls_mv_times_mat_add_mv(double* Y, int64_t ldy, int64_t m, int32_t l, const double* B,
+                            int64_t ldb, int32_t k, const double* S, double sign, double scale,
+                            double* nrm_out, void* ws, size_t ws_bytes, void* stream);
+
+/* y = A x for CSR rows (int64 row pointer, int32 columns, fp64 values),
+ * bit-identical to CsrMatrix.matvec (problems.py:127-136): products, then
+ * numpy's reduceat/pairwise summation order per row. */
+int kls_csr_spmv(const int64_t* rowptr, const int32_t* col, const double* val, int64_t nrows,
+                 const double* x, double* y, void* stream);
+
+/* Matrix-free 7-point Laplacian, bit-identical to StencilLaplace3D._matvec
+ * (problems.py:296-305) on nx local x-planes of a (.., ny, nz) grid; x_lo /
+ * x_hi are the neighbouring planes of other ranks (NULL at the boundary). */
+int kls_stencil7(const double* x, const double* x_lo, const double* x_hi, double* y, int64_t nx,
+                 int64_t ny, int64_t nz, void* stream);
+
+/* y = A x for a row-major dense A (DenseOperator._matvec, problems.py:76-77). */
+int kls_dense_gemv(const double* a, int64_t lda, int64_t n, const double* x, double* y,
+                   void* stream);
+
+/* y = x / alpha (mode 0, the normalisations u / alpha of arnoldi.py:391,453,
+ * ortho.py:136,158,398) or y = x * alpha (mode 1). */
+int kls_scale(const double* x, double* y, int64_t n, double alpha, int32_t mode, void* stream);
+
+/* out = a - b (restart residual b - A x, gmres.py:151). */
+int kls_sub(const double* a, const double* b, double* out, int64_t n, void* stream);
+
+/* Backward-error norms in one pass (gmres.backward_error, gmres.py:46-60):
+ * out = [||b - ax||^2, ||x||^2, ||b||^2] (device). */
+int kls_resid_norms(const double* b, const double* ax, const double* x, int64_t n, double* out,
+                    void* ws, size_t ws_bytes, void* stream);
+
+/* V(:, 0:k) <- V(:, 0:k) Z in place, Z k x k column-major on the device —
+ * the Krylov-Schur basis rotation v_mat[:, nlock:k] @ Z (eig.py:237). */
+int kls_tsgemm_inplace(double* V, int64_t ldv, int64_t m, int32_t k, const double* Z,
+                       void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* KLSGPU_H */

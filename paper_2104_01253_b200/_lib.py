@@ -1,0 +1,96 @@
+"""ctypes binding of libklsgpu.so (the C-ABI declared in include/klsgpu.h).
+
+There is no fallback: if the library or a GPU is missing, the first kernel
+call raises.  Loading the library itself does not need a GPU, so the CPU
+test suite can check that every declared symbol is exported.
+"""
+
+import ctypes
+import os
+import threading
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libklsgpu.so")
+
+c_dp = ctypes.c_void_p  # device pointers travel as integers
+i32 = ctypes.c_int32
+i64 = ctypes.c_int64
+f64 = ctypes.c_double
+sz = ctypes.c_size_t
+
+# name -> (restype, argtypes); must match include/klsgpu.h
+SIGNATURES = {
+    "kls_version": (ctypes.c_int, []),
+    "kls_last_error": (ctypes.c_char_p, []),
+    "kls_device_sm_count": (ctypes.c_int, []),
+    "kls_workspace_bytes": (sz, [i64, i32]),
+    "kls_mv_trans_mv": (ctypes.c_int, [c_dp, i64, i64, i32, c_dp, c_dp, c_dp, i32, i32, c_dp, c_dp, sz, c_dp]),
+    "kls_gram_dcgs2": (ctypes.c_int, [c_dp, i64, i64, i32, c_dp, c_dp, c_dp, c_dp, sz, c_dp]),
+    "kls_dcgs2_update": (ctypes.c_int, [c_dp, i64, i64, i32, c_dp, c_dp, c_dp, f64, i32, c_dp]),
+    "kls_mv_times_mat_add_mv": (
+        ctypes.c_int,
+        [c_dp, i64, i64, i32, c_dp, i64, i32, c_dp, f64, f64, c_dp, c_dp, sz, c_dp],
+    ),
+    "kls_csr_spmv": (ctypes.c_int, [c_dp, c_dp, c_dp, i64, c_dp, c_dp, c_dp]),
+    "kls_stencil7": (ctypes.c_int, [c_dp, c_dp, c_dp, c_dp, i64, i64, i64, c_dp]),
+    "kls_dense_gemv": (ctypes.c_int, [c_dp, i64, i64, c_dp, c_dp, c_dp]),
+    "kls_scale": (ctypes.c_int, [c_dp, c_dp, i64, f64, i32, c_dp]),
+    "kls_sub": (ctypes.c_int, [c_dp, c_dp, c_dp, i64, c_dp]),
+    "kls_resid_norms": (ctypes.c_int, [c_dp, c_dp, c_dp, i64, c_dp, c_dp, sz, c_dp]),
+    "kls_tsgemm_inplace": (ctypes.c_int, [c_dp, i64, i64, i32, c_dp, c_dp]),
+}
+
+_lock = threading.Lock()
+_lib = None
+_launches = 0  # kernel-launching calls made through this binding
+
+
+class KlsGpuError(RuntimeError):
+    """A libklsgpu call returned a negative status."""
+
+
+def load():
+    """Load libklsgpu.so (building it first if nvcc is present and it is stale)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            try:
+                from .csrc.build import build
+
+                build()
+            except Exception as exc:  # no toolkit on this host: report loudly
+                raise RuntimeError(
+                    f"libklsgpu.so is missing at {LIB_PATH} and could not be built: {exc}"
+                ) from exc
+        lib = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+    return _lib
+
+
+def call(name, *args):
+    """Invoke a status-returning entry point; raise KlsGpuError on failure."""
+    global _launches
+    lib = load()
+    rc = getattr(lib, name)(*args)
+    if rc != 0:
+        msg = lib.kls_last_error().decode(errors="replace")
+        raise KlsGpuError(f"{name} failed ({rc}): {msg}")
+    _launches += 1
+    return rc
+
+
+def launch_count():
+    return _launches
+
+
+def reset_launch_count():
+    global _launches
+    _launches = 0

@@ -1,0 +1,382 @@
+"""Arnoldi expansions A V_k = V_{k+1} Hbar_k on the device (reference
+arnoldi.py).
+
+The basis V lives in HBM (column-major, one padded column per basis
+vector); the small Hessenberg matrix and the DCGS2 correction ledger K stay
+on the host in numpy, updated in exactly the reference's order from the
+reduced Gram scalars, so H is bit-faithful to the scalars it is given.
+
+``dcgs2`` — _DelayedArnoldi (arnoldi.py:307-455): one fused reduction per
+step (kls_gram_dcgs2), one fused update pass (kls_dcgs2_update), one
+operator application.  ``cgs2`` — _ImmediateArnoldi with CGS2
+(arnoldi.py:121-172, ortho.py:139-158): three reductions per step.
+Other reference schemes are outside the hot path and
+raise UnknownSchemeError.
+"""
+
+import numpy as np
+import torch
+
+from . import ledger as _ledger
+from ._engine import Engine
+from .errors import BreakdownError, DimensionError, UnknownSchemeError
+from .ledger import SyncLedger
+
+_EPS = np.finfo(np.float64).eps
+
+ARNOLDI_SCHEMES = ("cgs2", "dcgs2")
+
+
+def _unsupported(scheme):
+    return UnknownSchemeError(
+        f"unknown scheme {scheme!r} (the B200 backend provides {', '.join(ARNOLDI_SCHEMES)})")
+
+
+class _BaseArnoldi:
+    scheme_id = None
+
+    def __init__(self, op, capacity, ledger):
+        if capacity < 2:
+            raise DimensionError("capacity of at least 2 basis vectors required")
+        self.op = op
+        self.capacity = capacity
+        self.ledger = ledger if ledger is not None else SyncLedger()
+        self.m = op.shape[0]
+        self.eng = Engine(op, capacity)
+        self._h = np.zeros((capacity, capacity - 1))
+        self.nbasis = 0
+        self.hcols = 0
+        self.happy = False
+        self.start_norm = None
+
+    # -- views (device tensors for the basis, numpy for H) -------------------------
+    @property
+    def basis(self):
+        return self.eng.block(self.nbasis)
+
+    @property
+    def h(self):
+        rows = min(self.hcols + 1, self.nbasis)
+        return self._h[:rows, : self.hcols]
+
+    @property
+    def h_extended(self):
+        return self._h[: self.hcols + 1, : self.hcols]
+
+    @property
+    def basis_extended(self):
+        return self.eng.block(self.hcols + 1)
+
+    @property
+    def size(self):
+        return self.nbasis + (1 if self._has_pending() else 0)
+
+    @property
+    def order(self):
+        return self.size if self.happy else self.size - 1
+
+    def _has_pending(self):
+        return False
+
+    # -- contract -----------------------------------------------------------------
+    def step(self):
+        """Grow by one column; False once a happy breakdown has been hit."""
+        if self.happy:
+            return False
+        if self.size >= self.capacity:
+            raise DimensionError("expansion capacity exhausted")
+        return self._step()
+
+    def finalize(self):
+        """Flush pending work; returns (V, Hbar).
+
+        V is an (m_local, nbasis) column-major view of the device basis (not a
+        copy: at m = 1e8 a copy would double a 100 GB footprint; basis columns
+        are append-only, so the view stays valid).  Hbar is a host copy.
+        """
+        self._flush()
+        return self.eng.block(self.nbasis), self._h[: self.nbasis, : self.hcols].copy()
+
+    def _step(self):
+        raise NotImplementedError
+
+    def _flush(self):
+        pass
+
+    def _mark_happy(self):
+        self.happy = True
+        return False
+
+    def _load_basis(self, basis, ncols):
+        e = self.eng
+        e.check_capacity(ncols)
+        if isinstance(basis, torch.Tensor) and basis.is_cuda:
+            if basis.shape != (e.ml, ncols):
+                raise DimensionError(f"basis of shape ({e.ml}, {ncols}) expected")
+            e.vbuf[:ncols, : e.ml].copy_(basis.T)
+        else:
+            b = np.asarray(basis, dtype=np.float64)
+            lo, hi = self.op.row_lo, self.op.row_hi
+            if b.shape[0] == self.m and (hi - lo) != self.m:
+                b = b[lo:hi]
+            e.vbuf[:ncols, : e.ml].copy_(torch.from_numpy(np.ascontiguousarray(b.T)))
+
+    # -- ledger helpers (global m, reference flop formulas) -------------------------
+    def _rec(self, cls, flops):
+        self.ledger.record(cls, flops=flops)
+
+
+class _DelayedArnoldi(_BaseArnoldi):
+    """One-reduction delayed reorthogonalization (dcgs2)."""
+
+    scheme_id = "dcgs2"
+
+    def __init__(self, op, start, capacity, ledger=None):
+        super().__init__(op, capacity, ledger)
+        e = self.eng
+        self._w = op.new_vector()  # pending vector, with halo space
+        self._aw = torch.zeros(e.ld, dtype=torch.float64, device=e.vbuf.device)[: e.ml]
+        self._pending = False
+        self._wscale = 0.0
+        self._k = None
+        if start is not None:
+            self._w.local.copy_(op.take(start, "start vector"))
+            nrm = float(np.sqrt(e.sqnorm(self._w.local)))  # local norm, not counted
+            if not nrm > 0.0:
+                raise ValueError("zero start vector")
+            op.napply += 1
+            e.apply(self._w, self._aw)
+            self._pending = True
+            self._wscale = nrm
+
+    @classmethod
+    def resume(cls, op, basis, hbar, capacity, ledger=None):
+        self = cls(op, None, capacity, ledger)
+        k = hbar.shape[1]
+        self._load_basis(basis, k + 1)
+        self._h[: k + 1, :k] = hbar
+        self.nbasis = k + 1
+        self.hcols = k
+        return self
+
+    def _has_pending(self):
+        return self._pending
+
+    def _step(self):
+        e = self.eng
+        m = self.m
+        if not self._pending:
+            # resumed without pending work: prime from the image of the last
+            # (normalized) basis column (arnoldi.py:350-361)
+            j = self.nbasis
+            w = self._w
+            self.op.napply += 1
+            e.apply(e.col(j - 1), w.local)
+            r = e.project(j, w.local, xnorm=True)  # s = Q^T v, plus ||v||^2 (local)
+            s, vnorm2 = r[:j].copy(), float(r[j])
+            self._rec(_ledger.MV_TRANS_MV, 2 * m * j)
+            e.subtract_projection(w.local, j, s)
+            self._rec(_ledger.MV_TIMES_MAT_ADD_MV, 2 * m * j)
+            self._k = s
+            self.op.napply += 1
+            e.apply(w, self._aw)
+            self._pending = True
+            self._wscale = float(np.sqrt(vnorm2))
+            return True
+
+        j = self.nbasis
+        g = e.gram_dcgs2(j, self._w.local, self._aw)
+        self._rec(_ledger.MV_TRANS_MV, 2 * m * (j + 1) * 2)
+        c = g[:j].copy()
+        beta = float(g[j])
+        s = g[j + 1 : 2 * j + 1].copy()
+        s_piv = float(g[2 * j + 1])
+        aw_norm = float(np.sqrt(g[2 * j + 2]))
+        if not np.sqrt(max(beta, 0.0)) > _EPS * np.sqrt(m) * self._wscale:
+            # the pending direction vanished: invariant subspace
+            if j > 0:
+                self._h[:j, j - 1] = self._k + c
+                self._h[j, j - 1] = 0.0
+                self.hcols = j
+            self._pending = False
+            return self._mark_happy()
+        alpha_sq = beta - float(c @ c)
+        self.ledger.add_flops(2 * j)
+        if not alpha_sq > beta * _EPS * _EPS:
+            raise BreakdownError(
+                f"cancellation in the delayed norm of basis column {j}",
+                kind="pythagorean", column=j)
+        alpha = float(np.sqrt(alpha_sq))
+        self._rec(_ledger.MV_TIMES_MAT_ADD_MV, 2 * m * j)  # u = w - Q c
+        t_piv = (s_piv - float(c @ s)) / (alpha * alpha)
+        self.ledger.add_flops(2 * j)
+        if self.start_norm is None:
+            self.start_norm = alpha
+        t_full = np.append(s / alpha, t_piv)
+        if j > 0:
+            self._h[:j, j - 1] = self._k + c
+            self._h[j, j - 1] = alpha
+            self.hcols = j
+        hc = self._h[: j + 1, :j] @ c
+        self.ledger.add_flops(2 * (j + 1) * j)
+        self._k = t_full - hc / alpha
+        vscale = aw_norm / alpha  # pre-projection norm, arnoldi.py:414
+        self.ledger.add_flops(m)
+        self._rec(_ledger.MV_TIMES_MAT_ADD_MV, 2 * m * (j + 1))  # w' = aw/alpha - V t
+        # one pass: Q(:, j) = (w - Q c)/alpha; w = aw/alpha - Q t - q_j t_j
+        e.dcgs2_update(j, self._w.local, self._aw, c, t_full, alpha, divide=True)
+        self.nbasis += 1
+        self.op.napply += 1
+        e.apply(self._w, self._aw)
+        self._wscale = vscale
+        return True
+
+    def _flush(self):
+        """CGS2 pass on the pending vector (arnoldi.py:425-455): 2 reductions."""
+        if not self._pending:
+            return
+        e = self.eng
+        m = self.m
+        j = self.nbasis
+        w = self._w.local
+        c = e.project(j, w, xnorm=False) if j else np.zeros(0)
+        self._rec(_ledger.MV_TRANS_MV, 2 * m * j)
+        nrm2 = e.subtract_projection(w, j, c, want_norm=True)  # u = w - Q c, ||u||^2
+        self._rec(_ledger.MV_TIMES_MAT_ADD_MV, 2 * m * j)
+        self._rec(_ledger.MV_DOT, 2 * m)
+        alpha = float(np.sqrt(nrm2))
+        if not alpha > _EPS * np.sqrt(m) * self._wscale:
+            if j > 0:
+                self._h[:j, j - 1] = self._k + c
+                self._h[j, j - 1] = 0.0
+                self.hcols = j
+            self._pending = False
+            self._mark_happy()
+            return
+        if self.start_norm is None:
+            self.start_norm = alpha
+        if j > 0:
+            self._h[:j, j - 1] = self._k + c
+            self._h[j, j - 1] = alpha
+            self.hcols = j
+        e.divide_into(e.col(j), w, alpha)
+        self.nbasis += 1
+        self._pending = False
+
+
+class _ImmediateArnoldi(_BaseArnoldi):
+    """CGS2 expansion: each column finished within its step (3 reductions)."""
+
+    scheme_id = "cgs2"
+
+    def __init__(self, op, start, capacity, ledger=None):
+        super().__init__(op, capacity, ledger)
+        e = self.eng
+        self._v = torch.zeros(e.ld, dtype=torch.float64, device=e.vbuf.device)[: e.ml]
+        self.last_coeffs = None
+        self.last_alpha = None
+        if start is not None:
+            x = op.take(start, "start vector")
+            nrm = float(np.sqrt(e.sqnorm(x)))  # local normalization, not counted
+            if not nrm > 0.0:
+                raise ValueError("zero start vector")
+            self.start_norm = nrm
+            e.divide_into(e.col(0), x, nrm)
+            self.nbasis = 1
+
+    @classmethod
+    def resume(cls, op, basis, hbar, capacity, ledger=None):
+        self = cls(op, None, capacity, ledger)
+        k = hbar.shape[1]
+        self._load_basis(basis, k + 1)
+        self._h[: k + 1, :k] = hbar
+        self.nbasis = k + 1
+        self.hcols = k
+        return self
+
+    def _cgs2_push(self, v, j):
+        """Cgs2State.push (ortho.py:144-158) of the device column v against
+        Q(:, 0:j); returns (coeffs, alpha) and leaves u = v - Q(s+c) in v."""
+        e = self.eng
+        m = self.m
+        r = e.project(j, v, xnorm=True)  # s = Q^T a and the local scale ||a||^2
+        s, scale2 = r[:j].copy(), float(r[j])
+        if not np.isfinite(scale2):
+            raise ValueError("non-finite column")
+        scale = float(np.sqrt(scale2))
+        self._rec(_ledger.MV_TRANS_MV, 2 * m * j)
+        e.subtract_projection(v, j, s)
+        self._rec(_ledger.MV_TIMES_MAT_ADD_MV, 2 * m * j)
+        c = e.project(j, v, xnorm=False) if j else np.zeros(0)
+        self._rec(_ledger.MV_TRANS_MV, 2 * m * j)
+        nrm2 = e.subtract_projection(v, j, c, want_norm=True)
+        self._rec(_ledger.MV_TIMES_MAT_ADD_MV, 2 * m * j)
+        self._rec(_ledger.MV_DOT, 2 * m)
+        alpha = float(np.sqrt(nrm2))
+        self.last_coeffs, self.last_alpha = s + c, alpha
+        if not alpha > _EPS * np.sqrt(m) * scale:
+            raise BreakdownError(
+                f"column {j} is dependent at working precision "
+                f"(norm {alpha:.3e} against scale {scale:.3e})",
+                kind="dependent", column=j)
+        return s + c, alpha
+
+    def _step(self):
+        e = self.eng
+        j = self.nbasis
+        self.op.napply += 1
+        e.apply(e.col(j - 1), self._v)
+        try:
+            coeffs, alpha = self._cgs2_push(self._v, j)
+        except BreakdownError as err:
+            if err.kind != "dependent":
+                raise
+            coeffs = self.last_coeffs
+            self._h[: len(coeffs), j - 1] = coeffs
+            self._h[j, j - 1] = 0.0
+            self.hcols = j
+            return self._mark_happy()
+        self._h[: len(coeffs), j - 1] = coeffs
+        self._h[j, j - 1] = alpha
+        e.divide_into(e.col(j), self._v, alpha)
+        self.nbasis += 1
+        self.hcols = j
+        return True
+
+
+def arnoldi(op, start, scheme, capacity, ledger=None, **options):
+    """Construct an expansion for a scheme id from a start vector
+    (arnoldi.py:561-573)."""
+    if options:
+        raise TypeError(f"unexpected options {sorted(options)}")
+    if scheme == "dcgs2":
+        return _DelayedArnoldi(op, start, capacity, ledger)
+    if scheme == "cgs2":
+        return _ImmediateArnoldi(op, start, capacity, ledger)
+    raise _unsupported(scheme)
+
+
+def resume_arnoldi(op, basis, hbar, scheme, capacity, ledger=None, **options):
+    """Continue from A V_k = V_{k+1} Hbar (arnoldi.py:576-600); the coupling
+    row of hbar may be dense (Krylov-Schur form)."""
+    if options:
+        raise TypeError(f"unexpected options {sorted(options)}")
+    hbar = np.asarray(hbar, dtype=np.float64)
+    ncols = basis.shape[1]
+    if ncols != hbar.shape[0] or hbar.shape[0] != hbar.shape[1] + 1:
+        raise DimensionError(
+            f"expected (m, k+1) basis with (k+1, k) hbar, got {tuple(basis.shape)} {hbar.shape}")
+    if scheme == "dcgs2":
+        return _DelayedArnoldi.resume(op, basis, hbar, capacity, ledger)
+    if scheme == "cgs2":
+        return _ImmediateArnoldi.resume(op, basis, hbar, capacity, ledger)
+    raise _unsupported(scheme)
+
+
+def arnoldi_expand(op, start, scheme, steps, ledger=None, **options):
+    """Fixed-order expansion; returns (V, Hbar) (arnoldi.py:603-609)."""
+    exp = arnoldi(op, start, scheme, capacity=steps + 1, ledger=ledger, **options)
+    while exp.order < steps:
+        if not exp.step():
+            break
+    return exp.finalize()

@@ -1,0 +1,282 @@
+// K2: projection updates (the reference's MvTimesMatAddMv, kernels.py:63-84).
+//
+// kls_dcgs2_update fuses the two MvTimesMatAddMv calls of a DCGS2 Arnoldi
+// step (arnoldi.py:389-391 and :415-420; QR form ortho.py:396-398, 371-375)
+// into one streaming pass over Q(:, 0:j):
+//     u     = w - Q c             (delayed reorthogonalisation)
+//     q_j   = u / alpha           (lagged normalisation)   -> Q(:, j)
+//     w'    = aw / alpha - (Q t(0:j) + q_j t_j)            -> w (in place)
+// HBM traffic 8 m (j + 4): Q once, w, aw, and the two writes.
+//
+// kls_mv_times_mat_add_mv is the generic Y <- scale Y + sign B S for one or
+// two right-hand columns, optionally returning ||Y(:, l-1)||^2 of the result
+// (fused norm for the CGS2 comparator and the DCGS2 flush).
+#include "reduce.cuh"
+
+namespace {
+
+using namespace kls;
+
+constexpr int kCols = 4;        // Q columns streamed together
+constexpr int kUpdRP = 2;       // row pairs per lane per chunk
+constexpr int kUpdBlocksPerSm = 3;
+
+struct UpdParams {
+  double* Q;
+  int64_t ldq;
+  int64_t m;
+  int32_t j;
+  double* w;
+  const double* aw;
+  const double* coef;  // c[0:j], t[0:j+1]
+  double alpha;
+  int32_t divide;      // aw / alpha (Arnoldi) or aw as is (QR)
+};
+
+template <int RP, bool CHECK>
+__device__ __forceinline__ void upd_chunk(const UpdParams& p, const double2* sct, double tj,
+                                          int64_t wbase, int lane) {
+  double2 ac[RP], at[RP];
+#pragma unroll
+  for (int r = 0; r < RP; ++r) {
+    ac[r] = make_double2(0.0, 0.0);
+    at[r] = make_double2(0.0, 0.0);
+  }
+  for (int k0 = 0; k0 < p.j; k0 += kCols) {
+    double2 q[kCols][RP];
+#pragma unroll
+    for (int cc = 0; cc < kCols; ++cc) {
+      if (k0 + cc < p.j) {
+        const double* col = p.Q + static_cast<int64_t>(k0 + cc) * p.ldq;
+#pragma unroll
+        for (int r = 0; r < RP; ++r) q[cc][r] = load_pair<CHECK>(col, wbase + 64 * r + 2 * lane, p.m);
+      } else {
+#pragma unroll
+        for (int r = 0; r < RP; ++r) q[cc][r] = make_double2(0.0, 0.0);
+      }
+    }
+#pragma unroll
+    for (int cc = 0; cc < kCols; ++cc) {
+      const double2 ct = sct[k0 + cc];  // zero-padded past j
+#pragma unroll
+      for (int r = 0; r < RP; ++r) {
+        ac[r].x = fma(q[cc][r].x, ct.x, ac[r].x);
+        ac[r].y = fma(q[cc][r].y, ct.x, ac[r].y);
+        at[r].x = fma(q[cc][r].x, ct.y, at[r].x);
+        at[r].y = fma(q[cc][r].y, ct.y, at[r].y);
+      }
+    }
+  }
+  double* qout = p.Q + static_cast<int64_t>(p.j) * p.ldq;
+#pragma unroll
+  for (int r = 0; r < RP; ++r) {
+    const int64_t row = wbase + 64 * r + 2 * lane;
+    const double2 w = load_pair_rw<CHECK>(p.w, row, p.m);
+    const double2 a = load_pair<CHECK>(p.aw, row, p.m);
+    double2 qn, wn;
+    qn.x = (w.x - ac[r].x) / p.alpha;
+    qn.y = (w.y - ac[r].y) / p.alpha;
+    const double ax = p.divide ? a.x / p.alpha : a.x;
+    const double ay = p.divide ? a.y / p.alpha : a.y;
+    wn.x = ax - fma(qn.x, tj, at[r].x);
+    wn.y = ay - fma(qn.y, tj, at[r].y);
+    store_pair<CHECK>(qout, row, p.m, qn);
+    store_pair<CHECK>(p.w, row, p.m, wn);
+  }
+}
+
+template <int RP>
+__global__ void __launch_bounds__(kThreads, kUpdBlocksPerSm) dcgs2_update_kernel(UpdParams p) {
+  extern __shared__ double2 sct[];  // (c_k, t_k), padded to a multiple of kCols
+  const int jpad = (p.j + kCols - 1) / kCols * kCols;
+  for (int k = threadIdx.x; k < jpad; k += kThreads)
+    sct[k] = k < p.j ? make_double2(p.coef[k], p.coef[p.j + k]) : make_double2(0.0, 0.0);
+  const double tj = p.coef[2 * p.j];
+  __syncthreads();
+  constexpr int64_t WROWS = 64 * RP;
+  constexpr int64_t CROWS = WROWS * kWarps;
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t nchunks = (p.m + CROWS - 1) / CROWS;
+  for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+    const int64_t cbase = ch * CROWS;
+    const int64_t wbase = cbase + warp * WROWS;
+    if (cbase + CROWS <= p.m)
+      upd_chunk<RP, false>(p, sct, tj, wbase, lane);
+    else
+      upd_chunk<RP, true>(p, sct, tj, wbase, lane);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// generic Y <- scale * Y + sign * B S   (l = 1 or 2 columns of Y)
+
+struct MtmParams {
+  double* Y;
+  int64_t ldy;
+  int64_t m;
+  int32_t l;
+  const double* B;
+  int64_t ldb;
+  int32_t k;
+  const double* S;  // k x l column-major, ld = k
+  double sign;
+  double scale;
+  RedWs ws;
+  double* nrm_out;  // ||Y(:, l-1)||^2 after the update, or nullptr
+};
+
+template <int L, bool CHECK>
+__device__ __forceinline__ void mtm_chunk(const MtmParams& p, const double* ss, int64_t wbase,
+                                          int lane, double& nrm) {
+  constexpr int RP = kUpdRP;
+  double2 acc[L][RP];
+#pragma unroll
+  for (int t = 0; t < L; ++t)
+#pragma unroll
+    for (int r = 0; r < RP; ++r) acc[t][r] = make_double2(0.0, 0.0);
+  for (int k0 = 0; k0 < p.k; k0 += kCols) {
+    double2 q[kCols][RP];
+#pragma unroll
+    for (int cc = 0; cc < kCols; ++cc) {
+      if (k0 + cc < p.k) {
+        const double* col = p.B + static_cast<int64_t>(k0 + cc) * p.ldb;
+#pragma unroll
+        for (int r = 0; r < RP; ++r) q[cc][r] = load_pair<CHECK>(col, wbase + 64 * r + 2 * lane, p.m);
+      } else {
+#pragma unroll
+        for (int r = 0; r < RP; ++r) q[cc][r] = make_double2(0.0, 0.0);
+      }
+    }
+#pragma unroll
+    for (int cc = 0; cc < kCols; ++cc)
+#pragma unroll
+      for (int t = 0; t < L; ++t) {
+        const double s = ss[t * (p.k + kCols) + k0 + cc];
+#pragma unroll
+        for (int r = 0; r < RP; ++r) {
+          acc[t][r].x = fma(q[cc][r].x, s, acc[t][r].x);
+          acc[t][r].y = fma(q[cc][r].y, s, acc[t][r].y);
+        }
+      }
+  }
+#pragma unroll
+  for (int t = 0; t < L; ++t) {
+    double* ycol = p.Y + static_cast<int64_t>(t) * p.ldy;
+#pragma unroll
+    for (int r = 0; r < RP; ++r) {
+      const int64_t row = wbase + 64 * r + 2 * lane;
+      double2 y = load_pair_rw<CHECK>(ycol, row, p.m);
+      if (p.scale != 1.0) {
+        y.x *= p.scale;
+        y.y *= p.scale;
+      }
+      if (p.k > 0) {
+        y.x += p.sign * acc[t][r].x;
+        y.y += p.sign * acc[t][r].y;
+      }
+      store_pair<CHECK>(ycol, row, p.m, y);
+      if (t == L - 1) {
+        nrm = fma(y.x, y.x, nrm);
+        nrm = fma(y.y, y.y, nrm);
+      }
+    }
+  }
+}
+
+template <int L>
+__global__ void __launch_bounds__(kThreads, kUpdBlocksPerSm) mtm_kernel(MtmParams p) {
+  extern __shared__ double ss[];  // L x (k + kCols), zero-padded
+  const int ldss = p.k + kCols;
+  for (int i = threadIdx.x; i < L * ldss; i += kThreads) {
+    const int t = i / ldss, kk = i % ldss;
+    ss[i] = kk < p.k ? p.S[t * p.k + kk] : 0.0;
+  }
+  __syncthreads();
+  constexpr int64_t WROWS = 64 * kUpdRP;
+  constexpr int64_t CROWS = WROWS * kWarps;
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  double nrm = 0.0;
+  const int64_t nchunks = (p.m + CROWS - 1) / CROWS;
+  for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+    const int64_t cbase = ch * CROWS;
+    const int64_t wbase = cbase + warp * WROWS;
+    if (cbase + CROWS <= p.m)
+      mtm_chunk<L, false>(p, ss, wbase, lane, nrm);
+    else
+      mtm_chunk<L, true>(p, ss, wbase, lane, nrm);
+  }
+  if (p.nrm_out != nullptr) {
+    double v[1] = {nrm};
+    grid_reduce_finish<1>(v, p.ws, p.nrm_out);
+  }
+}
+
+int grid_for(int64_t m, int64_t crows, int per_sm) {
+  const int64_t nchunks = ceil_div(m, crows);
+  int grid = static_cast<int>(std::min<int64_t>(nchunks, (int64_t)per_sm * sm_count()));
+  return grid < 1 ? 1 : grid;
+}
+
+int set_smem(const void* fn, size_t smem) {
+  if (smem <= 48 * 1024) return KLS_OK;
+  if (smem > 227 * 1024) return fail(KLS_EINVAL, "shared memory request %zu too large", smem);
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return fail(KLS_ECUDA, "smem attribute: %s", cudaGetErrorString(e));
+  return KLS_OK;
+}
+
+bool misaligned(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) != 0; }
+
+}  // namespace
+
+// Fused DCGS2 step update (see the file header).  `coef` is a device array
+// [c(0:j), t(0:j+1)] of 2j+1 doubles; column j of Q receives q_j; w is
+// overwritten by the next pending vector.  divide != 0 gives the Arnoldi form
+// w' = aw/alpha - ...; divide == 0 the QR form w' = a - ....
+KLS_API int kls_dcgs2_update(double* Q, int64_t ldq, int64_t m, int32_t j, double* w,
+                             const double* aw, const double* coef, double alpha, int32_t divide,
+                             void* stream) {
+  if (Q == nullptr || w == nullptr || aw == nullptr || coef == nullptr || m < 0 || j < 0 ||
+      ldq < m || (ldq & 1))
+    return fail(KLS_EINVAL, "dcgs2_update: bad arguments");
+  if (misaligned(Q) || misaligned(w) || misaligned(aw))
+    return fail(KLS_EINVAL, "dcgs2_update: operands must be 16-byte aligned");
+  const size_t smem = sizeof(double2) * static_cast<size_t>((j + kCols - 1) / kCols * kCols + 1);
+  int rc = set_smem(reinterpret_cast<const void*>(dcgs2_update_kernel<kUpdRP>), smem);
+  if (rc) return rc;
+  UpdParams p{Q, ldq, m, j, w, aw, coef, alpha, divide};
+  const int grid = grid_for(m, 64 * kUpdRP * kWarps, kUpdBlocksPerSm);
+  dcgs2_update_kernel<kUpdRP><<<grid, kThreads, smem, static_cast<cudaStream_t>(stream)>>>(p);
+  return check_launch("dcgs2_update_kernel");
+}
+
+// Y(:, 0:l) <- scale * Y + sign * B(:, 0:k) S  with S (k x l, column-major,
+// device).  When nrm_out != NULL it receives ||Y(:, l-1)||^2 of the result
+// (requires ws).  Mirrors kernels.mv_times_mat_add_mv (kernels.py:63-84).
+KLS_API int kls_mv_times_mat_add_mv(double* Y, int64_t ldy, int64_t m, int32_t l, const double* B,
+                                    int64_t ldb, int32_t k, const double* S, double sign,
+                                    double scale, double* nrm_out, void* ws, size_t ws_bytes,
+                                    void* stream) {
+  if (Y == nullptr || m < 0 || k < 0 || (l != 1 && l != 2) || (l == 2 && (ldy < m || (ldy & 1))) ||
+      (k > 0 && (B == nullptr || S == nullptr || ldb < m || (ldb & 1))))
+    return fail(KLS_EINVAL, "mv_times_mat_add_mv: bad arguments (m=%lld k=%d l=%d)",
+                (long long)m, k, l);
+  if (misaligned(Y) || misaligned(B)) return fail(KLS_EINVAL, "mv_times_mat_add_mv: misaligned");
+  const int grid = grid_for(m, 64 * kUpdRP * kWarps, kUpdBlocksPerSm);
+  MtmParams p{Y, ldy, m, l, B, ldb, k, S, sign, scale, red_ws(ws), nrm_out};
+  if (nrm_out != nullptr && (ws == nullptr || !red_ws_fits(ws_bytes, grid, 1)))
+    return fail(KLS_ENOSPC, "mv_times_mat_add_mv: workspace too small for the fused norm");
+  const size_t smem = sizeof(double) * static_cast<size_t>(l) * (k + kCols);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int rc;
+  if (l == 1) {
+    if ((rc = set_smem(reinterpret_cast<const void*>(mtm_kernel<1>), smem))) return rc;
+    mtm_kernel<1><<<grid, kThreads, smem, st>>>(p);
+  } else {
+    if ((rc = set_smem(reinterpret_cast<const void*>(mtm_kernel<2>), smem))) return rc;
+    mtm_kernel<2><<<grid, kThreads, smem, st>>>(p);
+  }
+  return check_launch("mtm_kernel");
+}

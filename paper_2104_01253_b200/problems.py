@@ -1,0 +1,679 @@
+"""Operators with device-resident data, plus the host-side generators that
+build the reference's test problems (reference problems.py).
+
+Operators follow the reference's LinearOperator protocol (problems.py:12-65):
+``shape``, ``apply(x)`` (validates, counts ``napply``), ``frobenius_norm()``,
+``to_dense()``.  ``apply`` takes a device tensor holding this rank's rows (or
+a host array of the global length, which is sliced and uploaded) and returns
+a device tensor.  Rows are block-partitioned over the ranks of the active
+communicator; ``apply`` exchanges the halo rows a stencil/CSR row needs from
+neighbouring ranks before launching the kernel.
+
+Generators (CsrMatrix.from_coo, manteuffel_build, laplace3d, ...) run on the
+host with numpy and produce exactly the reference's CSR arrays (same entry
+order, same summed values), so device SpMV results are bit-identical.
+"""
+
+import io
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib, runtime
+from .errors import DimensionError, MatrixMarketError
+
+# ---------------------------------------------------------------------------
+# device vectors with halo space
+
+
+class HaloVector:
+    """A rank's rows of a vector plus storage for the halo rows an operator
+    reads from its neighbours.
+
+    ``local`` is the (aligned) view of the owned rows; ``ext`` is the base the
+    CSR column indices address; ``lo``/``hi`` are the halo views (or None).
+    """
+
+    def __init__(self, n_local, lo_rows=0, hi_rows=0, contiguous=True):
+        dev = runtime.device()
+        self.n_local = n_local
+        if contiguous:
+            # [pad | lo halo | local | hi halo] with local 256-byte aligned
+            pad = (-lo_rows) % runtime.ALIGN
+            total = pad + lo_rows + n_local + hi_rows
+            self.buf = torch.zeros(max(total, 2), dtype=torch.float64, device=dev)
+            self.ext_offset = pad
+            start = pad + lo_rows
+            self.local = self.buf[start : start + n_local]
+            self.lo = self.buf[pad : pad + lo_rows] if lo_rows else None
+            self.hi = self.buf[start + n_local : start + n_local + hi_rows] if hi_rows else None
+        else:
+            # [local (padded) | lo plane | hi plane]: halos by separate pointer
+            ld = runtime.pad_rows(n_local)
+            self.buf = torch.zeros(ld + lo_rows + hi_rows, dtype=torch.float64, device=dev)
+            self.ext_offset = 0
+            self.local = self.buf[:n_local]
+            self.lo = self.buf[ld : ld + lo_rows] if lo_rows else None
+            self.hi = self.buf[ld + lo_rows : ld + lo_rows + hi_rows] if hi_rows else None
+
+    @property
+    def ext_ptr(self):
+        return self.buf.data_ptr() + 8 * self.ext_offset
+
+
+# ---------------------------------------------------------------------------
+# operator protocol
+
+
+class LinearOperator:
+    """Square operator y = A x; subclasses implement ``_launch``.
+
+    ``napply`` counts applications through ``apply`` (one per matvec), which
+    the Arnoldi instrumentation asserts against (problems.py:12-33).
+    """
+
+    def __init__(self, n, comm=None):
+        self.n = int(n)
+        self.napply = 0
+        self._fro = None
+        self.comm = comm if comm is not None else runtime.comm()
+        self._scratch = None
+        self._partition()
+
+    # -- partition ----------------------------------------------------------
+    def _partition(self):
+        self.row_lo, self.row_hi = self.comm.split(self.n)
+
+    @property
+    def m_local(self):
+        return self.row_hi - self.row_lo
+
+    @property
+    def shape(self):
+        return (self.n, self.n)
+
+    # -- vectors ------------------------------------------------------------
+    def new_vector(self):
+        """A zeroed HaloVector laid out for this operator's kernel."""
+        return HaloVector(self.m_local)
+
+    def take(self, x, name="operand"):
+        """Validate an operand and return this rank's rows on the device."""
+        if isinstance(x, torch.Tensor) and x.is_cuda:
+            if x.dim() != 1 or x.numel() != self.m_local:
+                raise DimensionError(
+                    f"{name} of local length {self.m_local} expected, got {tuple(x.shape)}"
+                )
+            return x if x.dtype == torch.float64 else x.double()
+        a = np.asarray(x.cpu().numpy() if isinstance(x, torch.Tensor) else x, dtype=np.float64)
+        if a.shape != (self.n,):
+            raise DimensionError(f"{name} of length {self.n} expected, got {a.shape}")
+        return runtime.upload(a[self.row_lo : self.row_hi])
+
+    # -- application ----------------------------------------------------------
+    def apply(self, x):
+        """y = A x as a new device tensor (counts one application)."""
+        xl = self.take(x)
+        self.napply += 1
+        y = torch.empty(self.m_local, dtype=torch.float64, device=xl.device)
+        self.apply_into(xl, y)
+        return y
+
+    def apply_into(self, x, y):
+        """Uncounted y = A x.  ``x`` is a HaloVector (no copy) or a device
+        tensor of the local rows (copied into scratch halo storage when the
+        operator needs neighbour rows)."""
+        if not isinstance(x, HaloVector):
+            if self._needs_halo():
+                if self._scratch is None:
+                    self._scratch = self.new_vector()
+                self._scratch.local.copy_(x)
+                x = self._scratch
+            else:
+                x = _PlainVector(x)
+        self._exchange(x)
+        self._launch(x, y)
+
+    def _needs_halo(self):
+        return False
+
+    def _exchange(self, x):
+        pass
+
+    def _launch(self, x, y):
+        raise NotImplementedError
+
+    # -- norms / dense ------------------------------------------------------
+    def to_dense(self, max_order=4000):
+        if self.n > max_order:
+            raise MemoryError(f"dense assembly of order {self.n} refused (limit {max_order})")
+        if self.comm.world != 1:
+            raise NotImplementedError("to_dense on a row-sharded operator")
+        out = np.empty((self.n, self.n), order="F")
+        e = torch.zeros(self.n, dtype=torch.float64, device=runtime.device())
+        y = torch.empty_like(e)
+        for j in range(self.n):
+            e[j] = 1.0
+            self.apply_into(e, y)
+            out[:, j] = y.cpu().numpy()
+            e[j] = 0.0
+        return out
+
+    def frobenius_norm(self, samples=64, seed=0):
+        """Estimated once by probing sampled columns (problems.py:51-65)."""
+        if self._fro is None:
+            if self.comm.world != 1:
+                raise NotImplementedError("probed Frobenius norm on a row-sharded operator")
+            t = min(samples, self.n)
+            rng = np.random.Generator(np.random.PCG64(seed))
+            cols = rng.choice(self.n, size=t, replace=False)
+            e = torch.zeros(self.n, dtype=torch.float64, device=runtime.device())
+            y = torch.empty_like(e)
+            acc = 0.0
+            for j in cols:
+                e[j] = 1.0
+                self.apply_into(e, y)
+                acc += float(torch.dot(y, y))
+                e[j] = 0.0
+            self._fro = float(np.sqrt(acc * self.n / t))
+        return self._fro
+
+
+class _PlainVector:
+    """Adapter: a local tensor viewed as a halo-free HaloVector."""
+
+    def __init__(self, t):
+        self.local = t
+        self.lo = self.hi = None
+        self.buf = t
+        self.ext_offset = 0
+
+    @property
+    def ext_ptr(self):
+        return self.local.data_ptr()
+
+
+def _p2p(ops):
+    import torch.distributed as dist
+
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+
+
+class DenseOperator(LinearOperator):
+    """Small dense operator (problems.py:68-85), single rank."""
+
+    def __init__(self, a, comm=None):
+        a = np.asarray(a, dtype=np.float64)
+        if a.ndim != 2 or a.shape[0] != a.shape[1]:
+            raise DimensionError(f"square matrix expected, got {a.shape}")
+        super().__init__(a.shape[0], comm)
+        if self.comm.world != 1:
+            raise NotImplementedError("DenseOperator is single-rank")
+        self.a = a
+        self._dev = runtime.upload(np.ascontiguousarray(a))
+
+    def _launch(self, x, y):
+        _lib.call("kls_dense_gemv", self._dev.data_ptr(), self.n, self.n, x.local.data_ptr(),
+                  y.data_ptr(), runtime.stream_handle())
+
+    def to_dense(self, max_order=None):
+        return self.a.copy()
+
+    def frobenius_norm(self, samples=None, seed=None):
+        if self._fro is None:
+            self._fro = float(np.linalg.norm(self.a))
+        return self._fro
+
+
+# ---------------------------------------------------------------------------
+# CSR storage (host) and the device CSR operator
+
+
+@dataclass
+class CsrMatrix:
+    """Host CSR with sorted, unique column indices per row (problems.py:88-151).
+
+    A data container: products run on the device through CsrOperator.
+    """
+
+    nrows: int
+    ncols: int
+    indptr: np.ndarray
+    indices: np.ndarray
+    data: np.ndarray
+
+    @classmethod
+    def from_coo(cls, nrows, ncols, rows, cols, vals):
+        """Build from triplets, summing duplicates in (row, col) order."""
+        rows = np.asarray(rows, dtype=np.int64)
+        cols = np.asarray(cols, dtype=np.int64)
+        vals = np.asarray(vals, dtype=np.float64)
+        perm = np.lexsort((cols, rows))  # stable: equal keys keep input order
+        rows, cols, vals = rows[perm], cols[perm], vals[perm]
+        if rows.size:
+            first = np.ones(rows.size, dtype=bool)
+            first[1:] = (rows[1:] != rows[:-1]) | (cols[1:] != cols[:-1])
+            slot = np.cumsum(first) - 1
+            summed = np.zeros(int(slot[-1]) + 1)
+            np.add.at(summed, slot, vals)  # sequential in input order
+            rows, cols, vals = rows[first], cols[first], summed
+        counts = np.bincount(rows, minlength=nrows) if rows.size else np.zeros(nrows, np.int64)
+        indptr = np.zeros(nrows + 1, dtype=np.int64)
+        np.cumsum(counts, out=indptr[1:])
+        return cls(nrows, ncols, indptr, cols, vals)
+
+    @property
+    def nnz(self):
+        return int(self.indices.size)
+
+    @property
+    def shape(self):
+        return (self.nrows, self.ncols)
+
+    def row_ids(self):
+        return np.repeat(np.arange(self.nrows), np.diff(self.indptr))
+
+    def transpose(self):
+        return CsrMatrix.from_coo(self.ncols, self.nrows, self.indices, self.row_ids(), self.data)
+
+    def to_dense(self):
+        out = np.zeros((self.nrows, self.ncols))
+        out[self.row_ids(), self.indices] = self.data
+        return out
+
+    def frobenius_norm(self):
+        return float(np.linalg.norm(self.data))
+
+
+class CsrOperator(LinearOperator):
+    """Device-resident CSR operator (problems.py:154-174).
+
+    Each rank uploads its row block; column indices are remapped onto the
+    rank's extended vector [lo halo | local | hi halo], where the halo window
+    spans the columns its rows touch outside the owned range.
+    """
+
+    def __init__(self, csr, comm=None):
+        if csr.nrows != csr.ncols:
+            raise DimensionError(f"square matrix expected, got {csr.shape}")
+        if csr.ncols >= 2**31:
+            raise DimensionError("column indices must fit in int32")
+        super().__init__(csr.nrows, comm)
+        self.csr = csr
+        lo, hi = self.row_lo, self.row_hi
+        s, e = int(csr.indptr[lo]), int(csr.indptr[hi])
+        cols = csr.indices[s:e]
+        cmin = int(cols.min()) if cols.size else lo
+        cmax = int(cols.max()) if cols.size else hi - 1
+        self.halo_lo = max(0, lo - min(cmin, lo))
+        self.halo_hi = max(0, max(cmax + 1, hi) - hi)
+        pad = (-self.halo_lo) % runtime.ALIGN
+        base = lo - self.halo_lo - pad  # global index of ext[0]
+        dev = runtime.device()
+        self._rowptr = torch.from_numpy(csr.indptr[lo : hi + 1] - s).to(dev)
+        self._col = torch.from_numpy((cols - base).astype(np.int32)).to(dev)
+        self._val = torch.from_numpy(np.ascontiguousarray(csr.data[s:e])).to(dev)
+        self._plan = None
+        if self.comm.world > 1:
+            self._plan = self._halo_plan()
+
+    def _needs_halo(self):
+        return self.halo_lo > 0 or self.halo_hi > 0
+
+    def new_vector(self):
+        return HaloVector(self.m_local, self.halo_lo, self.halo_hi, contiguous=True)
+
+    def _halo_plan(self):
+        """Which global row ranges each rank sends to / receives from whom."""
+        c = self.comm
+        mine = torch.tensor([self.row_lo - self.halo_lo, self.row_lo, self.row_hi,
+                             self.row_hi + self.halo_hi], dtype=torch.int64, device=runtime.device())
+        allw = [torch.empty_like(mine) for _ in range(c.world)]
+        import torch.distributed as dist
+
+        dist.all_gather(allw, mine, group=c.group)
+        win = [w.cpu().numpy() for w in allw]
+        sends, recvs = [], []
+        for q in range(c.world):
+            if q == c.rank:
+                continue
+            qlo, qhi = win[q][1], win[q][2]
+            # rows I own that q needs
+            for a, b in ((win[q][0], win[q][1]), (win[q][2], win[q][3])):
+                x0, x1 = max(a, self.row_lo), min(b, self.row_hi)
+                if x1 > x0:
+                    sends.append((q, x0 - self.row_lo, x1 - self.row_lo))
+            # rows q owns that I need
+            for a, b, side in ((self.row_lo - self.halo_lo, self.row_lo, "lo"),
+                               (self.row_hi, self.row_hi + self.halo_hi, "hi")):
+                x0, x1 = max(a, qlo), min(b, qhi)
+                if x1 > x0:
+                    off = x0 - a
+                    recvs.append((q, side, off, off + (x1 - x0)))
+        return sends, recvs
+
+    def _exchange(self, x):
+        if self._plan is None:
+            return
+        import torch.distributed as dist
+
+        sends, recvs = self._plan
+        ops = []
+        for q, a, b in sends:
+            ops.append(dist.P2POp(dist.isend, x.local[a:b], q, group=self.comm.group))
+        for q, side, a, b in recvs:
+            buf = x.lo if side == "lo" else x.hi
+            ops.append(dist.P2POp(dist.irecv, buf[a:b], q, group=self.comm.group))
+        _p2p(ops)
+
+    def _launch(self, x, y):
+        _lib.call("kls_csr_spmv", self._rowptr.data_ptr(), self._col.data_ptr(),
+                  self._val.data_ptr(), self.m_local, x.ext_ptr, y.data_ptr(),
+                  runtime.stream_handle())
+
+    def to_dense(self, max_order=4000):
+        if self.n > max_order:
+            raise MemoryError(f"dense assembly of order {self.n} refused (limit {max_order})")
+        return self.csr.to_dense()
+
+    def frobenius_norm(self, samples=None, seed=None):
+        if self._fro is None:
+            self._fro = self.csr.frobenius_norm()
+        return self._fro
+
+
+# ---------------------------------------------------------------------------
+# Manteuffel convection-diffusion (problems.py:177-284)
+
+
+@dataclass(frozen=True)
+class ManteuffelSpec:
+    """(1/h^2) M + (beta/2h) N on a k x k grid, m = k^2; defaults L = k+1,
+    h = 1."""
+
+    k: int
+    beta: float = 0.5
+    length: float = None
+
+    def __post_init__(self):
+        if self.k < 1:
+            raise ValueError("k >= 1 required")
+        if self.length is None:
+            object.__setattr__(self, "length", float(self.k + 1))
+
+    @property
+    def h(self):
+        return self.length / (self.k + 1)
+
+    @property
+    def m(self):
+        return self.k * self.k
+
+
+def _grid5(k):
+    """Row/col/kind triplets of the 5-point coupling on a k x k grid in CSR
+    order: per row r = blk*k + i, columns r-k, r-1, r, r+1, r+k when inside.
+    kind: -1 lower neighbour, 0 diagonal, +1 upper neighbour."""
+    r = np.arange(k * k, dtype=np.int64)
+    blk, i = np.divmod(r, k)
+    parts = [
+        (r - k, blk > 0, -1),
+        (r - 1, i > 0, -1),
+        (r, np.ones_like(i, dtype=bool), 0),
+        (r + 1, i < k - 1, 1),
+        (r + k, blk < k - 1, 1),
+    ]
+    cols = np.stack([p[0] for p in parts], axis=1)
+    mask = np.stack([p[1] for p in parts], axis=1)
+    kind = np.broadcast_to(np.array([p[2] for p in parts]), cols.shape)
+    counts = mask.sum(axis=1)
+    indptr = np.zeros(k * k + 1, dtype=np.int64)
+    np.cumsum(counts, out=indptr[1:])
+    return indptr, cols[mask], kind[mask]
+
+
+def manteuffel_parts(spec):
+    """Unscaled diffusion part M (4 on the diagonal, -1 off) and convection
+    part N (-1 below, +1 above), as CSR."""
+    k = spec.k
+    indptr, cols, kind = _grid5(k)
+    mm = CsrMatrix(spec.m, spec.m, indptr, cols.copy(), np.where(kind == 0, 4.0, -1.0))
+    off = kind != 0
+    rows = np.repeat(np.arange(spec.m), np.diff(indptr))[off]
+    n_ptr = np.zeros(spec.m + 1, dtype=np.int64)
+    np.cumsum(np.bincount(rows, minlength=spec.m), out=n_ptr[1:])
+    nn = CsrMatrix(spec.m, spec.m, n_ptr, cols[off].copy(), kind[off].astype(np.float64))
+    return mm, nn
+
+
+def manteuffel_build(spec):
+    """Assemble A = (1/h^2) M + (beta/2h) N as CSR.
+
+    Same entries and same rounding as the reference's from_coo of the two
+    scaled parts: off-diagonals are diff*(-1) + conv*(+-1), the diagonal is
+    diff*4 (problems.py:232-245).
+    """
+    indptr, cols, kind = _grid5(spec.k)
+    diff = 1.0 / (spec.h * spec.h)
+    conv = spec.beta / (2.0 * spec.h)
+    vals = np.where(kind == 0, diff * 4.0, diff * -1.0 + conv * kind.astype(np.float64))
+    return CsrMatrix(spec.m, spec.m, indptr, cols.astype(np.int64), vals)
+
+
+@dataclass(frozen=True)
+class EigenvalueTable:
+    """Exact spectrum with multiplicities (values sorted ascending)."""
+
+    values: np.ndarray
+    unique: np.ndarray
+    multiplicity: np.ndarray
+
+
+def manteuffel_eigenvalues(spec):
+    """Closed-form spectrum (problems.py:257-284):
+    lambda = (2/h^2) [2 - sqrt(1 - (beta h/2)^2)(cos(l pi/(k+1)) + cos(j pi/(k+1)))]."""
+    bh = spec.beta * spec.h
+    if abs(bh) > 2.0:
+        raise ValueError("beta*h <= 2 required for a real spectrum")
+    rad = np.sqrt(1.0 - (bh / 2.0) ** 2)
+    th = np.cos(np.arange(1, spec.k + 1) * np.pi / (spec.k + 1))
+    values = np.sort(((2.0 / spec.h**2) * (2.0 - rad * (th[:, None] + th[None, :]))).ravel())
+    scale = max(abs(values[0]), abs(values[-1]), 1.0)
+    unique, mult = [], []
+    for v in values:
+        if unique and abs(v - unique[-1]) <= 1e-12 * scale:
+            mult[-1] += 1
+        else:
+            unique.append(v)
+            mult.append(1)
+    return EigenvalueTable(values=values, unique=np.array(unique),
+                           multiplicity=np.array(mult, dtype=np.int64))
+
+
+# ---------------------------------------------------------------------------
+# matrix-free 3-D Laplacian (problems.py:287-344)
+
+
+class StencilLaplace3D(LinearOperator):
+    """Matrix-free 7-point Laplacian on an nx x ny x nz Dirichlet grid, x
+    slowest.  Ranks own contiguous blocks of x-planes; the neighbouring
+    planes arrive by NCCL send/recv before each application."""
+
+    def __init__(self, nx, ny, nz, comm=None):
+        if min(nx, ny, nz) < 1:
+            raise ValueError("dimensions >= 1 required")
+        self.dims = (int(nx), int(ny), int(nz))
+        super().__init__(nx * ny * nz, comm)
+
+    def _partition(self):
+        nx, ny, nz = self.dims
+        self.plane = ny * nz
+        self.x_lo, self.x_hi = self.comm.split(nx)
+        self.row_lo, self.row_hi = self.x_lo * self.plane, self.x_hi * self.plane
+
+    def _needs_halo(self):
+        return self.comm.world > 1
+
+    def new_vector(self):
+        lo = self.plane if self.x_lo > 0 else 0
+        hi = self.plane if self.x_hi < self.dims[0] else 0
+        if self.comm.world == 1:
+            lo = hi = 0
+        return HaloVector(self.m_local, lo, hi, contiguous=False)
+
+    def _exchange(self, x):
+        if self.comm.world == 1:
+            return
+        import torch.distributed as dist
+
+        P, g = self.plane, self.comm.group
+        nxl = self.x_hi - self.x_lo
+        ops = []
+        r = self.comm.rank
+        if nxl > 0:
+            if self.x_lo > 0:
+                ops.append(dist.P2POp(dist.isend, x.local[:P], r - 1, group=g))
+                ops.append(dist.P2POp(dist.irecv, x.lo, r - 1, group=g))
+            if self.x_hi < self.dims[0]:
+                ops.append(dist.P2POp(dist.isend, x.local[(nxl - 1) * P :], r + 1, group=g))
+                ops.append(dist.P2POp(dist.irecv, x.hi, r + 1, group=g))
+        _p2p(ops)
+
+    def _launch(self, x, y):
+        _, ny, nz = self.dims
+        lo = x.lo.data_ptr() if x.lo is not None else None
+        hi = x.hi.data_ptr() if x.hi is not None else None
+        _lib.call("kls_stencil7", x.local.data_ptr(), lo, hi, y.data_ptr(),
+                  self.x_hi - self.x_lo, ny, nz, runtime.stream_handle())
+
+    def to_csr(self):
+        """Host CSR with the same entries (for CSR-path runs and tests)."""
+        nx, ny, nz = self.dims
+        idx = np.arange(self.n, dtype=np.int64).reshape(self.dims)
+        rows = [idx.ravel()]
+        cols = [idx.ravel()]
+        vals = [np.full(self.n, 6.0)]
+        for axis in range(3):
+            a = np.take(idx, np.arange(self.dims[axis] - 1), axis=axis).ravel()
+            b = np.take(idx, np.arange(1, self.dims[axis]), axis=axis).ravel()
+            rows += [a, b]
+            cols += [b, a]
+            vals += [np.full(a.size, -1.0), np.full(a.size, -1.0)]
+        return CsrMatrix.from_coo(self.n, self.n, np.concatenate(rows), np.concatenate(cols),
+                                  np.concatenate(vals))
+
+    def frobenius_norm(self, samples=None, seed=None):
+        if self._fro is None:
+            nx, ny, nz = self.dims
+            edges = (nx - 1) * ny * nz + nx * (ny - 1) * nz + nx * ny * (nz - 1)
+            self._fro = float(np.sqrt(36.0 * self.n + 2.0 * edges))
+        return self._fro
+
+
+def laplace3d(nx, ny, nz, comm=None):
+    return StencilLaplace3D(nx, ny, nz, comm)
+
+
+# ---------------------------------------------------------------------------
+# Matrix Market coordinate format (problems.py:364-489)
+
+
+def _lines(source):
+    if hasattr(source, "read"):
+        return source, False
+    if isinstance(source, str) and source.lstrip().startswith("%%MatrixMarket"):
+        return io.StringIO(source), False
+    return open(source, "r", encoding="ascii"), True
+
+
+def parse_matrix_market(source):
+    """Real/integer coordinate Matrix Market -> CsrMatrix (general,
+    symmetric, skew-symmetric); errors carry the 1-based line number."""
+    f, owned = _lines(source)
+    try:
+        head = f.readline().strip().split()
+        ln = 1
+        if len(head) != 5 or head[0] != "%%MatrixMarket":
+            raise MatrixMarketError("missing %%MatrixMarket header", line=1)
+        obj, fmt, field, sym = (t.lower() for t in head[1:])
+        if obj != "matrix" or fmt != "coordinate":
+            raise MatrixMarketError(f"unsupported object/format {obj!r}/{fmt!r}", line=1)
+        if field not in ("real", "integer"):
+            raise MatrixMarketError(f"non-real field {field!r}", line=1)
+        if sym not in ("general", "symmetric", "skew-symmetric"):
+            raise MatrixMarketError(f"unsupported symmetry {sym!r}", line=1)
+        size = None
+        for raw in f:
+            ln += 1
+            t = raw.strip()
+            if not t or t.startswith("%"):
+                continue
+            toks = t.split()
+            if len(toks) != 3:
+                raise MatrixMarketError("size line needs 'rows cols nnz'", line=ln)
+            try:
+                size = tuple(int(v) for v in toks)
+            except ValueError:
+                raise MatrixMarketError("non-integer size entry", line=ln) from None
+            break
+        if size is None:
+            raise MatrixMarketError("missing size line", line=ln)
+        nr, nc, nnz = size
+        if min(size) < 0:
+            raise MatrixMarketError("negative size entry", line=ln)
+        rows = np.empty(nnz, dtype=np.int64)
+        cols = np.empty(nnz, dtype=np.int64)
+        vals = np.empty(nnz)
+        got = 0
+        for raw in f:
+            ln += 1
+            t = raw.strip()
+            if not t or t.startswith("%"):
+                continue
+            if got >= nnz:
+                raise MatrixMarketError("more entries than declared", line=ln)
+            toks = t.split()
+            if len(toks) != 3:
+                raise MatrixMarketError("entry line needs 'row col value'", line=ln)
+            try:
+                i, j, v = int(toks[0]), int(toks[1]), float(toks[2])
+            except ValueError:
+                raise MatrixMarketError("malformed entry", line=ln) from None
+            if not (1 <= i <= nr and 1 <= j <= nc):
+                raise MatrixMarketError(f"index ({i}, {j}) out of bounds for {nr}x{nc}", line=ln)
+            if sym == "skew-symmetric" and i == j and v != 0.0:
+                raise MatrixMarketError("nonzero diagonal in skew-symmetric matrix", line=ln)
+            rows[got], cols[got], vals[got] = i - 1, j - 1, v
+            got += 1
+        if got != nnz:
+            raise MatrixMarketError(f"declared {nnz} entries, found {got}", line=ln)
+    finally:
+        if owned:
+            f.close()
+    if sym != "general":
+        off = rows != cols
+        sgn = -1.0 if sym == "skew-symmetric" else 1.0
+        rows, cols, vals = (np.concatenate([rows, cols[off]]), np.concatenate([cols, rows[off]]),
+                            np.concatenate([vals, sgn * vals[off]]))
+    return CsrMatrix.from_coo(nr, nc, rows, cols, vals)
+
+
+def write_matrix_market(csr, target, symmetry="general", comment=None):
+    """Coordinate real general output of the stored entries."""
+    if symmetry != "general":
+        raise ValueError("only general output is supported")
+    own = not hasattr(target, "write")
+    f = open(target, "w", encoding="ascii") if own else target
+    try:
+        f.write("%%MatrixMarket matrix coordinate real general\n")
+        for ln in (comment.splitlines() if comment else []):
+            f.write(f"% {ln}\n")
+        f.write(f"{csr.nrows} {csr.ncols} {csr.nnz}\n")
+        for i, j, v in zip(csr.row_ids(), csr.indices, csr.data):
+            f.write(f"{i + 1} {j + 1} {float(v)!r}\n")
+    finally:
+        if own:
+            f.close()

@@ -1,0 +1,197 @@
+"""Device plumbing: device/stream selection, the row partition over ranks,
+reduction workspaces, pinned staging buffers.
+
+PyTorch is used for device memory, streams and torch.distributed (NCCL)
+only; all arithmetic on the path runs in libklsgpu.so.
+
+Row partition: every distributed object (operator, vector,
+basis block) is split into contiguous row blocks, one per rank, in rank
+order — the paper's SPMD model.  A single process is the
+world-size-1 case of the same code.
+"""
+
+import numpy as np
+import torch
+
+from . import _lib
+
+ALIGN = 32  # doubles: 256-byte column alignment for Q
+
+
+def pad_rows(m):
+    """Leading dimension for an m-row column block."""
+    return max(ALIGN, (m + ALIGN - 1) // ALIGN * ALIGN)
+
+
+def device():
+    if not torch.cuda.is_available():
+        raise RuntimeError(
+            "paper_2104_01253_b200 needs a CUDA device (B200, sm_100a); no CPU fallback exists"
+        )
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream_handle():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def ptr(t):
+    """Device address of a tensor (None -> NULL)."""
+    return None if t is None else t.data_ptr()
+
+
+# ---------------------------------------------------------------------------
+# communicator
+
+
+class Comm:
+    """Ranks of torch.distributed (NCCL) or the single-process world."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        self.group = group
+        if dist.is_available() and dist.is_initialized():
+            self.rank = dist.get_rank(group)
+            self.world = dist.get_world_size(group)
+        else:
+            self.rank, self.world = 0, 1
+        self.allreduce_calls = 0
+
+    def split(self, n):
+        """Contiguous near-equal split of n items: this rank's [lo, hi)."""
+        return block_range(n, self.world, self.rank)
+
+    def allreduce_(self, t):
+        """In-place sum over ranks (the one global reduction of a step)."""
+        if self.world > 1:
+            import torch.distributed as dist
+
+            dist.all_reduce(t, group=self.group)
+            self.allreduce_calls += 1
+        return t
+
+    def allreduce_host(self, arr):
+        """Sum a small host array over ranks (returns a new numpy array)."""
+        arr = np.asarray(arr, dtype=np.float64)
+        if self.world == 1:
+            return arr.copy()
+        t = torch.from_numpy(arr.copy()).to(device())
+        self.allreduce_(t)
+        return t.cpu().numpy()
+
+
+def block_range(n, parts, index):
+    base, extra = divmod(n, parts)
+    lo = index * base + min(index, extra)
+    return lo, lo + base + (1 if index < extra else 0)
+
+
+_default_comm = None
+
+
+def comm():
+    """The communicator operators bind to when none is given."""
+    global _default_comm
+    import torch.distributed as dist
+
+    live = dist.is_available() and dist.is_initialized()
+    if _default_comm is None or (live and _default_comm.world == 1 and dist.get_world_size() > 1):
+        _default_comm = Comm()
+    return _default_comm
+
+
+def set_comm(c):
+    global _default_comm
+    _default_comm = c
+
+
+# ---------------------------------------------------------------------------
+# workspaces and staging
+
+
+class Workspace:
+    """Zeroed reduction workspace for one stream (tickets reset themselves)."""
+
+    def __init__(self):
+        self._buf = None
+        self._bytes = 0
+
+    def get(self, kmax):
+        need = int(_lib.load().kls_workspace_bytes(0, int(max(kmax, 8))))
+        if self._buf is None or need > self._bytes:
+            self._buf = torch.zeros(need, dtype=torch.uint8, device=device())
+            self._bytes = need
+        return self._buf.data_ptr(), self._bytes
+
+
+_workspaces = {}
+
+
+def workspace(kmax):
+    key = (torch.cuda.current_device(), stream_handle())
+    ws = _workspaces.get(key)
+    if ws is None:
+        ws = _workspaces[key] = Workspace()
+    return ws.get(kmax)
+
+
+class Staging:
+    """Pinned host buffer pair for the per-step scalar round trip."""
+
+    def __init__(self, n):
+        self.n = 0
+        self._grow(max(n, 64))
+
+    def _grow(self, n):
+        self.n = n
+        self.host_out = torch.empty(n, dtype=torch.float64, pin_memory=True)
+        self.host_in = torch.empty(n, dtype=torch.float64, pin_memory=True)
+        self.dev_out = torch.empty(n, dtype=torch.float64, device=device())
+        self.dev_in = torch.empty(n, dtype=torch.float64, device=device())
+
+    def ensure(self, n):
+        if n > self.n:
+            self._grow(max(n, 2 * self.n))
+
+    def fetch(self, count):
+        """D2H of dev_out[:count]; blocks until it lands; returns numpy view."""
+        h = self.host_out[:count]
+        h.copy_(self.dev_out[:count], non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return h.numpy()
+
+    def push(self, values):
+        """H2D of a small host vector into dev_in (ordered on the stream).
+
+        Safe to reuse the pinned buffer: every step synchronizes the stream in
+        fetch() before the next push overwrites host_in.
+        """
+        values = np.asarray(values, dtype=np.float64)
+        count = values.size
+        self.ensure(count)
+        self.host_in[:count].numpy()[:] = values
+        self.dev_in[:count].copy_(self.host_in[:count], non_blocking=True)
+        return self.dev_in[:count]
+
+
+def upload(arr):
+    """Blocking host->device copy of a small array (non-hot paths)."""
+    return torch.as_tensor(np.ascontiguousarray(arr, dtype=np.float64)).to(device())
+
+
+def as_device_vector(x, n_local, lo=0, name="vector"):
+    """Accept a numpy array of the global length (sliced to this rank) or a
+    device tensor of the local length; return a fresh float64 device vector."""
+    if isinstance(x, torch.Tensor):
+        if x.dim() != 1:
+            raise ValueError(f"{name} must be 1-D")
+        if x.numel() == n_local:
+            return x.to(device=device(), dtype=torch.float64).clone()
+        x = x.detach().cpu().numpy()
+    a = np.asarray(x, dtype=np.float64)
+    if a.ndim != 1:
+        raise ValueError(f"{name} must be 1-D")
+    if a.size != n_local:
+        a = a[lo : lo + n_local]
+    return torch.from_numpy(np.ascontiguousarray(a)).to(device())

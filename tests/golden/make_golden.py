@@ -1,0 +1,206 @@
+"""Generate the golden fixtures in tests/golden/ from the REFERENCE itself.
+
+Run in the build container (where /root/reference exists):
+
+    python tests/golden/make_golden.py
+
+It imports kls 0.1.0 from /root/reference/pkg/src, runs the hot-path entry
+points on small seeded inputs, and stores inputs and outputs as compressed
+npz files.  The GPU box never runs this script; the tests only read the
+committed fixtures.
+"""
+
+import os
+import sys
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+OUT = os.path.dirname(os.path.abspath(__file__))
+
+
+def ledger_fields(led):
+    return dict(reductions=led.reductions, flops=led.flops,
+                mvtransmv=led.kernel_counts["MvTransMv"],
+                mvtimes=led.kernel_counts["MvTimesMatAddMv"], mvdot=led.kernel_counts["MvDot"])
+
+
+def main():
+    sys.path.insert(0, REF)
+    import kls
+    from kls.ortho import Dcgs2State
+
+    rng = np.random.Generator(np.random.PCG64(20240915))
+
+    # -- CSR matvec with ragged rows (pairwise summation branches) ----------
+    lengths = [0, 1, 2, 3, 7, 8, 9, 15, 16, 17, 64, 127, 128, 129, 130, 200, 256, 257, 300, 0, 5]
+    n = 400
+    rows, cols, vals = [], [], []
+    for r, L in enumerate(lengths):
+        c = np.sort(rng.choice(n, size=L, replace=False))
+        rows += [r] * L
+        cols += list(c)
+        vals += list(rng.standard_normal(L) * 10.0 ** rng.integers(-6, 7, size=L))
+    csr = kls.CsrMatrix.from_coo(len(lengths), n, rows, cols, vals)
+    x = rng.standard_normal(n) * 10.0 ** rng.integers(-3, 4, size=n)
+    np.savez_compressed(os.path.join(OUT, "csr_ragged.npz"), indptr=csr.indptr,
+                        indices=csr.indices, data=csr.data, x=x, y=csr.matvec(x))
+
+    # -- stencil and generators ----------------------------------------------
+    out = {}
+    for dims in ((5, 4, 6), (1, 1, 1), (3, 1, 7), (8, 8, 8)):
+        op = kls.laplace3d(*dims)
+        xs = rng.standard_normal(op.n)
+        key = "x".join(map(str, dims))
+        out[f"x_{key}"] = xs
+        out[f"y_{key}"] = op.apply(xs)
+        out[f"fro_{key}"] = op.frobenius_norm()
+        c = op.to_csr()
+        out[f"csr_indptr_{key}"], out[f"csr_indices_{key}"], out[f"csr_data_{key}"] = (
+            c.indptr, c.indices, c.data)
+    for k, beta in ((1, 0.5), (2, 0.5), (4, 0.5), (7, 0.3), (10, 0.5), (6, 0.0)):
+        a = kls.manteuffel_build(kls.ManteuffelSpec(k=k, beta=beta))
+        out[f"mant_indptr_{k}_{beta}"] = a.indptr
+        out[f"mant_indices_{k}_{beta}"] = a.indices
+        out[f"mant_data_{k}_{beta}"] = a.data
+        out[f"mant_eigs_{k}_{beta}"] = kls.manteuffel_eigenvalues(
+            kls.ManteuffelSpec(k=k, beta=beta)).values
+    np.savez_compressed(os.path.join(OUT, "operators.npz"), **out)
+
+    # -- Arnoldi: Manteuffel k=10 (tests/test_arnoldi.py fixtures) -----------
+    out = {}
+    op = kls.CsrOperator(kls.manteuffel_build(kls.ManteuffelSpec(k=10)))
+    start = np.random.Generator(np.random.PCG64(77)).standard_normal(100)
+    out["start"] = start
+    for scheme in ("dcgs2", "cgs2"):
+        led = kls.SyncLedger()
+        op.napply = 0
+        V, H = kls.arnoldi_expand(op, start, scheme, steps=40, ledger=led)
+        out[f"{scheme}_V"], out[f"{scheme}_H"] = V, H
+        out[f"{scheme}_napply"] = op.napply
+        for kk, vv in ledger_fields(led).items():
+            out[f"{scheme}_{kk}"] = vv
+    # per-step reduction counts and a mid-run snapshot
+    exp = kls.arnoldi(op, start, "dcgs2", capacity=10)
+    for _ in range(6):
+        exp.step()
+    out["mid_h_ext"] = exp.h_extended.copy()
+    out["mid_basis_ext"] = exp.basis_extended.copy()
+    # resume from a cgs2 decomposition with a dense coupling row
+    v0, h0 = kls.arnoldi_expand(op, start, "cgs2", steps=8)
+    hbar = h0.copy()
+    hbar[8, :] = 0.3 * np.arange(1.0, 9.0)
+    out["resume_v0"], out["resume_hbar"] = v0, hbar
+    for scheme in ("dcgs2", "cgs2"):
+        led = kls.SyncLedger()
+        e = kls.resume_arnoldi(op, v0, hbar, scheme, capacity=20, ledger=led)
+        while e.order < 14:
+            e.step()
+        V, H = e.finalize()
+        out[f"resume_{scheme}_V"], out[f"resume_{scheme}_H"] = V, H
+        out[f"resume_{scheme}_reductions"] = led.reductions
+    np.savez_compressed(os.path.join(OUT, "arnoldi_m10.npz"), **out)
+
+    # -- config 1: 2D Poisson 100x100 (beta = 0), n = 50, dcgs2 and cgs2 ------
+    out = {}
+    op = kls.CsrOperator(kls.manteuffel_build(kls.ManteuffelSpec(k=100, beta=0.0)))
+    start = np.random.Generator(np.random.PCG64(1729)).standard_normal(op.n)
+    for scheme in ("dcgs2", "cgs2"):
+        led = kls.SyncLedger()
+        V, H = kls.arnoldi_expand(op, start, scheme, steps=50, ledger=led)
+        out[f"{scheme}_H"] = H
+        out[f"{scheme}_Vsub"] = V[::97]
+        out[f"{scheme}_Vcolsum"] = V.sum(axis=0)
+        out[f"{scheme}_loo"] = kls.loss_of_orthogonality(V)
+        out[f"{scheme}_rre"] = kls.representation_error_arnoldi(op, V, H)
+        out[f"{scheme}_reductions"] = led.reductions
+    np.savez_compressed(os.path.join(OUT, "arnoldi_poisson100.npz"), **out)
+
+    # -- matrix-free 3-D Laplacian, dcgs2 / cgs2 --------------------------------
+    out = {}
+    op = kls.laplace3d(6, 5, 4)
+    start = np.random.Generator(np.random.PCG64(1729)).standard_normal(op.n)
+    out["start"] = start
+    for scheme in ("dcgs2", "cgs2"):
+        V, H = kls.arnoldi_expand(op, start, scheme, steps=30)
+        out[f"{scheme}_V"], out[f"{scheme}_H"] = V, H
+    np.savez_compressed(os.path.join(OUT, "arnoldi_laplace3d.npz"), **out)
+
+    # -- QR --------------------------------------------------------------------
+    out = {}
+    a = rng.standard_normal((100, 10))
+    out["A"] = a
+    for scheme in ("dcgs2", "cgs2"):
+        led = kls.SyncLedger()
+        q, r = kls.qr_factorize(a, scheme, ledger=led)
+        out[f"{scheme}_Q"], out[f"{scheme}_R"] = q, r
+        for kk, vv in ledger_fields(led).items():
+            out[f"{scheme}_{kk}"] = vv
+    ak = kls.synthetic_kappa(100, 10, 1e4, seed=17)
+    out["Akappa"] = ak
+    for scheme in ("dcgs2", "cgs2"):
+        q, r = kls.qr_factorize(ak, scheme)
+        out[f"kappa_{scheme}_Q"], out[f"kappa_{scheme}_R"] = q, r
+    st = Dcgs2State(3, 3)
+    st._q[:, 0] = [0.0, 0.0, 1.0]
+    st.ncols = 1
+    st.npushed = 1
+    st._w = np.array([3.0, 4.0, 1.0])
+    st._s = np.array([0.0])
+    st._wscale = float(np.linalg.norm(st._w))
+    st.npushed += 1
+    st.push(np.array([1.0, 0.0, 0.0]))
+    out["hand_R"] = st._r.copy()
+    out["hand_Q"] = st._q.copy()
+    np.savez_compressed(os.path.join(OUT, "qr.npz"), **out)
+
+    # -- GMRES -------------------------------------------------------------------
+    out = {}
+    cases = {
+        "mant12": (kls.CsrOperator(kls.manteuffel_build(kls.ManteuffelSpec(k=12))), 10, 1e-8, 400),
+        "lap8": (kls.laplace3d(8, 8, 8), 0, 0.0, 60),
+        "mant100": (kls.CsrOperator(kls.manteuffel_build(kls.ManteuffelSpec(k=100))), 50, 1e-6,
+                    10000),
+    }
+    for name, (op, restart, rtol, iters) in cases.items():
+        one = op.apply(np.ones(op.n))
+        b = one / np.linalg.norm(one)
+        out[f"{name}_b"] = b
+        for scheme in ("dcgs2", "cgs2"):
+            if name == "mant100" and scheme == "cgs2":
+                continue
+            led = kls.SyncLedger()
+            res = kls.gmres_solve(op, b, kls.GmresConfig(max_iters=iters, restart=restart,
+                                                         rtol=rtol, scheme=scheme), ledger=led)
+            p = f"{name}_{scheme}"
+            out[f"{p}_iterations"] = res.iterations
+            out[f"{p}_residual_history"] = res.residual_history
+            out[f"{p}_backward_errors"] = res.backward_errors
+            out[f"{p}_reduction_history"] = res.reduction_history
+            out[f"{p}_converged"] = res.converged
+            out[f"{p}_x"] = res.x if op.n <= 1000 else res.x[::97]
+    np.savez_compressed(os.path.join(OUT, "gmres.npz"), **out)
+
+    # -- Krylov-Schur ------------------------------------------------------------
+    out = {}
+    for name, k, mb, seed, rst, scheme in (("k5", 5, 25, 3, 100, "dcgs2"),
+                                           ("k8", 8, 30, 11, 8, "dcgs2"),
+                                           ("k10", 10, 20, 5, 30, "dcgs2"),
+                                           ("k10c", 10, 20, 5, 30, "cgs2")):
+        spec = kls.ManteuffelSpec(k=k)
+        op = kls.CsrOperator(kls.manteuffel_build(spec))
+        cfg = kls.KrylovSchurConfig(max_basis=mb, tol=1e-7, scheme=scheme, max_restarts=rst)
+        res = kls.krylov_schur_run(op, cfg, seed=seed, exact=kls.manteuffel_eigenvalues(spec))
+        out[f"{name}_values"] = res.values
+        out[f"{name}_residuals"] = res.residuals
+        out[f"{name}_lock_history"] = np.array(res.lock_history)
+        out[f"{name}_restarts"] = res.restarts
+        out[f"{name}_invariant_dim"] = res.invariant_dim
+        out[f"{name}_incomplete"] = res.incomplete
+        out[f"{name}_over"] = res.over_multiplicity
+    np.savez_compressed(os.path.join(OUT, "krylov_schur.npz"), **out)
+    print("golden fixtures written to", OUT)
+
+
+if __name__ == "__main__":
+    main()

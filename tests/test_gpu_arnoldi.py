@@ -1,0 +1,258 @@
+"""End-to-end parity of the device Arnoldi-QR against golden vectors from
+the reference (tests/golden) and the oracle.  Tolerances (BASELINE.json
+north_star): H and R entries within 1e-10 relative (normwise: |dH| <=
+1e-10 max|H|), loss of orthogonality of the same O(eps) order, identical
+ledger counts and operator-application counts."""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from conftest import golden
+
+pytestmark = pytest.mark.gpu
+
+H_RTOL = 1e-10
+
+
+def kls():
+    import paper_2104_01253_b200 as k
+
+    return k
+
+
+def mant(k, beta=0.5):
+    K = kls()
+    return K.CsrOperator(K.manteuffel_build(K.ManteuffelSpec(k=k, beta=beta)))
+
+
+def host(t):
+    return t.cpu().numpy() if isinstance(t, torch.Tensor) else np.asarray(t)
+
+
+def assert_h_close(h, ref, rtol=H_RTOL):
+    assert h.shape == ref.shape
+    scale = max(np.max(np.abs(ref)), 1e-300)
+    assert np.max(np.abs(h - ref)) <= rtol * scale, np.max(np.abs(h - ref)) / scale
+
+
+@pytest.mark.parametrize("scheme", ["dcgs2", "cgs2"])
+def test_manteuffel10_matches_reference(cuda, scheme):
+    K = kls()
+    g = golden("arnoldi_m10.npz")
+    op = mant(10)
+    led = K.SyncLedger()
+    V, H = K.arnoldi_expand(op, g["start"], scheme, steps=40, ledger=led)
+    assert V.shape == (100, 41) and H.shape == (41, 40)
+    assert_h_close(H, g[f"{scheme}_H"])
+    assert np.max(np.abs(host(V) - g[f"{scheme}_V"])) <= 1e-10
+    assert led.reductions == g[f"{scheme}_reductions"]
+    assert led.flops == g[f"{scheme}_flops"]
+    assert led.kernel_counts["MvTransMv"] == g[f"{scheme}_mvtransmv"]
+    assert led.kernel_counts["MvTimesMatAddMv"] == g[f"{scheme}_mvtimes"]
+    assert led.kernel_counts["MvDot"] == g[f"{scheme}_mvdot"]
+    assert op.napply == g[f"{scheme}_napply"]
+    assert K.loss_of_orthogonality(V) <= 1e-13
+    assert K.representation_error_arnoldi(op, V, H) <= 1e-12
+    assert not np.any(np.tril(H, -2))
+    assert np.all(np.diag(H, -1) >= 0)
+
+
+@pytest.mark.parametrize("scheme", ["dcgs2", "cgs2"])
+def test_config1_poisson100(cuda, scheme):
+    """Config 1: 2-D Poisson 100x100 (m = 1e4), n = 50."""
+    K = kls()
+    g = golden("arnoldi_poisson100.npz")
+    op = mant(100, 0.0)
+    start = np.random.Generator(np.random.PCG64(1729)).standard_normal(op.n)
+    led = K.SyncLedger()
+    V, H = K.arnoldi_expand(op, start, scheme, steps=50, ledger=led)
+    assert_h_close(H, g[f"{scheme}_H"])
+    assert np.max(np.abs(host(V)[::97] - g[f"{scheme}_Vsub"])) <= 1e-9
+    loo = K.loss_of_orthogonality(V)
+    assert loo <= 10 * max(float(g[f"{scheme}_loo"]), 1e-15)
+    assert led.reductions == g[f"{scheme}_reductions"]
+
+
+@pytest.mark.parametrize("scheme", ["dcgs2", "cgs2"])
+def test_stencil_expansion(cuda, scheme):
+    K = kls()
+    g = golden("arnoldi_laplace3d.npz")
+    op = K.laplace3d(6, 5, 4)
+    V, H = K.arnoldi_expand(op, g["start"], scheme, steps=30)
+    assert_h_close(H, g[f"{scheme}_H"])
+    assert np.max(np.abs(host(V) - g[f"{scheme}_V"])) <= 1e-10
+
+
+def test_dcgs2_vs_cgs2_agree(cuda):
+    K = kls()
+    op = mant(20)
+    start = np.random.Generator(np.random.PCG64(3)).standard_normal(op.n)
+    _, h1 = K.arnoldi_expand(op, start, "cgs2", steps=50)
+    _, h2 = K.arnoldi_expand(op, start, "dcgs2", steps=50)
+    assert np.max(np.abs(h1 - h2)) <= 1e-8 * op.frobenius_norm()
+
+
+def test_reduction_counts_per_step(cuda):
+    K = kls()
+    op = mant(10)
+    start = golden("arnoldi_m10.npz")["start"]
+    for scheme, per in (("cgs2", 3), ("dcgs2", 1)):
+        led = K.SyncLedger()
+        exp = K.arnoldi(op, start, scheme, capacity=12, ledger=led)
+        for _ in range(8):
+            before = led.reductions
+            exp.step()
+            assert led.reductions - before == per
+
+
+def test_delayed_totals_and_napply(cuda):
+    K = kls()
+    op = mant(10)
+    start = golden("arnoldi_m10.npz")["start"]
+    for steps in (1, 5, 25):
+        led = K.SyncLedger()
+        op.napply = 0
+        V, _ = K.arnoldi_expand(op, start, "dcgs2", steps=steps, ledger=led)
+        assert led.reductions <= steps + 2
+        assert V.shape[1] == steps + 1
+        assert op.napply == steps + 1
+
+
+def test_happy_breakdowns_and_guards(cuda):
+    K = kls()
+    for scheme in ("dcgs2", "cgs2"):
+        exp = K.arnoldi(K.DenseOperator(np.eye(7)), np.ones(7), scheme, capacity=8)
+        while exp.step():
+            pass
+        V, H = exp.finalize()
+        assert exp.happy and V.shape == (7, 1) and H.shape == (1, 1)
+        assert H[0, 0] == pytest.approx(1.0, rel=1e-14)
+    exp = K.arnoldi(K.DenseOperator(np.diag([1.0, 2.0, 3.0])), np.array([1.0, 0, 0]), "cgs2", 4)
+    assert exp.step() is False
+    V, H = exp.finalize()
+    assert H.shape == (1, 1) and np.allclose(host(V)[:, 0], [1, 0, 0])
+    with pytest.raises(ValueError):
+        K.arnoldi(K.DenseOperator(np.eye(3)), np.zeros(3), "dcgs2", capacity=3)
+    op = mant(10)
+    exp = K.arnoldi(op, golden("arnoldi_m10.npz")["start"], "cgs2", capacity=3)
+    exp.step()
+    exp.step()
+    with pytest.raises(K.DimensionError):
+        exp.step()
+    with pytest.raises(K.UnknownSchemeError):
+        K.arnoldi(op, np.ones(100), "mgs", capacity=3)
+
+
+def test_finalize_without_steps(cuda):
+    K = kls()
+    op = mant(10)
+    start = golden("arnoldi_m10.npz")["start"]
+    for scheme in ("dcgs2", "cgs2"):
+        V, H = K.arnoldi(op, start, scheme, capacity=4).finalize()
+        assert V.shape == (100, 1) and H.shape == (1, 0)
+        assert np.linalg.norm(host(V)[:, 0]) == pytest.approx(1.0, rel=1e-13)
+
+
+def test_mid_run_extended_views(cuda):
+    K = kls()
+    g = golden("arnoldi_m10.npz")
+    op = mant(10)
+    exp = K.arnoldi(op, g["start"], "dcgs2", capacity=10)
+    for _ in range(6):
+        exp.step()
+    assert_h_close(exp.h_extended, g["mid_h_ext"])
+    assert np.max(np.abs(host(exp.basis_extended) - g["mid_basis_ext"])) <= 1e-12
+    assert K.representation_error_arnoldi(op, exp.basis_extended, exp.h_extended) <= 1e-13
+
+
+@pytest.mark.parametrize("scheme", ["dcgs2", "cgs2"])
+def test_resume_generalized_coupling_row(cuda, scheme):
+    K = kls()
+    g = golden("arnoldi_m10.npz")
+    op = mant(10)
+    led = K.SyncLedger()
+    exp = K.resume_arnoldi(op, g["resume_v0"], g["resume_hbar"], scheme, capacity=20, ledger=led)
+    while exp.order < 14:
+        exp.step()
+    V, H = exp.finalize()
+    assert_h_close(H, g[f"resume_{scheme}_H"])
+    assert np.max(np.abs(host(V) - g[f"resume_{scheme}_V"])) <= 1e-10
+    assert led.reductions == g[f"resume_{scheme}_reductions"]
+
+
+@pytest.mark.parametrize("scheme", ["dcgs2", "cgs2"])
+def test_qr_matches_reference(cuda, scheme):
+    K = kls()
+    g = golden("qr.npz")
+    led = K.SyncLedger()
+    Q, R = K.qr_factorize(g["A"], scheme, ledger=led)
+    assert_h_close(R, g[f"{scheme}_R"])
+    assert np.max(np.abs(host(Q) - g[f"{scheme}_Q"])) <= 1e-12
+    assert led.reductions == g[f"{scheme}_reductions"]
+    assert led.flops == g[f"{scheme}_flops"]
+    Q, R = K.qr_factorize(g["Akappa"], scheme)
+    assert_h_close(R, g[f"kappa_{scheme}_R"])
+
+
+def test_qr_hand_worked_step(cuda):
+    """tests/test_ortho.py:145-158 / SPEC.md:215: beta=26, c=1, alpha=5."""
+    K = kls()
+    Q, R = K.qr_factorize(np.array([[0.0, 3.0, 1.0], [0.0, 4.0, 0.0], [1.0, 1.0, 0.0]]), "dcgs2")
+    assert R[1, 1] == pytest.approx(5.0, rel=1e-15)
+    assert np.allclose(host(Q)[:, 1], [0.6, 0.8, 0.0], atol=1e-15)
+
+
+def test_qr_breakdown_on_duplicate_column(cuda, rng):
+    K = kls()
+    a = rng.standard_normal(40)
+    for scheme in ("dcgs2", "cgs2"):
+        st = K.make_state(scheme, 40, 4)
+        st.push(a)
+        with pytest.raises(K.BreakdownError):
+            st.push(a.copy())
+            st.push(rng.standard_normal(40))
+            st.finalize()
+
+
+def test_large_m_against_oracle(cuda):
+    """m ~ 1e6 stencil, 20 steps: device H vs the oracle on the same input."""
+    K = kls()
+    dims = (100, 100, 100)
+    start = np.random.Generator(np.random.PCG64(1729)).standard_normal(10**6)
+    V, H = K.arnoldi_expand(K.laplace3d(*dims), start, "dcgs2", steps=20)
+    _, Hr, _ = oracle.dcgs2_arnoldi(lambda x: oracle.stencil7_matvec(x, dims), start, 20)
+    assert_h_close(H, Hr)
+    assert K.loss_of_orthogonality(V) <= 1e-13
+
+
+def test_determinism_bitwise(cuda):
+    K = kls()
+    op = mant(30)
+    start = np.random.Generator(np.random.PCG64(9)).standard_normal(op.n)
+    V1, H1 = K.arnoldi_expand(op, start, "dcgs2", steps=25)
+    V1 = V1.clone()
+    V2, H2 = K.arnoldi_expand(op, start, "dcgs2", steps=25)
+    assert np.array_equal(H1, H2)
+    assert torch.equal(V1, V2)
+
+
+def test_qr_hand_worked_pending_state(cuda):
+    """The exact hand-worked state of tests/test_ortho.py:145-158: q0 = e3,
+    pending w = [3, 4, 1] with s = [0]; pushing e1 gives beta = 26, c = 1,
+    alpha = 5, q1 = [0.6, 0.8, 0]."""
+    K = kls()
+    g = golden("qr.npz")
+    st = K.make_state("dcgs2", 3, 3)
+    st.eng.col(0).copy_(torch.tensor([0.0, 0.0, 1.0], dtype=torch.float64))
+    st.ncols = 1
+    st.npushed = 2
+    st._w.copy_(torch.tensor([3.0, 4.0, 1.0], dtype=torch.float64))
+    st._s = np.array([0.0])
+    st._wscale = float(np.sqrt(26.0))
+    st._pending = True
+    st.push(np.array([1.0, 0.0, 0.0]))
+    assert st._r[1, 1] == pytest.approx(5.0, rel=1e-15)
+    assert np.allclose(host(st.q)[:, 1], [0.6, 0.8, 0.0], atol=1e-15)
+    assert np.allclose(st._r, g["hand_R"], rtol=1e-15, atol=1e-15)

@@ -1,0 +1,217 @@
+"""Kernel-level parity on the GPU: every libklsgpu entry point against a
+numpy fp64 reference or the oracle, including odd / empty / ragged shapes.
+Integer-exact operators (CSR, stencil) must be bit-identical."""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from conftest import golden
+
+pytestmark = pytest.mark.gpu
+
+
+def _lib():
+    from paper_2104_01253_b200 import _lib, runtime
+
+    return _lib, runtime
+
+
+def _colmajor(a):
+    """Device copy of a host (m, k) array as a column-major block with a
+    padded leading dimension; returns (buffer (k, ld), ld)."""
+    from paper_2104_01253_b200 import runtime
+
+    m, k = a.shape
+    ld = runtime.pad_rows(m)
+    buf = torch.zeros((max(k, 1), ld), dtype=torch.float64, device="cuda")
+    if k:
+        buf[:k, :m] = torch.from_numpy(np.ascontiguousarray(a.T)).cuda()
+    return buf, ld
+
+
+def _dot_tol(a, b):
+    """Forward error bound scale for sums of products: eps * n * sum|a b|."""
+    return 1e-15 * max(a.shape[0], 1) * (np.abs(a).T @ np.abs(b))
+
+
+@pytest.mark.parametrize("m", [1, 2, 3, 63, 64, 1000, 4097, 100003])
+@pytest.mark.parametrize("k", [0, 1, 3, 4, 5, 17])
+def test_gram_dcgs2_matches_numpy(cuda, rng, m, k):
+    lib, rt = _lib()
+    Q = rng.standard_normal((m, k))
+    w = rng.standard_normal(m)
+    aw = rng.standard_normal(m)
+    qb, ld = _colmajor(Q)
+    wd = torch.from_numpy(w).cuda()
+    awd = torch.from_numpy(aw).cuda()
+    out = torch.full((2 * k + 3,), np.nan, dtype=torch.float64, device="cuda")
+    ws, wsb = rt.workspace(k + 1)
+    lib.call("kls_gram_dcgs2", qb.data_ptr(), ld, m, k, wd.data_ptr(), awd.data_ptr(),
+             out.data_ptr(), ws, wsb, rt.stream_handle())
+    got = out.cpu().numpy()
+    left = np.hstack([Q, w[:, None]])
+    right = np.column_stack([w, aw])
+    want = np.concatenate([(left.T @ right).T.ravel(), [aw @ aw]])
+    tol = np.concatenate([_dot_tol(left, right).T.ravel(), _dot_tol(aw[:, None], aw[:, None]).ravel()])
+    assert np.all(np.abs(got - want) <= tol + 1e-300)
+    # bitwise reproducible
+    out2 = torch.empty_like(out)
+    lib.call("kls_gram_dcgs2", qb.data_ptr(), ld, m, k, wd.data_ptr(), awd.data_ptr(),
+             out2.data_ptr(), ws, wsb, rt.stream_handle())
+    assert torch.equal(out, out2)
+
+
+@pytest.mark.parametrize("k", [0, 2, 7, 1030])
+def test_mv_trans_mv_generic_panels(cuda, rng, k):
+    """k > 1024 exercises the multi-panel path; nx=1 with xnorm."""
+    lib, rt = _lib()
+    m = 3001
+    Q = rng.standard_normal((m, k))
+    x = rng.standard_normal(m)
+    qb, ld = _colmajor(Q)
+    xd = torch.from_numpy(x).cuda()
+    out = torch.full((k + 1,), np.nan, dtype=torch.float64, device="cuda")
+    ws, wsb = rt.workspace(k + 1)
+    lib.call("kls_mv_trans_mv", qb.data_ptr() if k else None, ld, m, k, None, xd.data_ptr(), None,
+             1, 1, out.data_ptr(), ws, wsb, rt.stream_handle())
+    got = out.cpu().numpy()
+    want = np.concatenate([Q.T @ x, [x @ x]])
+    assert np.allclose(got, want, rtol=1e-12, atol=1e-11)
+
+
+@pytest.mark.parametrize("m", [1, 5, 64, 1001, 70001])
+@pytest.mark.parametrize("j", [0, 1, 4, 9])
+@pytest.mark.parametrize("divide", [0, 1])
+def test_dcgs2_update_matches_numpy(cuda, rng, m, j, divide):
+    lib, rt = _lib()
+    Q = rng.standard_normal((m, j + 1))
+    Q[:, j] = 0.0
+    w = rng.standard_normal(m)
+    aw = rng.standard_normal(m)
+    c = rng.standard_normal(j)
+    t = rng.standard_normal(j + 1)
+    alpha = 1.7
+    qb, ld = _colmajor(Q)
+    wd = torch.from_numpy(w.copy()).cuda()
+    awd = torch.from_numpy(aw).cuda()
+    coef = torch.from_numpy(np.concatenate([c, t])).cuda()
+    lib.call("kls_dcgs2_update", qb.data_ptr(), ld, m, j, wd.data_ptr(), awd.data_ptr(),
+             coef.data_ptr(), alpha, divide, rt.stream_handle())
+    u = w - Q[:, :j] @ c
+    q = u / alpha
+    a = aw / alpha if divide else aw
+    wn = a - (Q[:, :j] @ t[:j] + q * t[j])
+    got_q = qb[j, :m].cpu().numpy()
+    assert np.allclose(got_q, q, rtol=1e-13, atol=1e-13)
+    assert np.allclose(wd.cpu().numpy(), wn, rtol=1e-13, atol=1e-12)
+    # untouched columns stay untouched
+    if j:
+        assert np.array_equal(qb[:j, :m].cpu().numpy(), Q[:, :j].T)
+
+
+@pytest.mark.parametrize("l", [1, 2])
+@pytest.mark.parametrize("k", [0, 3, 6])
+def test_mv_times_mat_add_mv_with_fused_norm(cuda, rng, l, k):
+    lib, rt = _lib()
+    m = 5003
+    B = rng.standard_normal((m, k))
+    Y = rng.standard_normal((m, l))
+    S = rng.standard_normal((k, l))
+    bb, ldb = _colmajor(B)
+    yb, ldy = _colmajor(Y)
+    sd = torch.from_numpy(np.ascontiguousarray(S.T).ravel()).cuda()
+    nrm = torch.zeros(1, dtype=torch.float64, device="cuda")
+    ws, wsb = rt.workspace(8)
+    lib.call("kls_mv_times_mat_add_mv", yb.data_ptr(), ldy, m, l, bb.data_ptr() if k else None, ldb,
+             k, sd.data_ptr() if k else None, -1.0, 0.5, nrm.data_ptr(), ws, wsb,
+             rt.stream_handle())
+    want = 0.5 * Y - B @ S
+    got = yb[:l, :m].cpu().numpy().T
+    assert np.allclose(got, want, rtol=1e-13, atol=1e-12)
+    assert np.isclose(nrm.item(), want[:, -1] @ want[:, -1], rtol=1e-12)
+
+
+def test_csr_spmv_bitwise_ragged(cuda):
+    """Rows of 0..300 nonzeros: numpy's reduceat/pairwise order, bit for bit."""
+    from paper_2104_01253_b200 import CsrMatrix, CsrOperator
+
+    g = golden("csr_ragged.npz")
+    nrows = len(g["indptr"]) - 1
+    n = g["x"].size
+    # square-ify: pad with empty rows so the operator is n x n
+    indptr = np.concatenate([g["indptr"], np.full(n - nrows, g["indptr"][-1])])
+    op = CsrOperator(CsrMatrix(n, n, indptr, g["indices"], g["data"]))
+    y = op.apply(g["x"]).cpu().numpy()
+    assert np.array_equal(y[:nrows], g["y"])
+    assert np.all(y[nrows:] == 0.0)
+
+
+@pytest.mark.parametrize("k,beta", [(1, 0.5), (4, 0.5), (10, 0.5), (6, 0.0)])
+def test_manteuffel_operator_bitwise(cuda, rng, k, beta):
+    from paper_2104_01253_b200 import CsrOperator, ManteuffelSpec, manteuffel_build
+
+    csr = manteuffel_build(ManteuffelSpec(k=k, beta=beta))
+    ptr, idx, dat = oracle.manteuffel_csr(k, beta)
+    assert np.array_equal(csr.indptr, ptr) and np.array_equal(csr.indices, idx)
+    assert np.array_equal(csr.data, dat)
+    x = rng.standard_normal(k * k)
+    y = CsrOperator(csr).apply(x).cpu().numpy()
+    assert np.array_equal(y, oracle.csr_matvec(ptr, idx, dat, x))
+
+
+@pytest.mark.parametrize("dims", [(5, 4, 6), (1, 1, 1), (3, 1, 7), (8, 8, 8)])
+def test_stencil_bitwise(cuda, dims):
+    from paper_2104_01253_b200 import laplace3d
+
+    g = golden("operators.npz")
+    key = "x".join(map(str, dims))
+    op = laplace3d(*dims)
+    y = op.apply(g[f"x_{key}"]).cpu().numpy()
+    assert np.array_equal(y, g[f"y_{key}"])
+    assert op.frobenius_norm() == g[f"fro_{key}"]
+    assert op.napply == 1
+
+
+def test_stencil_large_bitwise_against_oracle(cuda, rng):
+    from paper_2104_01253_b200 import laplace3d
+
+    dims = (61, 67, 129)
+    x = rng.standard_normal(int(np.prod(dims)))
+    y = laplace3d(*dims).apply(x).cpu().numpy()
+    assert np.array_equal(y, oracle.stencil7_matvec(x, dims))
+
+
+def test_tsgemm_inplace(cuda, rng):
+    lib, rt = _lib()
+    m, k = 10007, 37
+    V = rng.standard_normal((m, k))
+    Z = rng.standard_normal((k, k))
+    vb, ld = _colmajor(V)
+    zd = torch.from_numpy(np.ascontiguousarray(Z.T).ravel()).cuda()  # column-major
+    lib.call("kls_tsgemm_inplace", vb.data_ptr(), ld, m, k, zd.data_ptr(), rt.stream_handle())
+    assert np.allclose(vb[:k, :m].cpu().numpy().T, V @ Z, rtol=1e-12, atol=1e-12)
+
+
+def test_resid_norms_and_scale(cuda, rng):
+    lib, rt = _lib()
+    n = 12345
+    b, ax, x = (rng.standard_normal(n) for _ in range(3))
+    bd, axd, xd = (torch.from_numpy(v).cuda() for v in (b, ax, x))
+    out = torch.zeros(3, dtype=torch.float64, device="cuda")
+    ws, wsb = rt.workspace(4)
+    lib.call("kls_resid_norms", bd.data_ptr(), axd.data_ptr(), xd.data_ptr(), n, out.data_ptr(),
+             ws, wsb, rt.stream_handle())
+    want = [np.sum((b - ax) ** 2), x @ x, b @ b]
+    assert np.allclose(out.cpu().numpy(), want, rtol=1e-12)
+    y = torch.empty_like(xd)
+    lib.call("kls_scale", xd.data_ptr(), y.data_ptr(), n, 3.0, 0, rt.stream_handle())
+    assert np.array_equal(y.cpu().numpy(), x / 3.0)
+
+
+def test_errors_surface_as_exceptions(cuda):
+    from paper_2104_01253_b200 import _lib
+
+    with pytest.raises(_lib.KlsGpuError):
+        _lib.call("kls_gram_dcgs2", None, 1, 10, 3, None, None, None, None, 0, None)
