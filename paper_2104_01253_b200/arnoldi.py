@@ -104,6 +104,9 @@ class _BaseArnoldi:
         pass
 
     def _mark_happy(self):
+        # basis_extended shows one zero column past a breakdown (the
+        # reference's zero-initialized storage)
+        self.eng.zero_col(self.nbasis)
         self.happy = True
         return False
 

@@ -20,7 +20,7 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
-from . import _lib, runtime
+from . import _lib, runtime, trace
 from .errors import DimensionError, MatrixMarketError
 
 # ---------------------------------------------------------------------------
@@ -106,7 +106,14 @@ class LinearOperator:
                     f"{name} of local length {self.m_local} expected, got {tuple(x.shape)}"
                 )
             return x if x.dtype == torch.float64 else x.double()
-        a = np.asarray(x.cpu().numpy() if isinstance(x, torch.Tensor) else x, dtype=np.float64)
+        if isinstance(x, torch.Tensor):
+            # host tensor (pinned for an async copy): this rank's rows only
+            if x.dim() != 1 or x.numel() != self.n:
+                raise DimensionError(f"{name} of length {self.n} expected, got {tuple(x.shape)}")
+            part = x[self.row_lo : self.row_hi].to(torch.float64)
+            runtime.XFER["h2d"] += 8 * part.numel()
+            return part.to(runtime.device(), non_blocking=part.is_pinned())
+        a = np.asarray(x, dtype=np.float64)
         if a.shape != (self.n,):
             raise DimensionError(f"{name} of length {self.n} expected, got {a.shape}")
         return runtime.upload(a[self.row_lo : self.row_hi])
@@ -133,7 +140,13 @@ class LinearOperator:
             else:
                 x = _PlainVector(x)
         self._exchange(x)
-        self._launch(x, y)
+        trace.note("apply", self.apply_bytes())
+        with trace.span("apply"):
+            self._launch(x, y)
+
+    def apply_bytes(self):
+        """Algorithmic HBM bytes of one application (x read, y written)."""
+        return 16 * self.m_local
 
     def _needs_halo(self):
         return False
@@ -369,6 +382,10 @@ class CsrOperator(LinearOperator):
             ops.append(dist.P2POp(dist.irecv, buf[a:b], q, group=self.comm.group))
         _p2p(ops)
 
+    def apply_bytes(self):
+        """x and y, plus values (8), column indices (4) and row pointers (8)."""
+        return 16 * self.m_local + 12 * int(self._col.numel()) + 8 * (self.m_local + 1)
+
     def _launch(self, x, y):
         _lib.call("kls_csr_spmv", self._rowptr.data_ptr(), self._col.data_ptr(),
                   self._val.data_ptr(), self.m_local, x.ext_ptr, y.data_ptr(),
@@ -527,6 +544,10 @@ class StencilLaplace3D(LinearOperator):
     def _exchange(self, x):
         if self.comm.world == 1:
             return
+        with trace.span("halo"):
+            self._exchange_planes(x)
+
+    def _exchange_planes(self, x):
         import torch.distributed as dist
 
         P, g = self.plane, self.comm.group

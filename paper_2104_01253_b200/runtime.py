@@ -17,6 +17,9 @@ from . import _lib
 
 ALIGN = 32  # doubles: 256-byte column alignment for Q
 
+# host<->device bytes moved by the package (bench.py's e2e accounting)
+XFER = {"h2d": 0, "d2h": 0}
+
 
 def pad_rows(m):
     """Leading dimension for an m-row column block."""
@@ -111,15 +114,23 @@ def set_comm(c):
 
 
 class Workspace:
-    """Zeroed reduction workspace for one stream (tickets reset themselves)."""
+    """Zeroed reduction workspace for one stream (tickets reset themselves).
+
+    Grows on demand; a replaced buffer is kept alive (``_old``) because work
+    already queued on the stream may still use it.  Callers must not cache
+    the pointer across calls that could grow it.
+    """
 
     def __init__(self):
         self._buf = None
         self._bytes = 0
+        self._old = []
 
     def get(self, kmax):
         need = int(_lib.load().kls_workspace_bytes(0, int(max(kmax, 8))))
         if self._buf is None or need > self._bytes:
+            if self._buf is not None:
+                self._old.append(self._buf)
             self._buf = torch.zeros(need, dtype=torch.uint8, device=device())
             self._bytes = need
         return self._buf.data_ptr(), self._bytes
@@ -155,11 +166,13 @@ class Staging:
             self._grow(max(n, 2 * self.n))
 
     def fetch(self, count):
-        """D2H of dev_out[:count]; blocks until it lands; returns numpy view."""
+        """D2H of dev_out[:count]; blocks until it lands; returns a numpy copy
+        (the pinned buffer is reused by the next fetch)."""
         h = self.host_out[:count]
+        XFER["d2h"] += 8 * count
         h.copy_(self.dev_out[:count], non_blocking=True)
         torch.cuda.current_stream().synchronize()
-        return h.numpy()
+        return h.numpy().copy()
 
     def push(self, values):
         """H2D of a small host vector into dev_in (ordered on the stream).
@@ -171,12 +184,14 @@ class Staging:
         count = values.size
         self.ensure(count)
         self.host_in[:count].numpy()[:] = values
+        XFER["h2d"] += 8 * count
         self.dev_in[:count].copy_(self.host_in[:count], non_blocking=True)
         return self.dev_in[:count]
 
 
 def upload(arr):
     """Blocking host->device copy of a small array (non-hot paths)."""
+    XFER["h2d"] += 8 * int(np.size(arr))
     return torch.as_tensor(np.ascontiguousarray(arr, dtype=np.float64)).to(device())
 
 
