@@ -32,6 +32,48 @@ def _unsupported(scheme):
         f"unknown scheme {scheme!r} (the B200 backend provides {', '.join(ARNOLDI_SCHEMES)})")
 
 
+def dcgs2_host_step(g, j, m, wscale, k_prev, h, ledger):
+    """Host half of a DCGS2 Arnoldi step (arnoldi.py:367-420), from the
+    reduced vector g = [c, beta, s, s_piv, ||aw||^2] of kls_gram_dcgs2.
+
+    Runs identically on every rank (the allreduced g is bitwise the same on
+    all of them), so no broadcast is needed.  Completes Hessenberg column
+    j-1 in ``h`` in the reference's order.  Returns None on a happy
+    breakdown, else (c, t_full, alpha, vscale, K_next) for the fused update.
+    Raises BreakdownError("pythagorean") like the reference.
+    """
+    c = np.array(g[:j], dtype=np.float64)
+    beta = float(g[j])
+    s = np.array(g[j + 1 : 2 * j + 1], dtype=np.float64)
+    s_piv = float(g[2 * j + 1])
+    aw_norm = float(np.sqrt(g[2 * j + 2]))
+    if not np.sqrt(max(beta, 0.0)) > _EPS * np.sqrt(m) * wscale:
+        if j > 0:
+            h[:j, j - 1] = k_prev + c
+            h[j, j - 1] = 0.0
+        return None
+    alpha_sq = beta - float(c @ c)
+    ledger.add_flops(2 * j)
+    if not alpha_sq > beta * _EPS * _EPS:
+        raise BreakdownError(f"cancellation in the delayed norm of basis column {j}",
+                             kind="pythagorean", column=j)
+    alpha = float(np.sqrt(alpha_sq))
+    ledger.record(_ledger.MV_TIMES_MAT_ADD_MV, flops=2 * m * j)  # u = w - Q c
+    t_piv = (s_piv - float(c @ s)) / (alpha * alpha)
+    ledger.add_flops(2 * j)
+    t_full = np.append(s / alpha, t_piv)
+    if j > 0:
+        h[:j, j - 1] = k_prev + c
+        h[j, j - 1] = alpha
+    hc = h[: j + 1, :j] @ c
+    ledger.add_flops(2 * (j + 1) * j)
+    k_next = t_full - hc / alpha
+    vscale = aw_norm / alpha  # pre-projection norm, arnoldi.py:414
+    ledger.add_flops(m)
+    ledger.record(_ledger.MV_TIMES_MAT_ADD_MV, flops=2 * m * (j + 1))  # w' = aw/alpha - V t
+    return c, t_full, alpha, vscale, k_next
+
+
 class _BaseArnoldi:
     scheme_id = None
 
@@ -190,42 +232,15 @@ class _DelayedArnoldi(_BaseArnoldi):
         j = self.nbasis
         g = e.gram_dcgs2(j, self._w.local, self._aw)
         self._rec(_ledger.MV_TRANS_MV, 2 * m * (j + 1) * 2)
-        c = g[:j].copy()
-        beta = float(g[j])
-        s = g[j + 1 : 2 * j + 1].copy()
-        s_piv = float(g[2 * j + 1])
-        aw_norm = float(np.sqrt(g[2 * j + 2]))
-        if not np.sqrt(max(beta, 0.0)) > _EPS * np.sqrt(m) * self._wscale:
-            # the pending direction vanished: invariant subspace
-            if j > 0:
-                self._h[:j, j - 1] = self._k + c
-                self._h[j, j - 1] = 0.0
-                self.hcols = j
+        res = dcgs2_host_step(g, j, m, self._wscale, self._k, self._h, self.ledger)
+        if j > 0:
+            self.hcols = j
+        if res is None:  # the pending direction vanished: invariant subspace
             self._pending = False
             return self._mark_happy()
-        alpha_sq = beta - float(c @ c)
-        self.ledger.add_flops(2 * j)
-        if not alpha_sq > beta * _EPS * _EPS:
-            raise BreakdownError(
-                f"cancellation in the delayed norm of basis column {j}",
-                kind="pythagorean", column=j)
-        alpha = float(np.sqrt(alpha_sq))
-        self._rec(_ledger.MV_TIMES_MAT_ADD_MV, 2 * m * j)  # u = w - Q c
-        t_piv = (s_piv - float(c @ s)) / (alpha * alpha)
-        self.ledger.add_flops(2 * j)
+        c, t_full, alpha, vscale, self._k = res
         if self.start_norm is None:
             self.start_norm = alpha
-        t_full = np.append(s / alpha, t_piv)
-        if j > 0:
-            self._h[:j, j - 1] = self._k + c
-            self._h[j, j - 1] = alpha
-            self.hcols = j
-        hc = self._h[: j + 1, :j] @ c
-        self.ledger.add_flops(2 * (j + 1) * j)
-        self._k = t_full - hc / alpha
-        vscale = aw_norm / alpha  # pre-projection norm, arnoldi.py:414
-        self.ledger.add_flops(m)
-        self._rec(_ledger.MV_TIMES_MAT_ADD_MV, 2 * m * (j + 1))  # w' = aw/alpha - V t
         # one pass: Q(:, j) = (w - Q c)/alpha; w = aw/alpha - Q t - q_j t_j
         e.dcgs2_update(j, self._w.local, self._aw, c, t_full, alpha, divide=True)
         self.nbasis += 1

@@ -215,6 +215,32 @@ def _p2p(ops):
             req.wait()
 
 
+def halo_plan(rank, windows):
+    """Point-to-point plan of a row-sharded SpMV halo exchange.
+
+    ``windows[q] = (need_lo, own_lo, own_hi, need_hi)``: rank q owns global
+    rows [own_lo, own_hi) and its rows read columns [need_lo, need_hi).
+    Returns (sends, recvs) for ``rank``: sends are (peer, a, b) slices of the
+    local rows; recvs are (peer, "lo"|"hi", a, b) slices of the halo buffers
+    (offsets from the start of the lo window [need_lo, own_lo) or the hi
+    window [own_hi, need_hi)).
+    """
+    need_lo, own_lo, own_hi, need_hi = windows[rank]
+    sends, recvs = [], []
+    for q, (qn_lo, q_lo, q_hi, qn_hi) in enumerate(windows):
+        if q == rank:
+            continue
+        for a, b in ((qn_lo, q_lo), (q_hi, qn_hi)):  # rows of mine that q reads
+            x0, x1 = max(a, own_lo), min(b, own_hi)
+            if x1 > x0:
+                sends.append((q, x0 - own_lo, x1 - own_lo))
+        for a, b, side in ((need_lo, own_lo, "lo"), (own_hi, need_hi, "hi")):  # q's rows I read
+            x0, x1 = max(a, q_lo), min(b, q_hi)
+            if x1 > x0:
+                recvs.append((q, side, x0 - a, x1 - a))
+    return sends, recvs
+
+
 class DenseOperator(LinearOperator):
     """Small dense operator (problems.py:68-85), single rank."""
 
@@ -323,8 +349,7 @@ class CsrOperator(LinearOperator):
         cmax = int(cols.max()) if cols.size else hi - 1
         self.halo_lo = max(0, lo - min(cmin, lo))
         self.halo_hi = max(0, max(cmax + 1, hi) - hi)
-        pad = (-self.halo_lo) % runtime.ALIGN
-        base = lo - self.halo_lo - pad  # global index of ext[0]
+        base = lo - self.halo_lo  # global row of ext[0] (HaloVector.ext_ptr)
         dev = runtime.device()
         self._rowptr = torch.from_numpy(csr.indptr[lo : hi + 1] - s).to(dev)
         self._col = torch.from_numpy((cols - base).astype(np.int32)).to(dev)
@@ -340,7 +365,7 @@ class CsrOperator(LinearOperator):
         return HaloVector(self.m_local, self.halo_lo, self.halo_hi, contiguous=True)
 
     def _halo_plan(self):
-        """Which global row ranges each rank sends to / receives from whom."""
+        """Exchange plan from every rank's [need_lo, own_lo, own_hi, need_hi)."""
         c = self.comm
         mine = torch.tensor([self.row_lo - self.halo_lo, self.row_lo, self.row_hi,
                              self.row_hi + self.halo_hi], dtype=torch.int64, device=runtime.device())
@@ -348,25 +373,7 @@ class CsrOperator(LinearOperator):
         import torch.distributed as dist
 
         dist.all_gather(allw, mine, group=c.group)
-        win = [w.cpu().numpy() for w in allw]
-        sends, recvs = [], []
-        for q in range(c.world):
-            if q == c.rank:
-                continue
-            qlo, qhi = win[q][1], win[q][2]
-            # rows I own that q needs
-            for a, b in ((win[q][0], win[q][1]), (win[q][2], win[q][3])):
-                x0, x1 = max(a, self.row_lo), min(b, self.row_hi)
-                if x1 > x0:
-                    sends.append((q, x0 - self.row_lo, x1 - self.row_lo))
-            # rows q owns that I need
-            for a, b, side in ((self.row_lo - self.halo_lo, self.row_lo, "lo"),
-                               (self.row_hi, self.row_hi + self.halo_hi, "hi")):
-                x0, x1 = max(a, qlo), min(b, qhi)
-                if x1 > x0:
-                    off = x0 - a
-                    recvs.append((q, side, off, off + (x1 - x0)))
-        return sends, recvs
+        return halo_plan(c.rank, [tuple(int(v) for v in w.cpu().tolist()) for w in allw])
 
     def _exchange(self, x):
         if self._plan is None:

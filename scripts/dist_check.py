@@ -1,0 +1,96 @@
+"""Multi-GPU parity check (torchrun, one process per GPU, NCCL):
+
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 scripts/dist_check.py
+
+Row-sharded DCGS2 / CGS2 Arnoldi on the matrix-free stencil and on a CSR
+operator, plus restarted GMRES, compared on rank 0 with the CPU oracle run
+single-process on the same global input.  Prints one JSON line; exit 1 on a
+parity failure.
+"""
+
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def main():
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    rank, world = dist.get_rank(), dist.get_world_size()
+    import oracle
+    import paper_2104_01253_b200 as kls
+
+    res = {"world": world}
+    ok = True
+
+    def gather_h(H):
+        return H  # host math is replicated: every rank holds the same H
+
+    # stencil, both schemes
+    dims = (40, 30, 20)
+    start = np.random.Generator(np.random.PCG64(1729)).standard_normal(int(np.prod(dims)))
+    for scheme in ("dcgs2", "cgs2"):
+        op = kls.laplace3d(*dims)
+        led = kls.SyncLedger()
+        V, H = kls.arnoldi_expand(op, start, scheme, steps=30, ledger=led)
+        loo = kls.loss_of_orthogonality(V)
+        if rank == 0:
+            _, Hr, cnt = getattr(oracle, f"{scheme}_arnoldi")(
+                lambda x: oracle.stencil7_matvec(x, dims), start, 30)
+            err = float(np.max(np.abs(H - Hr)) / np.max(np.abs(Hr)))
+            res[f"stencil_{scheme}_relerr"] = err
+            res[f"stencil_{scheme}_loo"] = loo
+            res[f"stencil_{scheme}_reductions"] = [led.reductions, cnt.reductions]
+            ok &= err <= 1e-10 and led.reductions == cnt.reductions and loo <= 1e-12
+    # CSR (Manteuffel k=60)
+    k = 60
+    csr = kls.manteuffel_build(kls.ManteuffelSpec(k=k))
+    start = np.random.Generator(np.random.PCG64(7)).standard_normal(k * k)
+    op = kls.CsrOperator(csr)
+    V, H = kls.arnoldi_expand(op, start, "dcgs2", steps=30)
+    if rank == 0:
+        ptr, idx, dat = oracle.manteuffel_csr(k, 0.5)
+        _, Hr, _ = oracle.dcgs2_arnoldi(lambda x: oracle.csr_matvec(ptr, idx, dat, x), start, 30)
+        err = float(np.max(np.abs(H - Hr)) / np.max(np.abs(Hr)))
+        res["csr_dcgs2_relerr"] = err
+        ok &= err <= 1e-10
+    # GMRES
+    k = 30
+    csr = kls.manteuffel_build(kls.ManteuffelSpec(k=k))
+    op = kls.CsrOperator(csr)
+    ptr, idx, dat = oracle.manteuffel_csr(k, 0.5)
+    one = oracle.csr_matvec(ptr, idx, dat, np.ones(k * k))
+    b = one / np.linalg.norm(one)
+    g = kls.gmres_solve(op, b, kls.GmresConfig(max_iters=300, restart=20, rtol=1e-8,
+                                               scheme="dcgs2"))
+    if rank == 0:
+        r = oracle.gmres(lambda x: oracle.csr_matvec(ptr, idx, dat, x), b,
+                         float(np.linalg.norm(dat)), 300, 20, 1e-8, "dcgs2")
+        res["gmres_iterations"] = [g.iterations, r["iterations"]]
+        nn = min(len(g.residual_history), len(r["residual_history"]))
+        dh = np.abs(g.residual_history[:nn] - r["residual_history"][:nn])
+        res["gmres_first_bad"] = int(np.argmax(dh > 1e-8)) if np.any(dh > 1e-8) else -1
+        res["gmres_hist"] = [g.residual_history[:45:4].tolist(), r["residual_history"][:45:4].tolist()]
+        res["gmres_be"] = [g.backward_errors[:45:4].tolist(), r["backward_errors"][:45:4].tolist()]
+        dev = float(np.max(dh)) if g.iterations == r["iterations"] else float("inf")
+        res["gmres_hist_maxdiff"] = dev
+        ok &= g.iterations == r["iterations"] and dev <= 1e-8
+    res["ok"] = bool(ok)
+    flag = torch.tensor([1.0 if ok or rank != 0 else 0.0], device="cuda")
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+    if rank == 0:
+        print(json.dumps(res), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+    return 0 if flag.item() == 1.0 else 1
+
+
+if __name__ == "__main__":
+    sys.exit(main())
