@@ -77,14 +77,16 @@ def dcgs2_host_step(g, j, m, wscale, k_prev, h, ledger):
 class _BaseArnoldi:
     scheme_id = None
 
-    def __init__(self, op, capacity, ledger):
+    def __init__(self, op, capacity, ledger, engine=None):
         if capacity < 2:
             raise DimensionError("capacity of at least 2 basis vectors required")
         self.op = op
         self.capacity = capacity
         self.ledger = ledger if ledger is not None else SyncLedger()
         self.m = op.shape[0]
-        self.eng = Engine(op, capacity)
+        # a caller (Krylov-Schur restart) may hand over an engine whose basis
+        # buffer already holds the columns to resume from
+        self.eng = engine if engine is not None else Engine(op, capacity)
         self._h = np.zeros((capacity, capacity - 1))
         self.nbasis = 0
         self.hcols = 0
@@ -176,8 +178,8 @@ class _DelayedArnoldi(_BaseArnoldi):
 
     scheme_id = "dcgs2"
 
-    def __init__(self, op, start, capacity, ledger=None):
-        super().__init__(op, capacity, ledger)
+    def __init__(self, op, start, capacity, ledger=None, engine=None):
+        super().__init__(op, capacity, ledger, engine)
         e = self.eng
         self._w = op.new_vector()  # pending vector, with halo space
         self._aw = torch.zeros(e.ld, dtype=torch.float64, device=e.vbuf.device)[: e.ml]
@@ -287,8 +289,8 @@ class _ImmediateArnoldi(_BaseArnoldi):
 
     scheme_id = "cgs2"
 
-    def __init__(self, op, start, capacity, ledger=None):
-        super().__init__(op, capacity, ledger)
+    def __init__(self, op, start, capacity, ledger=None, engine=None):
+        super().__init__(op, capacity, ledger, engine)
         e = self.eng
         self._v = torch.zeros(e.ld, dtype=torch.float64, device=e.vbuf.device)[: e.ml]
         self.last_coeffs = None

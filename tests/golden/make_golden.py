@@ -199,6 +199,34 @@ def main():
         out[f"{name}_incomplete"] = res.incomplete
         out[f"{name}_over"] = res.over_multiplicity
     np.savez_compressed(os.path.join(OUT, "krylov_schur.npz"), **out)
+
+    # -- small dense Schur services (host side of Krylov-Schur) ------------------
+    from kls.schur import (SchurForm, hessenberg_real_schur, hessenberg_reduce,
+                           move_blocks_front, schur_eigenvectors, sort_schur)
+    out = {}
+    srng = np.random.Generator(np.random.PCG64(4242))
+    for i, n in enumerate((1, 2, 3, 5, 8, 13, 21, 30, 30, 45)):
+        a = srng.standard_normal((n, n))
+        if i == 8:  # clustered real spectrum plus a rotation block
+            q = np.linalg.qr(srng.standard_normal((n, n)))[0]
+            d = np.diag(np.repeat(np.arange(1.0, 11.0), 3))
+            d[0, 1], d[1, 0] = 0.5, -0.5
+            a = q @ d @ q.T
+        h, u = hessenberg_reduce(a)
+        f = hessenberg_real_schur(h)
+        sel = srng.random(len(f.blocks())) < 0.4
+        g = SchurForm(f.t.copy(), f.z.copy())
+        moved = move_blocks_front(g, sel)
+        vals, vecs = schur_eigenvectors(g)
+        srt = SchurForm(f.t.copy(), f.z.copy())
+        sort_schur(srt, lambda lam: lam.real)
+        out[f"a{i}"], out[f"h{i}"], out[f"u{i}"] = a, h, u
+        out[f"t{i}"], out[f"z{i}"] = f.t, f.z
+        out[f"sel{i}"], out[f"moved{i}"] = sel, moved
+        out[f"mt{i}"], out[f"mz{i}"] = g.t, g.z
+        out[f"vals{i}"], out[f"vecs{i}"] = vals, vecs
+        out[f"st{i}"], out[f"sz{i}"] = srt.t, srt.z
+    np.savez_compressed(os.path.join(OUT, "schur.npz"), **out)
     print("golden fixtures written to", OUT)
 
 

@@ -1,0 +1,75 @@
+"""Krylov-Schur on the device against the reference's golden runs:
+identical lock histories and restart counts, Ritz values within 1e-9
+relative, locked pairs passing an explicit residual recompute."""
+
+import numpy as np
+import pytest
+
+from conftest import golden
+
+pytestmark = pytest.mark.gpu
+
+
+def kls():
+    import paper_2104_01253_b200 as k
+
+    return k
+
+
+@pytest.mark.parametrize("name,k,mb,seed,rst,scheme", [
+    ("k5", 5, 25, 3, 100, "dcgs2"), ("k8", 8, 30, 11, 8, "dcgs2"),
+    ("k10", 10, 20, 5, 30, "dcgs2"), ("k10c", 10, 20, 5, 30, "cgs2")])
+def test_krylov_schur_matches_reference(cuda, name, k, mb, seed, rst, scheme):
+    K = kls()
+    g = golden("krylov_schur.npz")
+    spec = K.ManteuffelSpec(k=k)
+    op = K.CsrOperator(K.manteuffel_build(spec))
+    cfg = K.KrylovSchurConfig(max_basis=mb, tol=1e-7, scheme=scheme, max_restarts=rst)
+    res = K.krylov_schur_run(op, cfg, seed=seed, exact=K.manteuffel_eigenvalues(spec))
+    assert list(res.lock_history) == list(g[f"{name}_lock_history"])
+    assert res.restarts == g[f"{name}_restarts"]
+    assert res.invariant_dim == g[f"{name}_invariant_dim"]
+    assert res.incomplete == bool(g[f"{name}_incomplete"])
+    assert res.over_multiplicity == bool(g[f"{name}_over"])
+    ref = g[f"{name}_values"]
+    assert res.values.shape == ref.shape
+    assert np.max(np.abs(res.values - ref) / np.abs(ref)) <= 1e-9
+    dense = op.to_dense()
+    Z = res.vectors.cpu().numpy()
+    for i, lam in enumerate(res.values):
+        z = Z[:, i]
+        assert np.linalg.norm(dense @ z - lam * z) <= 20 * cfg.tol
+
+
+def test_k5_full_spectrum_exact_multiplicities(cuda):
+    K = kls()
+    spec = K.ManteuffelSpec(k=5)
+    op = K.CsrOperator(K.manteuffel_build(spec))
+    table = K.manteuffel_eigenvalues(spec)
+    res = K.krylov_schur_run(op, K.KrylovSchurConfig(max_basis=25, tol=1e-7, scheme="dcgs2"),
+                             seed=3, exact=table)
+    assert res.invariant_dim == 25 and not res.over_multiplicity
+    assert K.match_eigenvalues(res.values.real, table, 1e-7).n_matched == 25
+
+
+def test_diagonal_and_rotation_operators(cuda, rng):
+    K = kls()
+    op = K.DenseOperator(np.diag(np.arange(1.0, 11.0)))
+    res = K.krylov_schur_run(op, K.KrylovSchurConfig(max_basis=10, tol=1e-7, scheme="cgs2"), 42)
+    assert res.invariant_dim == 10 and not res.incomplete
+    assert np.allclose(np.sort(res.values.real), np.arange(1.0, 11.0), atol=1e-12)
+    blocks = []
+    for t in (0.3, 1.1, 2.0):
+        c, s = np.cos(t), np.sin(t)
+        blocks.append(np.array([[c, -s], [s, c]]) * (1.0 + t))
+    a = np.zeros((8, 8))
+    for i, blk in enumerate(blocks):
+        a[2 * i : 2 * i + 2, 2 * i : 2 * i + 2] = blk
+    a[6, 6], a[7, 7] = 0.5, -0.25
+    q = np.linalg.qr(rng.standard_normal((8, 8)))[0]
+    res = K.krylov_schur_run(K.DenseOperator(q @ a @ q.T),
+                             K.KrylovSchurConfig(max_basis=8, tol=1e-8, scheme="dcgs2"), seed=1)
+    assert res.invariant_dim == 8
+    got = np.sort_complex(res.values)
+    want = np.sort_complex(np.linalg.eigvals(a))
+    assert np.max(np.abs(got - want)) <= 1e-8
