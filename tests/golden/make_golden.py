@@ -198,6 +198,11 @@ def main():
         out[f"{name}_invariant_dim"] = res.invariant_dim
         out[f"{name}_incomplete"] = res.incomplete
         out[f"{name}_over"] = res.over_multiplicity
+        # the reference's own sensitivity: the same matrix applied as a
+        # DenseOperator (only the matvec summation order changes)
+        alt = kls.krylov_schur_run(kls.DenseOperator(op.to_dense()), cfg, seed=seed)
+        out[f"{name}_alt_lock_history"] = np.array(alt.lock_history)
+        out[f"{name}_alt_values"] = alt.values
     np.savez_compressed(os.path.join(OUT, "krylov_schur.npz"), **out)
 
     # -- small dense Schur services (host side of Krylov-Schur) ------------------
