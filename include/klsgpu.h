@@ -41,6 +41,11 @@ int kls_version(void);
 const char* kls_last_error(void);
 /* SM count of the current device (grid sizing). */
 int kls_device_sm_count(void);
+/* cudaStreamSynchronize(stream): the one host wait of a DCGS2 step. */
+int kls_stream_sync(void* stream);
+/* Device address of page-locked host memory, so a reduction can deposit its
+ * 2j+3 scalars straight into a pinned host buffer (no D2H copy call). */
+int kls_host_device_ptr(void* host, void** dev);
 
 /* Bytes of reduction workspace that cover any call with <= kmax basis
  * columns on the current device.  Zero it once before first use; every
@@ -75,6 +80,12 @@ int kls_gram_dcgs2(const double* Q, int64_t ldq, int64_t m, int32_t j, const dou
 int kls_dcgs2_update(double* Q, int64_t ldq, int64_t m, int32_t j, double* w, const double* aw,
                      const double* coef, double alpha, int32_t divide, void* stream);
 
+/* kls_dcgs2_update with the 2j+1 coefficients in HOST memory: they are
+ * carried in the kernel launch (2j+1 <= 2048), so a step needs no H2D copy. */
+int kls_dcgs2_update_host(double* Q, int64_t ldq, int64_t m, int32_t j, double* w,
+                          const double* aw, const double* coef_host, double alpha, int32_t divide,
+                          void* stream);
+
 /* Y(:,0:l) <- scale*Y + sign*B(:,0:k) S — kernels.mv_times_mat_add_mv
  * (kernels.py:63-84) for l = 1 or 2; S is k x l column-major on the device.
  * nrm_out (optional, device) receives ||Y(:, l-1)||^2 of the result, fusing
@@ -82,6 +93,11 @@ int kls_dcgs2_update(double* Q, int64_t ldq, int64_t m, int32_t j, double* w, co
 int kls_mv_times_mat_add_mv(double* Y, int64_t ldy, int64_t m, int32_t l, const double* B,
                             int64_t ldb, int32_t k, const double* S, double sign, double scale,
                             double* nrm_out, void* ws, size_t ws_bytes, void* stream);
+/* Same with S in HOST memory (k*l <= 2048), carried in the launch. */
+int kls_mv_times_mat_add_mv_host(double* Y, int64_t ldy, int64_t m, int32_t l, const double* B,
+                                 int64_t ldb, int32_t k, const double* S_host, double sign,
+                                 double scale, double* nrm_out, void* ws, size_t ws_bytes,
+                                 void* stream);
 
 /* y = A x for CSR rows (int64 row pointer, int32 columns, fp64 values),
  * bit-identical to CsrMatrix.matvec (problems.py:127-136): products, then

@@ -1,10 +1,17 @@
 """Per-expansion device engine: one basis block, one stream, one reduction
-workspace, one pinned staging pair, and the communicator of the operator.
+workspace, one pinned result buffer, and the communicator of the operator.
 
-Every reducing call here is: kernel -> (allreduce over ranks) -> one small
-D2H of the reduced scalars.  That D2H is the only host synchronization of a
-DCGS2 step.
+Every reducing call is: kernel -> (allreduce over ranks) -> the reduced
+scalars on the host.  On one GPU the reducing kernel's last CTA writes its
+2j+3 results straight into page-locked host memory (device-mapped), so the
+only host action per step is one stream synchronize; the update's
+coefficients ride in the kernel launch (kls_*_host).  That is the single
+host synchronization of a DCGS2 step.
+
+The engine binds the stream that is current when it is created.
 """
+
+import ctypes
 
 import numpy as np
 import torch
@@ -12,33 +19,49 @@ import torch
 from . import _lib, runtime, trace
 from .errors import DimensionError
 
+_PACK = 2048  # coefficients that fit in a kernel launch (kls_*_host)
+
+
+def _mapped(host_ptr):
+    """Device address of a page-locked host address (identical under UVA)."""
+    dptr = ctypes.c_void_p()
+    try:
+        _lib.call("kls_host_device_ptr", host_ptr, ctypes.byref(dptr))
+        return dptr.value
+    except _lib.KlsGpuError:
+        return host_ptr
+
 
 class Engine:
     def __init__(self, op, capacity):
         self.op = op
         self.comm = op.comm
+        self.world = op.comm.world
         self.m = op.shape[0]  # global rows (guards, ledger flops)
         self.ml = op.m_local
         self.ld = runtime.pad_rows(self.ml)
         self.capacity = capacity
         dev = runtime.device()
+        _lib.load()
+        self.st = runtime.stream_handle()
         # column-major basis: row c of the buffer is column c of Q.  Not
         # zero-filled (a 100 GB memset per expansion): columns are written
         # before they are read, and zero_col() pads a breakdown column.
         self.vbuf = torch.empty((capacity, self.ld), dtype=torch.float64, device=dev)
-        self.stage = runtime.Staging(2 * capacity + 8)
-        runtime.workspace(capacity + 1)  # size it once up front
+        self.qptr = self.vbuf.data_ptr()
+        nres = 2 * capacity + 8
+        self.stage = runtime.Staging(nres)
+        # pinned result buffer the reducing kernels write into directly
+        self.res_host = torch.zeros(nres, dtype=torch.float64, pin_memory=True)
+        self.res_np = self.res_host.numpy()
+        self.res_dev = _mapped(self.res_host.data_ptr())
+        self.ws, self.wsb = runtime.workspace_for(self.st, capacity + 1)
 
-    @property
-    def wsp(self):
-        """(pointer, bytes) of the stream's reduction workspace."""
-        return runtime.workspace(self.capacity + 1)
-
+    # -- views ----------------------------------------------------------------
     def zero_col(self, c):
         if c < self.capacity:
             self.vbuf[c].zero_()
 
-    # -- views ----------------------------------------------------------------
     def col(self, c):
         return self.vbuf[c, : self.ml]
 
@@ -46,43 +69,53 @@ class Engine:
         """(m_local, k) column-major view of the first k columns."""
         return self.vbuf[:k, : self.ml].T
 
-    @property
-    def qptr(self):
-        return self.vbuf.data_ptr()
-
-    @property
-    def st(self):
-        return runtime.stream_handle()
-
     # -- reductions -----------------------------------------------------------
+    def _out(self, count):
+        """Where a reducing kernel writes `count` results."""
+        if self.world == 1:
+            if count > self.res_np.size:
+                raise DimensionError("result buffer too small")
+            return self.res_dev
+        self.stage.ensure(count)
+        return self.stage.dev_out.data_ptr()
+
     def _finish(self, count):
+        if self.world == 1:
+            _lib.call("kls_stream_sync", self.st)
+            runtime.XFER["d2h"] += 8 * count
+            return self.res_np[:count].copy()
         out = self.stage.dev_out[:count]
-        if self.comm.world > 1:
-            with trace.span("allreduce"):
+        rec = trace._active
+        if rec is not None and rec.events:
+            with rec.span("allreduce"):
                 self.comm.allreduce_(out)
+        else:
+            self.comm.allreduce_(out)
         return self.stage.fetch(count)
 
     def gram_dcgs2(self, j, w, aw):
         """[Q(:,0:j), w]^T [w, aw] and aw.aw over all ranks: 2j+3 values."""
-        self.stage.ensure(2 * j + 3)
-        ws, wsb = self.wsp
-        trace.note("gram", 8 * self.ml * (j + 2))
-        with trace.span("gram"):
+        out = self._out(2 * j + 3)
+        rec = trace._active
+        if rec is None:
             _lib.call("kls_gram_dcgs2", self.qptr, self.ld, self.ml, j, w.data_ptr(),
-                      aw.data_ptr(), self.stage.dev_out.data_ptr(), ws, wsb, self.st)
+                      aw.data_ptr(), out, self.ws, self.wsb, self.st)
+        else:
+            rec.note("gram", 8 * self.ml * (j + 2))
+            with rec.span("gram"):
+                _lib.call("kls_gram_dcgs2", self.qptr, self.ld, self.ml, j, w.data_ptr(),
+                          aw.data_ptr(), out, self.ws, self.wsb, self.st)
         return self._finish(2 * j + 3)
 
     def project(self, k, x, xnorm=True):
         """Q(:,0:k)^T x (and x.x) over all ranks: k (+1) values."""
         n = k + (1 if xnorm else 0)
-        self.stage.ensure(max(n, 1))
         if n == 0:
             return np.zeros(0)
-        ws, wsb = self.wsp
+        out = self._out(n)
         trace.note("project", 8 * self.ml * (k + 1))
         _lib.call("kls_mv_trans_mv", self.qptr if k else None, self.ld, self.ml, k, None,
-                  x.data_ptr(), None, 1, 1 if xnorm else 0, self.stage.dev_out.data_ptr(),
-                  ws, wsb, self.st)
+                  x.data_ptr(), None, 1, 1 if xnorm else 0, out, self.ws, self.wsb, self.st)
         return self._finish(n)
 
     def sqnorm(self, x):
@@ -90,21 +123,38 @@ class Engine:
 
     # -- updates ----------------------------------------------------------------
     def dcgs2_update(self, j, w, aw, c, t, alpha, divide):
-        coef = self.stage.push(np.concatenate([c, t]))
-        trace.note("update", 8 * self.ml * (j + 4))
-        with trace.span("update"):
-            _lib.call("kls_dcgs2_update", self.qptr, self.ld, self.ml, j, w.data_ptr(),
-                      aw.data_ptr(), coef.data_ptr(), float(alpha), 1 if divide else 0, self.st)
+        coef = np.concatenate([c, t])
+        rec = trace._active
+        if rec is not None:
+            rec.note("update", 8 * self.ml * (j + 4))
+        if coef.size <= _PACK:
+            runtime.XFER["h2d"] += 8 * coef.size
+            args = ("kls_dcgs2_update_host", self.qptr, self.ld, self.ml, j, w.data_ptr(),
+                    aw.data_ptr(), coef.ctypes.data, float(alpha), 1 if divide else 0, self.st)
+        else:
+            dev = self.stage.push(coef)
+            args = ("kls_dcgs2_update", self.qptr, self.ld, self.ml, j, w.data_ptr(),
+                    aw.data_ptr(), dev.data_ptr(), float(alpha), 1 if divide else 0, self.st)
+        if rec is not None and rec.events:
+            with rec.span("update"):
+                _lib.call(*args)
+        else:
+            _lib.call(*args)
 
     def subtract_projection(self, y, k, coef, want_norm=False):
         """y <- y - Q(:,0:k) coef; optionally return ||y||^2 over all ranks."""
-        dev_coef = self.stage.push(coef) if k else None
-        nrm = self.stage.dev_out.data_ptr() if want_norm else None
-        ws, wsb = self.wsp
+        nrm = self._out(1) if want_norm else None
         trace.note("mtm", 8 * self.ml * (k + 2))
-        _lib.call("kls_mv_times_mat_add_mv", y.data_ptr(), self.ld, self.ml, 1,
-                  self.qptr if k else None, self.ld, k,
-                  dev_coef.data_ptr() if k else None, -1.0, 1.0, nrm, ws, wsb, self.st)
+        if k <= _PACK:
+            c = np.ascontiguousarray(coef, dtype=np.float64) if k else None
+            runtime.XFER["h2d"] += 8 * k
+            _lib.call("kls_mv_times_mat_add_mv_host", y.data_ptr(), self.ld, self.ml, 1,
+                      self.qptr if k else None, self.ld, k, c.ctypes.data if k else None,
+                      -1.0, 1.0, nrm, self.ws, self.wsb, self.st)
+        else:
+            dev = self.stage.push(coef)
+            _lib.call("kls_mv_times_mat_add_mv", y.data_ptr(), self.ld, self.ml, 1, self.qptr,
+                      self.ld, k, dev.data_ptr(), -1.0, 1.0, nrm, self.ws, self.wsb, self.st)
         if want_norm:
             return float(self._finish(1)[0])
         return None
@@ -116,7 +166,7 @@ class Engine:
     # -- operator -----------------------------------------------------------------
     def apply(self, x, y):
         """Uncounted operator application (the caller bumps op.napply)."""
-        self.op.apply_into(x, y)
+        self.op.apply_into(x, y, self.st)
 
     def check_capacity(self, n):
         if n > self.capacity:

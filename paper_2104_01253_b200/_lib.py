@@ -23,11 +23,18 @@ SIGNATURES = {
     "kls_version": (ctypes.c_int, []),
     "kls_last_error": (ctypes.c_char_p, []),
     "kls_device_sm_count": (ctypes.c_int, []),
+    "kls_stream_sync": (ctypes.c_int, [c_dp]),
+    "kls_host_device_ptr": (ctypes.c_int, [c_dp, ctypes.POINTER(ctypes.c_void_p)]),
     "kls_workspace_bytes": (sz, [i64, i32]),
     "kls_mv_trans_mv": (ctypes.c_int, [c_dp, i64, i64, i32, c_dp, c_dp, c_dp, i32, i32, c_dp, c_dp, sz, c_dp]),
     "kls_gram_dcgs2": (ctypes.c_int, [c_dp, i64, i64, i32, c_dp, c_dp, c_dp, c_dp, sz, c_dp]),
     "kls_dcgs2_update": (ctypes.c_int, [c_dp, i64, i64, i32, c_dp, c_dp, c_dp, f64, i32, c_dp]),
+    "kls_dcgs2_update_host": (ctypes.c_int, [c_dp, i64, i64, i32, c_dp, c_dp, c_dp, f64, i32, c_dp]),
     "kls_mv_times_mat_add_mv": (
+        ctypes.c_int,
+        [c_dp, i64, i64, i32, c_dp, i64, i32, c_dp, f64, f64, c_dp, c_dp, sz, c_dp],
+    ),
+    "kls_mv_times_mat_add_mv_host": (
         ctypes.c_int,
         [c_dp, i64, i64, i32, c_dp, i64, i32, c_dp, f64, f64, c_dp, c_dp, sz, c_dp],
     ),

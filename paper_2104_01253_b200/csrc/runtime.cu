@@ -43,3 +43,19 @@ KLS_API int kls_version(void) { return 1; }
 KLS_API const char* kls_last_error(void) { return kls::g_err; }
 
 KLS_API int kls_device_sm_count(void) { return kls::sm_count(); }
+
+// Block the host until all work queued on `stream` has finished.
+KLS_API int kls_stream_sync(void* stream) {
+  cudaError_t e = cudaStreamSynchronize(static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return kls::fail(KLS_ECUDA, "stream sync: %s", cudaGetErrorString(e));
+  return KLS_OK;
+}
+
+// Device-side address of page-locked host memory (for kernels that write
+// their few reduced scalars straight to the host).
+KLS_API int kls_host_device_ptr(void* host, void** dev) {
+  if (host == nullptr || dev == nullptr) return kls::fail(KLS_EINVAL, "host_device_ptr: null");
+  cudaError_t e = cudaHostGetDevicePointer(dev, host, 0);
+  if (e != cudaSuccess) return kls::fail(KLS_ECUDA, "host_device_ptr: %s", cudaGetErrorString(e));
+  return KLS_OK;
+}

@@ -14,6 +14,8 @@
 // grid the neighbouring x-planes of other ranks come in through x_lo / x_hi.
 #include "common.cuh"
 
+#include <cstdlib>
+
 namespace {
 
 using namespace kls;
@@ -159,11 +161,16 @@ KLS_API int kls_stencil7(const double* x, const double* x_lo, const double* x_hi
   if (ny > INT32_MAX || nz > INT32_MAX) return fail(KLS_EINVAL, "stencil7: ny, nz must fit int32");
   const int64_t plane = ny * nz;
   const int64_t pblocks = ceil_div(plane, kThreads);
-  // enough x-chunks for ~8 resident CTAs per SM, each chunk >= 8 planes
-  int64_t chunks = std::max<int64_t>(1, ceil_div(8LL * sm_count(), pblocks));
-  chunks = std::min<int64_t>(chunks, std::max<int64_t>(1, nx / 8));
-  const int64_t xchunk = ceil_div(nx, chunks);
-  chunks = ceil_div(nx, xchunk);
+  // x-chunk length: short enough for several waves of CTAs (latency hiding),
+  // long enough that the two extra window loads per chunk stay cheap
+  static int env_chunk = -1;
+  if (env_chunk < 0) {
+    const char* e = getenv("KLS_STENCIL_XCHUNK");
+    env_chunk = e ? atoi(e) : 0;
+  }
+  int64_t xchunk = env_chunk > 0 ? env_chunk : 16;
+  xchunk = std::min<int64_t>(xchunk, nx);
+  int64_t chunks = ceil_div(nx, xchunk);
   if (pblocks > INT32_MAX || chunks > 65535) return fail(KLS_EINVAL, "stencil7: grid too large");
   dim3 grid(static_cast<unsigned>(pblocks), static_cast<unsigned>(chunks));
   stencil7_kernel<<<grid, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(

@@ -13,11 +13,22 @@
 // (fused norm for the CGS2 comparator and the DCGS2 flush).
 #include "reduce.cuh"
 
+#include <cstring>
+
 namespace {
 
 using namespace kls;
 
 constexpr int kCols = 4;        // Q columns streamed together
+
+// Small host coefficient vectors travel inside the launch (kernel parameter
+// space, up to 32 KB on sm_70+ with CUDA >= 12.1) instead of a separate H2D
+// copy: one API call per update.  __grid_constant__ lets the kernel index the
+// pack in place.  NC == 0 selects the device-pointer variant.
+template <int NC>
+struct CoefPack {
+  double v[NC > 0 ? NC : 1];
+};
 constexpr int kUpdRP = 2;       // row pairs per lane per chunk
 constexpr int kUpdBlocksPerSm = 3;
 
@@ -85,13 +96,15 @@ __device__ __forceinline__ void upd_chunk(const UpdParams& p, const double2* sct
   }
 }
 
-template <int RP>
-__global__ void __launch_bounds__(kThreads, kUpdBlocksPerSm) dcgs2_update_kernel(UpdParams p) {
+template <int RP, int NC>
+__global__ void __launch_bounds__(kThreads, kUpdBlocksPerSm)
+    dcgs2_update_kernel(UpdParams p, const __grid_constant__ CoefPack<NC> pk) {
   extern __shared__ double2 sct[];  // (c_k, t_k), padded to a multiple of kCols
+  const double* coef = NC > 0 ? pk.v : p.coef;
   const int jpad = (p.j + kCols - 1) / kCols * kCols;
   for (int k = threadIdx.x; k < jpad; k += kThreads)
-    sct[k] = k < p.j ? make_double2(p.coef[k], p.coef[p.j + k]) : make_double2(0.0, 0.0);
-  const double tj = p.coef[2 * p.j];
+    sct[k] = k < p.j ? make_double2(coef[k], coef[p.j + k]) : make_double2(0.0, 0.0);
+  const double tj = coef[2 * p.j];
   __syncthreads();
   constexpr int64_t WROWS = 64 * RP;
   constexpr int64_t CROWS = WROWS * kWarps;
@@ -184,13 +197,15 @@ __device__ __forceinline__ void mtm_chunk(const MtmParams& p, const double* ss, 
   }
 }
 
-template <int L>
-__global__ void __launch_bounds__(kThreads, kUpdBlocksPerSm) mtm_kernel(MtmParams p) {
+template <int L, int NC>
+__global__ void __launch_bounds__(kThreads, kUpdBlocksPerSm)
+    mtm_kernel(MtmParams p, const __grid_constant__ CoefPack<NC> pk) {
   extern __shared__ double ss[];  // L x (k + kCols), zero-padded
+  const double* S = NC > 0 ? pk.v : p.S;
   const int ldss = p.k + kCols;
   for (int i = threadIdx.x; i < L * ldss; i += kThreads) {
     const int t = i / ldss, kk = i % ldss;
-    ss[i] = kk < p.k ? p.S[t * p.k + kk] : 0.0;
+    ss[i] = kk < p.k ? S[t * p.k + kk] : 0.0;
   }
   __syncthreads();
   constexpr int64_t WROWS = 64 * kUpdRP;
@@ -229,6 +244,81 @@ int set_smem(const void* fn, size_t smem) {
 
 bool misaligned(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) != 0; }
 
+template <int NC>
+int launch_update(const UpdParams& p, const double* host_coef, cudaStream_t st) {
+  CoefPack<NC> pk;
+  if (NC > 0) std::memcpy(pk.v, host_coef, sizeof(double) * (2 * p.j + 1));
+  const size_t smem = sizeof(double2) * static_cast<size_t>((p.j + kCols - 1) / kCols * kCols + 1);
+  int rc = set_smem(reinterpret_cast<const void*>(dcgs2_update_kernel<kUpdRP, NC>), smem);
+  if (rc) return rc;
+  const int grid = grid_for(p.m, 64 * kUpdRP * kWarps, kUpdBlocksPerSm);
+  dcgs2_update_kernel<kUpdRP, NC><<<grid, kThreads, smem, st>>>(p, pk);
+  return check_launch("dcgs2_update_kernel");
+}
+
+int update_common(double* Q, int64_t ldq, int64_t m, int32_t j, double* w, const double* aw,
+                  const double* coef, double alpha, int32_t divide, bool host, void* stream) {
+  if (Q == nullptr || w == nullptr || aw == nullptr || coef == nullptr || m < 0 || j < 0 ||
+      ldq < m || (ldq & 1))
+    return fail(KLS_EINVAL, "dcgs2_update: bad arguments");
+  if (misaligned(Q) || misaligned(w) || misaligned(aw))
+    return fail(KLS_EINVAL, "dcgs2_update: operands must be 16-byte aligned");
+  UpdParams p{Q, ldq, m, j, w, aw, host ? nullptr : coef, alpha, divide};
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int nc = 2 * j + 1;
+  if (!host) return launch_update<0>(p, nullptr, st);
+  if (nc <= 32) return launch_update<32>(p, coef, st);
+  if (nc <= 128) return launch_update<128>(p, coef, st);
+  if (nc <= 512) return launch_update<512>(p, coef, st);
+  if (nc <= 2048) return launch_update<2048>(p, coef, st);
+  return fail(KLS_EINVAL, "dcgs2_update_host: 2j+1 = %d coefficients exceed the 2048 launch "
+              "pack; use kls_dcgs2_update with a device array", nc);
+}
+
+template <int L, int NC>
+int launch_mtm(const MtmParams& p, const double* host_s, cudaStream_t st) {
+  CoefPack<NC> pk;
+  if (NC > 0) std::memcpy(pk.v, host_s, sizeof(double) * p.k * L);
+  const size_t smem = sizeof(double) * static_cast<size_t>(L) * (p.k + kCols);
+  int rc = set_smem(reinterpret_cast<const void*>(mtm_kernel<L, NC>), smem);
+  if (rc) return rc;
+  const int grid = grid_for(p.m, 64 * kUpdRP * kWarps, kUpdBlocksPerSm);
+  mtm_kernel<L, NC><<<grid, kThreads, smem, st>>>(p, pk);
+  return check_launch("mtm_kernel");
+}
+
+template <int L>
+int mtm_dispatch(const MtmParams& p, const double* host_s, cudaStream_t st) {
+  const int n = p.k * L;
+  if (host_s == nullptr) return launch_mtm<L, 0>(p, nullptr, st);
+  if (n <= 32) return launch_mtm<L, 32>(p, host_s, st);
+  if (n <= 128) return launch_mtm<L, 128>(p, host_s, st);
+  if (n <= 512) return launch_mtm<L, 512>(p, host_s, st);
+  if (n <= 2048) return launch_mtm<L, 2048>(p, host_s, st);
+  return fail(KLS_EINVAL, "mv_times_mat_add_mv_host: %d coefficients exceed the launch pack", n);
+}
+
+int mtm_common(double* Y, int64_t ldy, int64_t m, int32_t l, const double* B, int64_t ldb,
+               int32_t k, const double* S, double sign, double scale, double* nrm_out, void* ws,
+               size_t ws_bytes, bool host, void* stream) {
+  if (Y == nullptr || m < 0 || k < 0 || (l != 1 && l != 2) || (l == 2 && (ldy < m || (ldy & 1))) ||
+      (k > 0 && (B == nullptr || S == nullptr || ldb < m || (ldb & 1))))
+    return fail(KLS_EINVAL, "mv_times_mat_add_mv: bad arguments (m=%lld k=%d l=%d)",
+                (long long)m, k, l);
+  if (misaligned(Y) || misaligned(B)) return fail(KLS_EINVAL, "mv_times_mat_add_mv: misaligned");
+  const int grid = grid_for(m, 64 * kUpdRP * kWarps, kUpdBlocksPerSm);
+  MtmParams p{Y, ldy, m, l, B, ldb, k, host ? nullptr : S, sign, scale, red_ws(ws), nrm_out};
+  if (nrm_out != nullptr && (ws == nullptr || !red_ws_fits(ws_bytes, grid, 1)))
+    return fail(KLS_ENOSPC, "mv_times_mat_add_mv: workspace too small for the fused norm");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const double* hs = host && k > 0 ? S : nullptr;
+  if (host && k == 0) {
+    static const double zero = 0.0;
+    hs = &zero;
+  }
+  return l == 1 ? mtm_dispatch<1>(p, hs, st) : mtm_dispatch<2>(p, hs, st);
+}
+
 }  // namespace
 
 // Fused DCGS2 step update (see the file header).  `coef` is a device array
@@ -238,18 +328,15 @@ bool misaligned(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) !=
 KLS_API int kls_dcgs2_update(double* Q, int64_t ldq, int64_t m, int32_t j, double* w,
                              const double* aw, const double* coef, double alpha, int32_t divide,
                              void* stream) {
-  if (Q == nullptr || w == nullptr || aw == nullptr || coef == nullptr || m < 0 || j < 0 ||
-      ldq < m || (ldq & 1))
-    return fail(KLS_EINVAL, "dcgs2_update: bad arguments");
-  if (misaligned(Q) || misaligned(w) || misaligned(aw))
-    return fail(KLS_EINVAL, "dcgs2_update: operands must be 16-byte aligned");
-  const size_t smem = sizeof(double2) * static_cast<size_t>((j + kCols - 1) / kCols * kCols + 1);
-  int rc = set_smem(reinterpret_cast<const void*>(dcgs2_update_kernel<kUpdRP>), smem);
-  if (rc) return rc;
-  UpdParams p{Q, ldq, m, j, w, aw, coef, alpha, divide};
-  const int grid = grid_for(m, 64 * kUpdRP * kWarps, kUpdBlocksPerSm);
-  dcgs2_update_kernel<kUpdRP><<<grid, kThreads, smem, static_cast<cudaStream_t>(stream)>>>(p);
-  return check_launch("dcgs2_update_kernel");
+  return update_common(Q, ldq, m, j, w, aw, coef, alpha, divide, false, stream);
+}
+
+// Same with the coefficients in HOST memory: they ride in the kernel launch
+// (2j+1 <= 2048), so the step needs no separate H2D copy.
+KLS_API int kls_dcgs2_update_host(double* Q, int64_t ldq, int64_t m, int32_t j, double* w,
+                                  const double* aw, const double* coef_host, double alpha,
+                                  int32_t divide, void* stream) {
+  return update_common(Q, ldq, m, j, w, aw, coef_host, alpha, divide, true, stream);
 }
 
 // Y(:, 0:l) <- scale * Y + sign * B(:, 0:k) S  with S (k x l, column-major,
@@ -259,24 +346,15 @@ KLS_API int kls_mv_times_mat_add_mv(double* Y, int64_t ldy, int64_t m, int32_t l
                                     int64_t ldb, int32_t k, const double* S, double sign,
                                     double scale, double* nrm_out, void* ws, size_t ws_bytes,
                                     void* stream) {
-  if (Y == nullptr || m < 0 || k < 0 || (l != 1 && l != 2) || (l == 2 && (ldy < m || (ldy & 1))) ||
-      (k > 0 && (B == nullptr || S == nullptr || ldb < m || (ldb & 1))))
-    return fail(KLS_EINVAL, "mv_times_mat_add_mv: bad arguments (m=%lld k=%d l=%d)",
-                (long long)m, k, l);
-  if (misaligned(Y) || misaligned(B)) return fail(KLS_EINVAL, "mv_times_mat_add_mv: misaligned");
-  const int grid = grid_for(m, 64 * kUpdRP * kWarps, kUpdBlocksPerSm);
-  MtmParams p{Y, ldy, m, l, B, ldb, k, S, sign, scale, red_ws(ws), nrm_out};
-  if (nrm_out != nullptr && (ws == nullptr || !red_ws_fits(ws_bytes, grid, 1)))
-    return fail(KLS_ENOSPC, "mv_times_mat_add_mv: workspace too small for the fused norm");
-  const size_t smem = sizeof(double) * static_cast<size_t>(l) * (k + kCols);
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  int rc;
-  if (l == 1) {
-    if ((rc = set_smem(reinterpret_cast<const void*>(mtm_kernel<1>), smem))) return rc;
-    mtm_kernel<1><<<grid, kThreads, smem, st>>>(p);
-  } else {
-    if ((rc = set_smem(reinterpret_cast<const void*>(mtm_kernel<2>), smem))) return rc;
-    mtm_kernel<2><<<grid, kThreads, smem, st>>>(p);
-  }
-  return check_launch("mtm_kernel");
+  return mtm_common(Y, ldy, m, l, B, ldb, k, S, sign, scale, nrm_out, ws, ws_bytes, false, stream);
+}
+
+// Same with S in HOST memory (k*l <= 2048), carried in the launch.
+KLS_API int kls_mv_times_mat_add_mv_host(double* Y, int64_t ldy, int64_t m, int32_t l,
+                                         const double* B, int64_t ldb, int32_t k,
+                                         const double* S_host, double sign, double scale,
+                                         double* nrm_out, void* ws, size_t ws_bytes,
+                                         void* stream) {
+  return mtm_common(Y, ldy, m, l, B, ldb, k, S_host, sign, scale, nrm_out, ws, ws_bytes, true,
+                    stream);
 }

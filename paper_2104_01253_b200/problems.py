@@ -127,10 +127,13 @@ class LinearOperator:
         self.apply_into(xl, y)
         return y
 
-    def apply_into(self, x, y):
-        """Uncounted y = A x.  ``x`` is a HaloVector (no copy) or a device
-        tensor of the local rows (copied into scratch halo storage when the
-        operator needs neighbour rows)."""
+    def apply_into(self, x, y, st=None):
+        """Uncounted y = A x on stream ``st`` (default: the current stream).
+        ``x`` is a HaloVector (no copy) or a device tensor of the local rows
+        (copied into scratch halo storage when the operator needs neighbour
+        rows)."""
+        if st is None:
+            st = runtime.stream_handle()
         if not isinstance(x, HaloVector):
             if self._needs_halo():
                 if self._scratch is None:
@@ -140,9 +143,13 @@ class LinearOperator:
             else:
                 x = _PlainVector(x)
         self._exchange(x)
-        trace.note("apply", self.apply_bytes())
-        with trace.span("apply"):
-            self._launch(x, y)
+        rec = trace._active
+        if rec is None:
+            self._launch(x, y, st)
+        else:
+            rec.note("apply", self.apply_bytes())
+            with rec.span("apply"):
+                self._launch(x, y, st)
 
     def apply_bytes(self):
         """Algorithmic HBM bytes of one application (x read, y written)."""
@@ -154,7 +161,7 @@ class LinearOperator:
     def _exchange(self, x):
         pass
 
-    def _launch(self, x, y):
+    def _launch(self, x, y, st):
         raise NotImplementedError
 
     # -- norms / dense ------------------------------------------------------
@@ -254,9 +261,9 @@ class DenseOperator(LinearOperator):
         self.a = a
         self._dev = runtime.upload(np.ascontiguousarray(a))
 
-    def _launch(self, x, y):
+    def _launch(self, x, y, st):
         _lib.call("kls_dense_gemv", self._dev.data_ptr(), self.n, self.n, x.local.data_ptr(),
-                  y.data_ptr(), runtime.stream_handle())
+                  y.data_ptr(), st)
 
     def to_dense(self, max_order=None):
         return self.a.copy()
@@ -354,6 +361,9 @@ class CsrOperator(LinearOperator):
         self._rowptr = torch.from_numpy(csr.indptr[lo : hi + 1] - s).to(dev)
         self._col = torch.from_numpy((cols - base).astype(np.int32)).to(dev)
         self._val = torch.from_numpy(np.ascontiguousarray(csr.data[s:e])).to(dev)
+        self._rowptr_p = self._rowptr.data_ptr()
+        self._col_p = self._col.data_ptr()
+        self._val_p = self._val.data_ptr()
         self._plan = None
         if self.comm.world > 1:
             self._plan = self._halo_plan()
@@ -393,10 +403,9 @@ class CsrOperator(LinearOperator):
         """x and y, plus values (8), column indices (4) and row pointers (8)."""
         return 16 * self.m_local + 12 * int(self._col.numel()) + 8 * (self.m_local + 1)
 
-    def _launch(self, x, y):
-        _lib.call("kls_csr_spmv", self._rowptr.data_ptr(), self._col.data_ptr(),
-                  self._val.data_ptr(), self.m_local, x.ext_ptr, y.data_ptr(),
-                  runtime.stream_handle())
+    def _launch(self, x, y, st):
+        _lib.call("kls_csr_spmv", self._rowptr_p, self._col_p, self._val_p, self.m_local,
+                  x.ext_ptr, y.data_ptr(), st)
 
     def to_dense(self, max_order=4000):
         if self.n > max_order:
@@ -570,12 +579,12 @@ class StencilLaplace3D(LinearOperator):
                 ops.append(dist.P2POp(dist.irecv, x.hi, r + 1, group=g))
         _p2p(ops)
 
-    def _launch(self, x, y):
+    def _launch(self, x, y, st):
         _, ny, nz = self.dims
         lo = x.lo.data_ptr() if x.lo is not None else None
         hi = x.hi.data_ptr() if x.hi is not None else None
         _lib.call("kls_stencil7", x.local.data_ptr(), lo, hi, y.data_ptr(),
-                  self.x_hi - self.x_lo, ny, nz, runtime.stream_handle())
+                  self.x_hi - self.x_lo, ny, nz, st)
 
     def to_csr(self):
         """Host CSR with the same entries (for CSR-path runs and tests)."""

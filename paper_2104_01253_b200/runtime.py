@@ -26,11 +26,17 @@ def pad_rows(m):
     return max(ALIGN, (m + ALIGN - 1) // ALIGN * ALIGN)
 
 
+_cuda_ok = None
+
+
 def device():
-    if not torch.cuda.is_available():
-        raise RuntimeError(
-            "paper_2104_01253_b200 needs a CUDA device (B200, sm_100a); no CPU fallback exists"
-        )
+    global _cuda_ok
+    if not _cuda_ok:
+        if not torch.cuda.is_available():
+            raise RuntimeError(
+                "paper_2104_01253_b200 needs a CUDA device (B200, sm_100a); no CPU fallback exists"
+            )
+        _cuda_ok = True
     return torch.device("cuda", torch.cuda.current_device())
 
 
@@ -125,9 +131,13 @@ class Workspace:
         self._buf = None
         self._bytes = 0
         self._old = []
+        self._need = {}
 
     def get(self, kmax):
-        need = int(_lib.load().kls_workspace_bytes(0, int(max(kmax, 8))))
+        kmax = int(max(kmax, 8))
+        need = self._need.get(kmax)
+        if need is None:
+            need = self._need[kmax] = int(_lib.load().kls_workspace_bytes(0, kmax))
         if self._buf is None or need > self._bytes:
             if self._buf is not None:
                 self._old.append(self._buf)
@@ -140,7 +150,13 @@ _workspaces = {}
 
 
 def workspace(kmax):
-    key = (torch.cuda.current_device(), stream_handle())
+    return workspace_for(stream_handle(), kmax)
+
+
+def workspace_for(stream, kmax):
+    """(pointer, bytes) of the reduction workspace of `stream`.  Replaced
+    buffers stay alive, so a returned pointer remains valid."""
+    key = (torch.cuda.current_device(), stream)
     ws = _workspaces.get(key)
     if ws is None:
         ws = _workspaces[key] = Workspace()
