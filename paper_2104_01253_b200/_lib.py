@@ -47,6 +47,10 @@ SIGNATURES = {
     "kls_tsgemm_inplace": (ctypes.c_int, [c_dp, i64, i64, i32, c_dp, c_dp]),
 }
 
+# entry points that launch no kernel (not counted as GPU launches)
+_NO_LAUNCH = frozenset({"kls_version", "kls_last_error", "kls_device_sm_count", "kls_stream_sync",
+                        "kls_host_device_ptr", "kls_workspace_bytes"})
+
 _lock = threading.Lock()
 _lib = None
 _launches = 0  # kernel-launching calls made through this binding
@@ -90,7 +94,8 @@ def call(name, *args):
     if rc != 0:
         msg = lib.kls_last_error().decode(errors="replace")
         raise KlsGpuError(f"{name} failed ({rc}): {msg}")
-    _launches += 1
+    if name not in _NO_LAUNCH:
+        _launches += 1
     return rc
 
 
