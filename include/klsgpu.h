@@ -132,6 +132,33 @@ int kls_resid_norms(const double* b, const double* ax, const double* x, int64_t 
 int kls_tsgemm_inplace(double* V, int64_t ldv, int64_t m, int32_t k, const double* Z,
                        void* stream);
 
+/* ---- cross-GPU exchange over NVLink peer memory ---------------------------
+ * Symmetric buffers (same layout on every rank, mapped into every peer) of
+ * kls_peer_buffer_bytes(cap) bytes; bufs[r] is rank r's buffer as seen from
+ * this GPU.  All spins time out after 20 s and set *err instead of hanging. */
+size_t kls_peer_buffer_bytes(int32_t cap);
+
+/* The DCGS2 step's single global reduction (ledger site
+ * kernels.py:57-59) as a one-shot NVLink exchange: sum over ranks of nv
+ * doubles at src, accumulated in rank order (bitwise identical on all ranks),
+ * written to out (device or mapped host memory).  epoch: +1 per call, same on
+ * all ranks. */
+int kls_peer_allreduce(const double* src, int32_t nv, double* out, void* const* bufs, int32_t rank,
+                       int32_t world, int32_t cap, uint64_t epoch, int* err, void* stream);
+
+/* Raise this rank's halo flag (= epoch) in the buffers of the ranks set in
+ * target_mask, ordered after all prior work on the stream. */
+int kls_peer_signal(void* const* bufs, int32_t rank, int32_t world, int32_t target_mask,
+                    uint64_t epoch, void* stream);
+
+/* kls_stencil7 reading the neighbouring x-planes directly from peer memory
+ * (x_lo / x_hi peer-mapped, NULL at the physical boundary) once the lower /
+ * upper neighbour's halo flag in mybuf reaches epoch — the halo exchange of
+ * the row-sharded operator (problems.py:296-305) fused into the apply. */
+int kls_stencil7_peer(const double* x, const double* x_lo, const double* x_hi, double* y,
+                      int64_t nx, int64_t ny, int64_t nz, void* mybuf, int32_t rank,
+                      uint64_t epoch, int* err, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -56,6 +56,9 @@ class Engine:
         self.res_np = self.res_host.numpy()
         self.res_dev = _mapped(self.res_host.data_ptr())
         self.ws, self.wsb = runtime.workspace_for(self.st, capacity + 1)
+        # N > 1: the per-step reduction goes over NVLink peer memory when
+        # available (csrc/comm.cu), else through NCCL
+        self.peer = runtime.peer_link(self.comm) if self.world > 1 else None
 
     # -- views ----------------------------------------------------------------
     def zero_col(self, c):
@@ -84,8 +87,20 @@ class Engine:
             _lib.call("kls_stream_sync", self.st)
             runtime.XFER["d2h"] += 8 * count
             return self.res_np[:count].copy()
-        out = self.stage.dev_out[:count]
         rec = trace._active
+        if self.peer is not None:
+            if count > self.res_np.size:
+                raise DimensionError("result buffer too small")
+            if rec is not None and rec.events:
+                with rec.span("allreduce"):
+                    self.peer.allreduce(self.stage.dev_out.data_ptr(), count, self.res_dev, self.st)
+            else:
+                self.peer.allreduce(self.stage.dev_out.data_ptr(), count, self.res_dev, self.st)
+            _lib.call("kls_stream_sync", self.st)
+            self.peer.check()
+            runtime.XFER["d2h"] += 8 * count
+            return self.res_np[:count].copy()
+        out = self.stage.dev_out[:count]
         if rec is not None and rec.events:
             with rec.span("allreduce"):
                 self.comm.allreduce_(out)

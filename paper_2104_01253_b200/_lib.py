@@ -45,11 +45,17 @@ SIGNATURES = {
     "kls_sub": (ctypes.c_int, [c_dp, c_dp, c_dp, i64, c_dp]),
     "kls_resid_norms": (ctypes.c_int, [c_dp, c_dp, c_dp, i64, c_dp, c_dp, sz, c_dp]),
     "kls_tsgemm_inplace": (ctypes.c_int, [c_dp, i64, i64, i32, c_dp, c_dp]),
+    "kls_peer_buffer_bytes": (sz, [i32]),
+    "kls_peer_allreduce": (ctypes.c_int, [c_dp, i32, c_dp, c_dp, i32, i32, i32, ctypes.c_uint64,
+                                          c_dp, c_dp]),
+    "kls_peer_signal": (ctypes.c_int, [c_dp, i32, i32, i32, ctypes.c_uint64, c_dp]),
+    "kls_stencil7_peer": (ctypes.c_int, [c_dp, c_dp, c_dp, c_dp, i64, i64, i64, c_dp, i32,
+                                         ctypes.c_uint64, c_dp, c_dp]),
 }
 
 # entry points that launch no kernel (not counted as GPU launches)
 _NO_LAUNCH = frozenset({"kls_version", "kls_last_error", "kls_device_sm_count", "kls_stream_sync",
-                        "kls_host_device_ptr", "kls_workspace_bytes"})
+                        "kls_host_device_ptr", "kls_workspace_bytes", "kls_peer_buffer_bytes"})
 
 _lock = threading.Lock()
 _lib = None

@@ -216,6 +216,8 @@ class _DelayedArnoldi(_BaseArnoldi):
             # resumed without pending work: prime from the image of the last
             # (normalized) basis column (arnoldi.py:350-361)
             j = self.nbasis
+            if getattr(self._w, "leased", True) is False:  # released by a finalize
+                self._w = self.op.new_vector()
             w = self._w
             self.op.napply += 1
             e.apply(e.col(j - 1), w.local)
@@ -251,9 +253,15 @@ class _DelayedArnoldi(_BaseArnoldi):
         self._wscale = vscale
         return True
 
+    def _release_w(self):
+        rel = getattr(self._w, "release", None)
+        if rel is not None:
+            rel()
+
     def _flush(self):
         """CGS2 pass on the pending vector (arnoldi.py:425-455): 2 reductions."""
         if not self._pending:
+            self._release_w()
             return
         e = self.eng
         m = self.m
@@ -272,6 +280,7 @@ class _DelayedArnoldi(_BaseArnoldi):
                 self.hcols = j
             self._pending = False
             self._mark_happy()
+            self._release_w()
             return
         if self.start_norm is None:
             self.start_norm = alpha
@@ -282,6 +291,7 @@ class _DelayedArnoldi(_BaseArnoldi):
         e.divide_into(e.col(j), w, alpha)
         self.nbasis += 1
         self._pending = False
+        self._release_w()
 
 
 class _ImmediateArnoldi(_BaseArnoldi):

@@ -1,0 +1,241 @@
+// Cross-GPU exchange over NVLink peer memory (symmetric buffers).
+//
+// kls_peer_allreduce is the DCGS2 step's one global reduction (the paper's
+// MPI_Allreduce; ledger site kernels.py:57-59) done as a
+// one-shot exchange instead of an NCCL call: every rank copies its 2j+3
+// partial sums into its own symmetric buffer, raises an epoch flag in every
+// peer's buffer, waits for all peers' flags, then sums the N peer vectors in
+// rank order 0..N-1.  Every rank computes the same sum in the same order,
+// so all ranks hold bitwise-identical results (the property the replicated
+// host step relies on) — and the sum lands directly in page-locked host
+// memory.  Double-buffered by epoch parity: a rank can only reuse a slot
+// after every peer has signalled the following epoch, i.e. after they have
+// finished reading it.
+//
+// kls_peer_signal / kls_stencil7_peer replace the halo exchange: a rank
+// signals "my vector for epoch e is written" to its neighbours, and the
+// stencil kernel reads the neighbouring x-planes straight from the peers'
+// memory once their flags reach e.
+//
+// Symmetric buffer layout (per rank, identical offsets):
+//   uint64 ar_flag[kMaxPeers] | uint64 halo_flag[kMaxPeers] | pad |
+//   double slot[2][cap]
+// Every spin has a wall-clock timeout (globaltimer) so a missing peer turns
+// into an error code instead of a hung GPU.
+#include "common.cuh"
+
+namespace {
+
+using namespace kls;
+
+constexpr int kMaxPeers = 8;
+constexpr size_t kDataOff = 256;
+constexpr uint64_t kTimeoutNs = 20ull * 1000 * 1000 * 1000;
+
+struct Peers {
+  char* buf[kMaxPeers];  // symmetric buffer base of every rank (peer-mapped)
+  int rank;
+  int world;
+  int cap;  // doubles per slot
+};
+
+__device__ __forceinline__ uint64_t* ar_flags(char* b) { return reinterpret_cast<uint64_t*>(b); }
+__device__ __forceinline__ uint64_t* halo_flags(char* b) {
+  return reinterpret_cast<uint64_t*>(b) + kMaxPeers;
+}
+__device__ __forceinline__ double* slot(char* b, int cap, uint64_t epoch) {
+  return reinterpret_cast<double*>(b + kDataOff) + (epoch & 1) * static_cast<size_t>(cap);
+}
+
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ uint64_t now_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// spin until *flag >= epoch; false on timeout
+__device__ __forceinline__ bool wait_flag(const uint64_t* flag, uint64_t epoch) {
+  if (ld_acquire_sys(flag) >= epoch) return true;
+  const uint64_t t0 = now_ns();
+  while (ld_acquire_sys(flag) < epoch) {
+    if (now_ns() - t0 > kTimeoutNs) return false;
+    __nanosleep(64);
+  }
+  return true;
+}
+
+__global__ void __launch_bounds__(kThreads) peer_allreduce_kernel(const double* __restrict__ src,
+                                                                  int nv, double* out, Peers p,
+                                                                  uint64_t epoch, int* err) {
+  __shared__ int s_ok;
+  char* mine = p.buf[p.rank];
+  double* dst = slot(mine, p.cap, epoch);
+  for (int i = threadIdx.x; i < nv; i += blockDim.x) dst[i] = src[i];
+  if (threadIdx.x == 0) s_ok = 1;
+  __syncthreads();
+  if (threadIdx.x < p.world) {
+    __threadfence_system();
+    st_release_sys(ar_flags(p.buf[threadIdx.x]) + p.rank, epoch);
+    if (!wait_flag(ar_flags(mine) + threadIdx.x, epoch)) atomicExch(&s_ok, 0);
+  }
+  __syncthreads();
+  if (!s_ok) {
+    if (threadIdx.x == 0) *err = 1;
+    for (int i = threadIdx.x; i < nv; i += blockDim.x) out[i] = __longlong_as_double(0x7ff8000000000000ll);
+    return;
+  }
+  for (int i = threadIdx.x; i < nv; i += blockDim.x) {
+    double s = 0.0;
+    for (int r = 0; r < p.world; ++r) {
+      const volatile double* v = slot(p.buf[r], p.cap, epoch);
+      s += v[i];
+    }
+    out[i] = s;
+  }
+}
+
+__global__ void peer_signal_kernel(Peers p, int target_mask, uint64_t epoch) {
+  const int t = threadIdx.x;
+  if (t < p.world && ((target_mask >> t) & 1)) {
+    __threadfence_system();
+    st_release_sys(halo_flags(p.buf[t]) + p.rank, epoch);
+  }
+}
+
+// Stencil with peer halos: CTAs whose chunk touches a rank boundary wait for
+// the neighbour's flag, then read its plane over NVLink.
+__global__ void __launch_bounds__(kThreads) stencil7_peer_kernel(
+    const double* __restrict__ x, const double* x_lo, const double* x_hi, double* __restrict__ y,
+    int64_t nx, int32_t ny, int32_t nz, int32_t xchunk, const uint64_t* flag_lo,
+    const uint64_t* flag_hi, uint64_t epoch, int* err) {
+  __shared__ int s_ok;
+  const int64_t plane = static_cast<int64_t>(ny) * nz;
+  const int64_t xa = static_cast<int64_t>(blockIdx.y) * xchunk;
+  const int64_t xb = xa + xchunk < nx ? xa + xchunk : nx;
+  const bool need_lo = xa == 0 && x_lo != nullptr;
+  const bool need_hi = xb == nx && x_hi != nullptr;
+  if (need_lo || need_hi) {
+    if (threadIdx.x == 0) {
+      bool ok = true;
+      if (need_lo) ok = ok && wait_flag(flag_lo, epoch);
+      if (need_hi) ok = ok && wait_flag(flag_hi, epoch);
+      s_ok = ok;
+      if (!ok) *err = 1;
+    }
+    __syncthreads();
+    if (!s_ok) return;
+  }
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= plane || xa >= xb) return;
+  const int32_t iy = static_cast<int32_t>(t / nz);
+  const int32_t iz = static_cast<int32_t>(t - static_cast<int64_t>(iy) * nz);
+  const bool ylo = iy > 0, yhi = iy + 1 < ny, zlo = iz > 0, zhi = iz + 1 < nz;
+  bool has_prev = xa > 0 || x_lo != nullptr;
+  double prev = xa > 0 ? __ldg(x + (xa - 1) * plane + t)
+                       : (x_lo != nullptr ? *(reinterpret_cast<const volatile double*>(x_lo + t)) : 0.0);
+  double cur = __ldg(x + xa * plane + t);
+#pragma unroll 4
+  for (int64_t ix = xa; ix < xb; ++ix) {
+    const int64_t i = ix * plane + t;
+    const bool has_next = ix + 1 < nx || x_hi != nullptr;
+    const double next =
+        ix + 1 < nx ? __ldg(x + i + plane)
+                    : (x_hi != nullptr ? *(reinterpret_cast<const volatile double*>(x_hi + t)) : 0.0);
+    double acc = __dmul_rn(6.0, cur);
+    if (has_prev) acc = __dsub_rn(acc, prev);
+    if (has_next) acc = __dsub_rn(acc, next);
+    if (ylo) acc = __dsub_rn(acc, __ldg(x + i - nz));
+    if (yhi) acc = __dsub_rn(acc, __ldg(x + i + nz));
+    if (zlo) acc = __dsub_rn(acc, __ldg(x + i - 1));
+    if (zhi) acc = __dsub_rn(acc, __ldg(x + i + 1));
+    y[i] = acc;
+    prev = cur;
+    cur = next;
+    has_prev = true;
+  }
+}
+
+int make_peers(Peers& p, void* const* bufs, int rank, int world, int cap) {
+  if (world < 1 || world > kMaxPeers || rank < 0 || rank >= world || bufs == nullptr || cap < 1)
+    return fail(KLS_EINVAL, "peer: bad rank/world (%d/%d) or capacity", rank, world);
+  for (int r = 0; r < kMaxPeers; ++r) p.buf[r] = r < world ? static_cast<char*>(bufs[r]) : nullptr;
+  for (int r = 0; r < world; ++r)
+    if (p.buf[r] == nullptr) return fail(KLS_EINVAL, "peer: null buffer for rank %d", r);
+  p.rank = rank;
+  p.world = world;
+  p.cap = cap;
+  return KLS_OK;
+}
+
+}  // namespace
+
+// Bytes of a symmetric peer buffer holding `cap` doubles per slot.
+KLS_API size_t kls_peer_buffer_bytes(int32_t cap) {
+  return kDataOff + 2 * static_cast<size_t>(cap) * sizeof(double);
+}
+
+// One-shot allreduce (sum) of nv doubles at `src` (device) over the ranks
+// whose symmetric buffers are bufs[0..world).  The rank-ordered sum is
+// written to `out` (device or mapped host memory).  `epoch` must increase
+// by one per call and be identical on all ranks; *err (device int) is set
+// to 1 when a peer does not arrive within the timeout.
+KLS_API int kls_peer_allreduce(const double* src, int32_t nv, double* out, void* const* bufs,
+                               int32_t rank, int32_t world, int32_t cap, uint64_t epoch, int* err,
+                               void* stream) {
+  Peers p;
+  int rc = make_peers(p, bufs, rank, world, cap);
+  if (rc) return rc;
+  if (nv < 0 || nv > cap || src == nullptr || out == nullptr || err == nullptr)
+    return fail(KLS_EINVAL, "peer_allreduce: nv=%d exceeds slot capacity %d", nv, cap);
+  peer_allreduce_kernel<<<1, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(src, nv, out, p,
+                                                                                epoch, err);
+  return check_launch("peer_allreduce_kernel");
+}
+
+// Raise this rank's halo flag (value epoch) in the buffers of the ranks in
+// target_mask, after all prior work on the stream.
+KLS_API int kls_peer_signal(void* const* bufs, int32_t rank, int32_t world, int32_t target_mask,
+                            uint64_t epoch, void* stream) {
+  Peers p;
+  int rc = make_peers(p, bufs, rank, world, 1);
+  if (rc) return rc;
+  peer_signal_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(p, target_mask, epoch);
+  return check_launch("peer_signal_kernel");
+}
+
+// kls_stencil7 with the neighbouring planes read from peer memory: x_lo /
+// x_hi are peer-mapped addresses (or NULL at the physical boundary); the
+// kernel first waits until this rank's halo flags from the lower / upper
+// neighbour (in its own symmetric buffer `mybuf`) reach `epoch`.
+KLS_API int kls_stencil7_peer(const double* x, const double* x_lo, const double* x_hi, double* y,
+                              int64_t nx, int64_t ny, int64_t nz, void* mybuf, int32_t rank,
+                              uint64_t epoch, int* err, void* stream) {
+  if (x == nullptr || y == nullptr || nx < 0 || ny < 0 || nz < 0 || mybuf == nullptr ||
+      rank < 0 || rank >= kMaxPeers || err == nullptr)
+    return fail(KLS_EINVAL, "stencil7_peer: bad arguments");
+  const int64_t plane = ny * nz;
+  if (nx * plane == 0) return KLS_OK;
+  const uint64_t* flags = reinterpret_cast<const uint64_t*>(static_cast<char*>(mybuf)) + kMaxPeers;
+  const uint64_t* flag_lo = rank > 0 ? flags + (rank - 1) : flags;
+  const uint64_t* flag_hi = flags + (rank + 1 < kMaxPeers ? rank + 1 : rank);
+  const int64_t pblocks = ceil_div(plane, kThreads);
+  const int64_t xchunk = std::min<int64_t>(16, nx);
+  const int64_t chunks = ceil_div(nx, xchunk);
+  if (pblocks > INT32_MAX || chunks > 65535 || ny > INT32_MAX || nz > INT32_MAX)
+    return fail(KLS_EINVAL, "stencil7_peer: grid too large");
+  dim3 grid(static_cast<unsigned>(pblocks), static_cast<unsigned>(chunks));
+  stencil7_peer_kernel<<<grid, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+      x, x_lo, x_hi, y, nx, static_cast<int32_t>(ny), static_cast<int32_t>(nz),
+      static_cast<int32_t>(xchunk), flag_lo, flag_hi, epoch, err);
+  return check_launch("stencil7_peer_kernel");
+}

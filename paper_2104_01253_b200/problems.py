@@ -134,7 +134,7 @@ class LinearOperator:
         rows)."""
         if st is None:
             st = runtime.stream_handle()
-        if not isinstance(x, HaloVector):
+        if not isinstance(x, (HaloVector, PeerVector)):
             if self._needs_halo():
                 if self._scratch is None:
                     self._scratch = self.new_vector()
@@ -198,6 +198,28 @@ class LinearOperator:
                 e[j] = 0.0
             self._fro = float(np.sqrt(acc * self.n / t))
         return self._fro
+
+
+class PeerVector:
+    """A vector in NVLink symmetric memory: peers read its rows directly."""
+
+    def __init__(self, link, n_local):
+        self.link = link
+        self.n_local = n_local
+        self.buf, self.peer_ptrs, self._hdl = link.symmetric_vector(runtime.pad_rows(n_local))
+        self.local = self.buf[:n_local]
+        self.lo = self.hi = None
+        self.ext_offset = 0
+        self.leased = False
+
+    def release(self):
+        """Return the vector to its operator's pool (explicit, same program
+        point on every rank)."""
+        self.leased = False
+
+    @property
+    def ext_ptr(self):
+        return self.local.data_ptr()
 
 
 class _PlainVector:
@@ -550,17 +572,51 @@ class StencilLaplace3D(LinearOperator):
     def _needs_halo(self):
         return self.comm.world > 1
 
-    def new_vector(self):
+    def _plain_vector(self):
         lo = self.plane if self.x_lo > 0 else 0
         hi = self.plane if self.x_hi < self.dims[0] else 0
         if self.comm.world == 1:
             lo = hi = 0
         return HaloVector(self.m_local, lo, hi, contiguous=False)
 
+    def new_vector(self):
+        """Halo-capable vector.  With an NVLink peer link the vector lives in
+        symmetric memory and neighbours read its boundary planes directly
+        (kls_stencil7_peer); otherwise halos arrive by NCCL send/recv."""
+        link = runtime.peer_link(self.comm) if self.comm.world > 1 else None
+        if link is None:
+            return self._plain_vector()
+        # symmetric allocations need a collective rendezvous (slow): reuse
+        # released vectors.  Leases are taken and returned at the same
+        # program points on every rank (SPMD), so the pools stay aligned.
+        pool = self.__dict__.setdefault("_peer_pool", [])
+        for v in pool:
+            if not v.leased:
+                v.leased = True
+                return v
+        v = PeerVector(link, self.m_local)
+        v.leased = True
+        pool.append(v)
+        return v
+
+    def apply_into(self, x, y, st=None):
+        if not isinstance(x, (HaloVector, PeerVector)) and self._needs_halo():
+            # scratch copies take the NCCL path: back-to-back applies on one
+            # scratch buffer would race a peer still reading the last one
+            if self._scratch is None:
+                self._scratch = self._plain_vector()
+            self._scratch.local.copy_(x)
+            x = self._scratch
+        super().apply_into(x, y, st)
+
     def _exchange(self, x):
-        if self.comm.world == 1:
+        if self.comm.world == 1 or isinstance(x, PeerVector):
             return
-        with trace.span("halo"):
+        rec = trace._active
+        if rec is not None and rec.events:
+            with rec.span("halo"):
+                self._exchange_planes(x)
+        else:
             self._exchange_planes(x)
 
     def _exchange_planes(self, x):
@@ -581,10 +637,37 @@ class StencilLaplace3D(LinearOperator):
 
     def _launch(self, x, y, st):
         _, ny, nz = self.dims
+        if isinstance(x, PeerVector):
+            return self._launch_peer(x, y, st)
         lo = x.lo.data_ptr() if x.lo is not None else None
         hi = x.hi.data_ptr() if x.hi is not None else None
         _lib.call("kls_stencil7", x.local.data_ptr(), lo, hi, y.data_ptr(),
                   self.x_hi - self.x_lo, ny, nz, st)
+
+    def _launch_peer(self, x, y, st):
+        """Signal 'my vector is written' to the x-neighbours, then run the
+        stencil reading their boundary planes over NVLink."""
+        link = x.link
+        r, world = self.comm.rank, self.comm.world
+        nx, ny, nz = self.dims
+        lo_ptr = hi_ptr = None
+        mask = 0
+        if self.x_lo > 0:
+            plo, phi = runtime.block_range(nx, world, r - 1)
+            lo_ptr = x.peer_ptrs[r - 1] + 8 * (phi - plo - 1) * self.plane
+            mask |= 1 << (r - 1)
+        if self.x_hi < nx:
+            hi_ptr = x.peer_ptrs[r + 1]
+            mask |= 1 << (r + 1)
+        link.halo_epoch += 1
+        rec = trace._active
+        if rec is not None and rec.events:
+            with rec.span("halo"):
+                _lib.call("kls_peer_signal", link.ptrs, r, world, mask, link.halo_epoch, st)
+        else:
+            _lib.call("kls_peer_signal", link.ptrs, r, world, mask, link.halo_epoch, st)
+        _lib.call("kls_stencil7_peer", x.local.data_ptr(), lo_ptr, hi_ptr, y.data_ptr(),
+                  self.x_hi - self.x_lo, ny, nz, link.mybuf, r, link.halo_epoch, link.err_dev, st)
 
     def to_csr(self):
         """Host CSR with the same entries (for CSR-path runs and tests)."""

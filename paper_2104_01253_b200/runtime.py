@@ -226,3 +226,87 @@ def as_device_vector(x, n_local, lo=0, name="vector"):
     if a.size != n_local:
         a = a[lo : lo + n_local]
     return torch.from_numpy(np.ascontiguousarray(a)).to(device())
+
+
+# ---------------------------------------------------------------------------
+# NVLink peer link (symmetric memory)
+
+
+class PeerLink:
+    """Symmetric buffers of one process group, mapped into every peer GPU.
+
+    Carries the one-shot allreduce of the per-step Gram scalars and the halo
+    flags of peer-read stencils (csrc/comm.cu).  Allocation and rendezvous
+    are collective: every rank must create the link / vectors in the same
+    order (they do: the solvers are SPMD).
+    """
+
+    CAP = 8192  # doubles per allreduce slot (2j+3 <= CAP)
+
+    def __init__(self, comm):
+        import ctypes
+
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm_mem
+
+        self.comm = comm
+        self.rank, self.world = comm.rank, comm.world
+        if self.world > 8:
+            raise RuntimeError("peer link supports up to 8 ranks (one NVLink domain)")
+        group = comm.group if comm.group is not None else dist.group.WORLD
+        self._group_name = group.group_name
+        nbytes = int(_lib.load().kls_peer_buffer_bytes(self.CAP))
+        self.buf = symm_mem.empty(nbytes, dtype=torch.uint8, device=device())
+        self.buf.zero_()
+        self.hdl = symm_mem.rendezvous(self.buf, self._group_name)
+        self.ptrs = (ctypes.c_void_p * self.world)(*[int(p) for p in self.hdl.buffer_ptrs])
+        self.mybuf = int(self.hdl.buffer_ptrs[self.rank])
+        self.err_host = torch.zeros(1, dtype=torch.int32, pin_memory=True)
+        from ._engine import _mapped
+
+        self.err_dev = _mapped(self.err_host.data_ptr())
+        self.ar_epoch = 0
+        self.halo_epoch = 0
+        torch.cuda.synchronize()
+        dist.barrier(group=group)
+
+    def symmetric_vector(self, n):
+        """A zeroed device vector in symmetric memory plus every rank's
+        pointer to its copy."""
+        import torch.distributed._symmetric_memory as symm_mem
+
+        t = symm_mem.empty(max(n, 2), dtype=torch.float64, device=device())
+        t.zero_()
+        hdl = symm_mem.rendezvous(t, self._group_name)
+        return t, [int(p) for p in hdl.buffer_ptrs], hdl
+
+    def allreduce(self, src_ptr, count, out_ptr, stream):
+        if count > self.CAP:
+            raise RuntimeError(f"peer allreduce of {count} values exceeds the slot ({self.CAP})")
+        self.ar_epoch += 1
+        _lib.call("kls_peer_allreduce", src_ptr, count, out_ptr, self.ptrs, self.rank, self.world,
+                  self.CAP, self.ar_epoch, self.err_dev, stream)
+        self.comm.allreduce_calls += 1
+
+    def check(self):
+        if int(self.err_host[0]) != 0:
+            raise RuntimeError("NVLink peer exchange timed out (a rank did not arrive)")
+
+
+def peer_link(comm):
+    """The comm's PeerLink, or None (single rank, disabled by KLS_PEER=0, or
+    symmetric memory unavailable, in which case NCCL carries the traffic)."""
+    import os
+
+    if comm.world == 1 or os.environ.get("KLS_PEER", "1") == "0":
+        return None
+    if getattr(comm, "_peer", None) is None and not getattr(comm, "_peer_failed", False):
+        try:
+            comm._peer = PeerLink(comm)
+        except Exception as exc:  # transport selection only; compute is unchanged
+            import warnings
+
+            warnings.warn(f"NVLink peer link unavailable ({exc}); using NCCL collectives")
+            comm._peer_failed = True
+            comm._peer = None
+    return getattr(comm, "_peer", None)
