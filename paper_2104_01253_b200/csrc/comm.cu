@@ -22,7 +22,7 @@
 //   double slot[2][cap]
 // Every spin has a wall-clock timeout (globaltimer) so a missing peer turns
 // into an error code instead of a hung GPU.
-#include "common.cuh"
+#include "stencil.cuh"
 
 namespace {
 
@@ -114,18 +114,17 @@ __global__ void peer_signal_kernel(Peers p, int target_mask, uint64_t epoch) {
 
 // Stencil with peer halos: CTAs whose chunk touches a rank boundary wait for
 // the neighbour's flag, then read its plane over NVLink.
-__global__ void __launch_bounds__(kThreads) stencil7_peer_kernel(
+__global__ void __launch_bounds__(kTileZ * kTileY) stencil7_peer_kernel(
     const double* __restrict__ x, const double* x_lo, const double* x_hi, double* __restrict__ y,
     int64_t nx, int32_t ny, int32_t nz, int32_t xchunk, const uint64_t* flag_lo,
     const uint64_t* flag_hi, uint64_t epoch, int* err) {
   __shared__ int s_ok;
-  const int64_t plane = static_cast<int64_t>(ny) * nz;
-  const int64_t xa = static_cast<int64_t>(blockIdx.y) * xchunk;
+  const int64_t xa = static_cast<int64_t>(blockIdx.z) * xchunk;
   const int64_t xb = xa + xchunk < nx ? xa + xchunk : nx;
   const bool need_lo = xa == 0 && x_lo != nullptr;
   const bool need_hi = xb == nx && x_hi != nullptr;
   if (need_lo || need_hi) {
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && threadIdx.y == 0) {
       bool ok = true;
       if (need_lo) ok = ok && wait_flag(flag_lo, epoch);
       if (need_hi) ok = ok && wait_flag(flag_hi, epoch);
@@ -135,34 +134,7 @@ __global__ void __launch_bounds__(kThreads) stencil7_peer_kernel(
     __syncthreads();
     if (!s_ok) return;
   }
-  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (t >= plane || xa >= xb) return;
-  const int32_t iy = static_cast<int32_t>(t / nz);
-  const int32_t iz = static_cast<int32_t>(t - static_cast<int64_t>(iy) * nz);
-  const bool ylo = iy > 0, yhi = iy + 1 < ny, zlo = iz > 0, zhi = iz + 1 < nz;
-  bool has_prev = xa > 0 || x_lo != nullptr;
-  double prev = xa > 0 ? __ldg(x + (xa - 1) * plane + t)
-                       : (x_lo != nullptr ? *(reinterpret_cast<const volatile double*>(x_lo + t)) : 0.0);
-  double cur = __ldg(x + xa * plane + t);
-#pragma unroll 4
-  for (int64_t ix = xa; ix < xb; ++ix) {
-    const int64_t i = ix * plane + t;
-    const bool has_next = ix + 1 < nx || x_hi != nullptr;
-    const double next =
-        ix + 1 < nx ? __ldg(x + i + plane)
-                    : (x_hi != nullptr ? *(reinterpret_cast<const volatile double*>(x_hi + t)) : 0.0);
-    double acc = __dmul_rn(6.0, cur);
-    if (has_prev) acc = __dsub_rn(acc, prev);
-    if (has_next) acc = __dsub_rn(acc, next);
-    if (ylo) acc = __dsub_rn(acc, __ldg(x + i - nz));
-    if (yhi) acc = __dsub_rn(acc, __ldg(x + i + nz));
-    if (zlo) acc = __dsub_rn(acc, __ldg(x + i - 1));
-    if (zhi) acc = __dsub_rn(acc, __ldg(x + i + 1));
-    y[i] = acc;
-    prev = cur;
-    cur = next;
-    has_prev = true;
-  }
+  stencil7_march(x, x_lo, x_hi, y, nx, ny, nz, xa, xb);
 }
 
 int make_peers(Peers& p, void* const* bufs, int rank, int world, int cap) {
@@ -228,13 +200,11 @@ KLS_API int kls_stencil7_peer(const double* x, const double* x_lo, const double*
   const uint64_t* flags = reinterpret_cast<const uint64_t*>(static_cast<char*>(mybuf)) + kMaxPeers;
   const uint64_t* flag_lo = rank > 0 ? flags + (rank - 1) : flags;
   const uint64_t* flag_hi = flags + (rank + 1 < kMaxPeers ? rank + 1 : rank);
-  const int64_t pblocks = ceil_div(plane, kThreads);
   const int64_t xchunk = std::min<int64_t>(16, nx);
-  const int64_t chunks = ceil_div(nx, xchunk);
-  if (pblocks > INT32_MAX || chunks > 65535 || ny > INT32_MAX || nz > INT32_MAX)
+  dim3 grid;
+  if (ny > INT32_MAX || nz > INT32_MAX || !stencil7_grid(nx, ny, nz, xchunk, grid))
     return fail(KLS_EINVAL, "stencil7_peer: grid too large");
-  dim3 grid(static_cast<unsigned>(pblocks), static_cast<unsigned>(chunks));
-  stencil7_peer_kernel<<<grid, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+  stencil7_peer_kernel<<<grid, dim3(kTileZ, kTileY), 0, static_cast<cudaStream_t>(stream)>>>(
       x, x_lo, x_hi, y, nx, static_cast<int32_t>(ny), static_cast<int32_t>(nz),
       static_cast<int32_t>(xchunk), flag_lo, flag_hi, epoch, err);
   return check_launch("stencil7_peer_kernel");

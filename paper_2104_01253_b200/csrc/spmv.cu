@@ -12,7 +12,7 @@
 // x-slowest (nx, ny, nz) grid, y = 6 g minus the six Dirichlet neighbours in
 // the reference's order (x-1, x+1, y-1, y+1, z-1, z+1).  For a row-sharded
 // grid the neighbouring x-planes of other ranks come in through x_lo / x_hi.
-#include "common.cuh"
+#include "stencil.cuh"
 
 #include <cstdlib>
 
@@ -70,45 +70,12 @@ __global__ void __launch_bounds__(kThreads) csr_spmv_kernel(const int64_t* __res
   }
 }
 
-// One thread per (iy, iz) line marching through a chunk of x-planes: the
-// x-neighbours come from a register window (each element is read from HBM
-// once), the y/z neighbours from L1/L2 (adjacent threads load them as their
-// own centre).  No integer division in the loop.
-__global__ void __launch_bounds__(kThreads) stencil7_kernel(const double* __restrict__ x,
-                                                            const double* __restrict__ x_lo,
-                                                            const double* __restrict__ x_hi,
-                                                            double* __restrict__ y, int64_t nx,
-                                                            int32_t ny, int32_t nz,
-                                                            int32_t xchunk) {
-  const int64_t plane = static_cast<int64_t>(ny) * nz;
-  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (t >= plane) return;
-  const int32_t iy = static_cast<int32_t>(t / nz);
-  const int32_t iz = static_cast<int32_t>(t - static_cast<int64_t>(iy) * nz);
-  const int64_t xa = static_cast<int64_t>(blockIdx.y) * xchunk;
+__global__ void __launch_bounds__(kTileZ * kTileY) stencil7_kernel(
+    const double* __restrict__ x, const double* __restrict__ x_lo, const double* __restrict__ x_hi,
+    double* __restrict__ y, int64_t nx, int32_t ny, int32_t nz, int32_t xchunk) {
+  const int64_t xa = static_cast<int64_t>(blockIdx.z) * xchunk;
   const int64_t xb = xa + xchunk < nx ? xa + xchunk : nx;
-  if (xa >= xb) return;
-  const bool ylo = iy > 0, yhi = iy + 1 < ny, zlo = iz > 0, zhi = iz + 1 < nz;
-  bool has_prev = xa > 0 || x_lo != nullptr;
-  double prev = xa > 0 ? __ldg(x + (xa - 1) * plane + t) : (x_lo != nullptr ? __ldg(x_lo + t) : 0.0);
-  double cur = __ldg(x + xa * plane + t);
-#pragma unroll 4
-  for (int64_t ix = xa; ix < xb; ++ix) {
-    const int64_t i = ix * plane + t;
-    const bool has_next = ix + 1 < nx || x_hi != nullptr;
-    const double next = ix + 1 < nx ? __ldg(x + i + plane) : (x_hi != nullptr ? __ldg(x_hi + t) : 0.0);
-    double acc = __dmul_rn(6.0, cur);
-    if (has_prev) acc = __dsub_rn(acc, prev);
-    if (has_next) acc = __dsub_rn(acc, next);
-    if (ylo) acc = __dsub_rn(acc, __ldg(x + i - nz));
-    if (yhi) acc = __dsub_rn(acc, __ldg(x + i + nz));
-    if (zlo) acc = __dsub_rn(acc, __ldg(x + i - 1));
-    if (zhi) acc = __dsub_rn(acc, __ldg(x + i + 1));
-    y[i] = acc;
-    prev = cur;
-    cur = next;
-    has_prev = true;
-  }
+  stencil7_march(x, x_lo, x_hi, y, nx, ny, nz, xa, xb);
 }
 
 // dense y = A x, A row-major n x n (DenseOperator, problems.py:68-85):
@@ -159,21 +126,15 @@ KLS_API int kls_stencil7(const double* x, const double* x_lo, const double* x_hi
   const int64_t n = nx * ny * nz;
   if (n == 0) return KLS_OK;
   if (ny > INT32_MAX || nz > INT32_MAX) return fail(KLS_EINVAL, "stencil7: ny, nz must fit int32");
-  const int64_t plane = ny * nz;
-  const int64_t pblocks = ceil_div(plane, kThreads);
-  // x-chunk length: short enough for several waves of CTAs (latency hiding),
-  // long enough that the two extra window loads per chunk stay cheap
   static int env_chunk = -1;
   if (env_chunk < 0) {
     const char* e = getenv("KLS_STENCIL_XCHUNK");
     env_chunk = e ? atoi(e) : 0;
   }
-  int64_t xchunk = env_chunk > 0 ? env_chunk : 16;
-  xchunk = std::min<int64_t>(xchunk, nx);
-  int64_t chunks = ceil_div(nx, xchunk);
-  if (pblocks > INT32_MAX || chunks > 65535) return fail(KLS_EINVAL, "stencil7: grid too large");
-  dim3 grid(static_cast<unsigned>(pblocks), static_cast<unsigned>(chunks));
-  stencil7_kernel<<<grid, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+  const int64_t xchunk = std::min<int64_t>(env_chunk > 0 ? env_chunk : 16, nx);
+  dim3 grid;
+  if (!stencil7_grid(nx, ny, nz, xchunk, grid)) return fail(KLS_EINVAL, "stencil7: grid too large");
+  stencil7_kernel<<<grid, dim3(kTileZ, kTileY), 0, static_cast<cudaStream_t>(stream)>>>(
       x, x_lo, x_hi, y, nx, static_cast<int32_t>(ny), static_cast<int32_t>(nz),
       static_cast<int32_t>(xchunk));
   return check_launch("stencil7_kernel");
