@@ -1,0 +1,206 @@
+// K1, TMA-staged variant: the Q column tiles of a row chunk are brought into
+// shared memory with bulk asynchronous copies (cp.async.bulk, completed on
+// mbarriers) by one producer warp, while 8 consumer warps form the partial
+// dots from shared memory with the LDG kernel's halving-butterfly warp
+// reduction and epilogue.  Deterministic like it, with its own fixed
+// summation order (1024-row chunks, one CTA per SM).
+//
+// Pipeline per CTA (persistent, one CTA per SM): a 4-stage ring of
+// 4 columns x 1024 rows (32 KB per stage) for Q, and a double-buffered
+// slot for the chunk's right-hand vectors.  Only full 1024-row chunks go
+// through the copy engine; the ragged tail chunk is read directly.
+#include "gram.cuh"
+#include "tma.cuh"
+
+namespace kls {
+namespace gram {
+namespace {
+
+using namespace kls::tma;
+
+constexpr int kR = 1024;          // rows per chunk
+constexpr int kRPt = 2;           // row pairs per lane (8 warps x 64 x 2 = 1024)
+constexpr int kStages = 4;
+constexpr int kProducerWarp = kWarps;
+constexpr int kTmaThreads = (kWarps + 1) * 32;
+constexpr int kPanelTma = 256;    // basis columns per launch (per-warp accumulators in smem)
+
+template <int NX>
+__global__ void __launch_bounds__(kTmaThreads, 1) gram_tma_kernel(GramParams p) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  constexpr int V = kG * NX;
+  const int nxb = NX + ((p.bext != nullptr && p.bext != p.x0) ? 1 : 0);  // staged rhs columns
+  // layout: [mbarriers 256 B][Q ring][x double buffer][per-warp accumulators]
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty = full + kStages;
+  uint64_t* xfull = empty + kStages;
+  uint64_t* xempty = xfull + 2;
+  double* qring = reinterpret_cast<double*>(smem + 256);
+  double* xbuf = qring + static_cast<size_t>(kStages) * kG * kR;
+  double* sacc = xbuf + static_cast<size_t>(2) * 3 * kR;
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int ng = (p.k + kG - 1) / kG;
+  const int stride = ng * V;
+  const int64_t nfull = p.m / kR;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, kWarps);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(xfull + s, 1);
+      mbar_init(xempty + s, kWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp < kWarps) {
+    double* wacc = sacc + warp * stride;
+    for (int i = lane; i < stride; i += 32) wacc[i] = 0.0;
+  }
+  __syncthreads();
+
+  double ex[NX];
+#pragma unroll
+  for (int t = 0; t < NX; ++t) ex[t] = 0.0;
+  double xn = 0.0;
+
+  if (warp == kProducerWarp) {
+    if (lane == 0) {
+      const double* xsrc[3] = {p.x0, p.x1, p.bext};
+      uint32_t use = 0;  // Q stage fills so far
+      uint32_t xuse = 0;
+      for (int64_t c = blockIdx.x; c < nfull; c += gridDim.x, ++xuse) {
+        const int xs = xuse & 1;
+        if (xuse >= 2) mbar_wait(xempty + xs, ((xuse >> 1) - 1) & 1);
+        mbar_expect_tx(xfull + xs, static_cast<uint32_t>(nxb) * kR * sizeof(double));
+        for (int t = 0; t < nxb; ++t)
+          bulk_g2s(xbuf + (static_cast<size_t>(xs) * 3 + t) * kR, xsrc[t] + c * kR,
+                   kR * sizeof(double), xfull + xs);
+        for (int g = 0; g < ng; ++g, ++use) {
+          const int s = use % kStages;
+          const uint32_t round = use / kStages;
+          if (round >= 1) mbar_wait(empty + s, (round - 1) & 1);
+          const int ncols = min(kG, p.k - g * kG);
+          mbar_expect_tx(full + s, static_cast<uint32_t>(ncols) * kR * sizeof(double));
+          for (int cc = 0; cc < ncols; ++cc)
+            bulk_g2s(qring + (static_cast<size_t>(s) * kG + cc) * kR,
+                     p.Q + static_cast<int64_t>(g * kG + cc) * p.ldq + c * kR, kR * sizeof(double),
+                     full + s);
+        }
+      }
+    }
+  } else {
+    double* wacc = sacc + warp * stride;
+    const int64_t wrow = warp * (64 * kRPt);
+    uint32_t use = 0;
+    uint32_t xuse = 0;
+    for (int64_t c = blockIdx.x; c < nfull; c += gridDim.x, ++xuse) {
+      const int xs = xuse & 1;
+      mbar_wait(xfull + xs, (xuse >> 1) & 1);
+      double2 xv[NX][kRPt];
+      const double* xb = xbuf + static_cast<size_t>(xs) * 3 * kR;
+#pragma unroll
+      for (int t = 0; t < NX; ++t)
+#pragma unroll
+        for (int r = 0; r < kRPt; ++r)
+          xv[t][r] = *reinterpret_cast<const double2*>(xb + t * kR + wrow + 64 * r + 2 * lane);
+      if (p.bext != nullptr) {
+#pragma unroll
+        for (int r = 0; r < kRPt; ++r) {
+          const double2 b = p.bext == p.x0
+                                ? xv[0][r]
+                                : *reinterpret_cast<const double2*>(xb + NX * kR + wrow + 64 * r + 2 * lane);
+#pragma unroll
+          for (int t = 0; t < NX; ++t) {
+            ex[t] = fma(b.x, xv[t][r].x, ex[t]);
+            ex[t] = fma(b.y, xv[t][r].y, ex[t]);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(xempty + xs);
+      if (p.xnorm) {
+#pragma unroll
+        for (int r = 0; r < kRPt; ++r) {
+          xn = fma(xv[NX - 1][r].x, xv[NX - 1][r].x, xn);
+          xn = fma(xv[NX - 1][r].y, xv[NX - 1][r].y, xn);
+        }
+      }
+      for (int g = 0; g < ng; ++g, ++use) {
+        const int s = use % kStages;
+        mbar_wait(full + s, (use / kStages) & 1);
+        const double* qs = qring + static_cast<size_t>(s) * kG * kR;
+        double2 q[kG][kRPt];
+#pragma unroll
+        for (int cc = 0; cc < kG; ++cc) {
+          if (g * kG + cc < p.k) {
+#pragma unroll
+            for (int r = 0; r < kRPt; ++r)
+              q[cc][r] = *reinterpret_cast<const double2*>(qs + cc * kR + wrow + 64 * r + 2 * lane);
+          } else {
+#pragma unroll
+            for (int r = 0; r < kRPt; ++r) q[cc][r] = make_double2(0.0, 0.0);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + s);
+        double acc[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v) acc[v] = 0.0;
+#pragma unroll
+        for (int cc = 0; cc < kG; ++cc)
+#pragma unroll
+          for (int r = 0; r < kRPt; ++r)
+#pragma unroll
+            for (int t = 0; t < NX; ++t) {
+              acc[cc * NX + t] = fma(q[cc][r].x, xv[t][r].x, acc[cc * NX + t]);
+              acc[cc * NX + t] = fma(q[cc][r].y, xv[t][r].y, acc[cc * NX + t]);
+            }
+        const double sred = warp_transpose_reduce<V>(acc, lane);
+        if ((lane & (32 / V - 1)) == 0) wacc[g * V + warp_slot<V>(lane)] += sred;
+      }
+    }
+    // ragged tail: the CTA that would own chunk nfull reads it directly
+    if (nfull * kR < p.m && (nfull % gridDim.x) == blockIdx.x)
+      gram_chunk<NX, kRPt, true>(p, nfull * kR + wrow, lane, wacc, ex, xn);
+  }
+  gram_epilogue<NX>(p, sacc, stride, ex, xn);
+}
+
+}  // namespace
+
+bool tma_eligible(const GramParams& p) {
+  return p.k > 0 && p.k <= kPanelTma && p.m >= kR &&
+         ((reinterpret_cast<uintptr_t>(p.Q) | reinterpret_cast<uintptr_t>(p.x0) |
+           reinterpret_cast<uintptr_t>(p.x1) | reinterpret_cast<uintptr_t>(p.bext)) &
+          15) == 0 &&
+         (p.ldq % 2) == 0;
+}
+
+template <int NX>
+int launch_gram_tma(GramParams p, size_t ws_bytes, cudaStream_t st) {
+  const int64_t nchunks = (p.m + kR - 1) / kR;
+  int grid = static_cast<int>(std::min<int64_t>(nchunks, sm_count()));
+  if (grid < 1) grid = 1;
+  const int has_b = p.bext != nullptr ? 1 : 0;
+  const int64_t nv = (int64_t)p.k * NX + has_b * NX + (p.xnorm ? 1 : 0);
+  if (!red_ws_fits(ws_bytes, grid, static_cast<int>(nv)))
+    return fail(KLS_ENOSPC, "gram_tma: workspace too small");
+  const int ng = (p.k + kG - 1) / kG;
+  const size_t smem = 256 + sizeof(double) * (static_cast<size_t>(kStages) * kG * kR + 2 * 3 * kR +
+                                              static_cast<size_t>(kWarps) * ng * kG * NX);
+  cudaError_t e = cudaFuncSetAttribute(gram_tma_kernel<NX>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return fail(KLS_ECUDA, "gram_tma: smem attr: %s", cudaGetErrorString(e));
+  gram_tma_kernel<NX><<<grid, kTmaThreads, smem, st>>>(p);
+  return check_launch("gram_tma_kernel");
+}
+
+template int launch_gram_tma<1>(GramParams, size_t, cudaStream_t);
+template int launch_gram_tma<2>(GramParams, size_t, cudaStream_t);
+
+}  // namespace gram
+}  // namespace kls

@@ -12,7 +12,9 @@
 // two right-hand columns, optionally returning ||Y(:, l-1)||^2 of the result
 // (fused norm for the CGS2 comparator and the DCGS2 flush).
 #include "reduce.cuh"
+#include "tma.cuh"
 
+#include <cstdlib>
 #include <cstring>
 
 namespace {
@@ -119,6 +121,147 @@ __global__ void __launch_bounds__(kThreads, kUpdBlocksPerSm)
     else
       upd_chunk<RP, true>(p, sct, tj, wbase, lane);
   }
+}
+
+// TMA-staged K2: a producer warp streams 4-column x 1024-row tiles of Q and
+// the chunk's w / aw rows into shared memory with cp.async.bulk (mbarrier
+// completion, 4-stage ring + double-buffered vector slot); 8 consumer warps
+// accumulate Q c and Q t from shared memory and write q_j and w' with
+// 128-bit stores.  Same per-row arithmetic and order as the LDG kernel, so
+// both variants give bitwise-identical results.
+constexpr int kUR = 1024;            // rows per chunk
+constexpr int kUStages = 4;
+constexpr int kUThreads = (kWarps + 1) * 32;
+
+template <int NC>
+__global__ void __launch_bounds__(kUThreads, 1)
+    dcgs2_update_tma_kernel(UpdParams p, const __grid_constant__ CoefPack<NC> pk) {
+  using namespace kls::tma;
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty = full + kUStages;
+  uint64_t* xfull = empty + kUStages;
+  uint64_t* xempty = xfull + 2;
+  const int jpad = (p.j + kCols - 1) / kCols * kCols;
+  double2* sct = reinterpret_cast<double2*>(smem + 256);
+  double* qring = reinterpret_cast<double*>(sct + jpad + 1);
+  double* xbuf = qring + static_cast<size_t>(kUStages) * kCols * kUR;
+
+  const double* coef = NC > 0 ? pk.v : p.coef;
+  for (int k = threadIdx.x; k < jpad; k += blockDim.x)
+    sct[k] = k < p.j ? make_double2(coef[k], coef[p.j + k]) : make_double2(0.0, 0.0);
+  const double tj = coef[2 * p.j];
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int ng = (p.j + kCols - 1) / kCols;
+  const int64_t nfull = p.m / kUR;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kUStages; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, kWarps);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(xfull + s, 1);
+      mbar_init(xempty + s, kWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == kWarps) {
+    if (lane == 0) {
+      uint32_t use = 0, xuse = 0;
+      for (int64_t c = blockIdx.x; c < nfull; c += gridDim.x, ++xuse) {
+        const int xs = xuse & 1;
+        if (xuse >= 2) mbar_wait(xempty + xs, ((xuse >> 1) - 1) & 1);
+        mbar_expect_tx(xfull + xs, 2u * kUR * sizeof(double));
+        bulk_g2s(xbuf + (static_cast<size_t>(xs) * 2) * kUR, p.w + c * kUR, kUR * sizeof(double),
+                 xfull + xs);
+        bulk_g2s(xbuf + (static_cast<size_t>(xs) * 2 + 1) * kUR, p.aw + c * kUR,
+                 kUR * sizeof(double), xfull + xs);
+        for (int g = 0; g < ng; ++g, ++use) {
+          const int s = use % kUStages;
+          const uint32_t round = use / kUStages;
+          if (round >= 1) mbar_wait(empty + s, (round - 1) & 1);
+          const int ncols = min(kCols, p.j - g * kCols);
+          mbar_expect_tx(full + s, static_cast<uint32_t>(ncols) * kUR * sizeof(double));
+          for (int cc = 0; cc < ncols; ++cc)
+            bulk_g2s(qring + (static_cast<size_t>(s) * kCols + cc) * kUR,
+                     p.Q + static_cast<int64_t>(g * kCols + cc) * p.ldq + c * kUR,
+                     kUR * sizeof(double), full + s);
+        }
+      }
+    }
+    return;
+  }
+  constexpr int RP = 2;
+  const int64_t wrow = warp * (64 * RP);
+  double* qout = p.Q + static_cast<int64_t>(p.j) * p.ldq;
+  uint32_t use = 0, xuse = 0;
+  for (int64_t c = blockIdx.x; c < nfull; c += gridDim.x, ++xuse) {
+    double2 ac[RP], at[RP];
+#pragma unroll
+    for (int r = 0; r < RP; ++r) {
+      ac[r] = make_double2(0.0, 0.0);
+      at[r] = make_double2(0.0, 0.0);
+    }
+    for (int g = 0; g < ng; ++g, ++use) {
+      const int s = use % kUStages;
+      mbar_wait(full + s, (use / kUStages) & 1);
+      const double* qs = qring + static_cast<size_t>(s) * kCols * kUR;
+      double2 q[kCols][RP];
+#pragma unroll
+      for (int cc = 0; cc < kCols; ++cc) {
+        if (g * kCols + cc < p.j) {
+#pragma unroll
+          for (int r = 0; r < RP; ++r)
+            q[cc][r] = *reinterpret_cast<const double2*>(qs + cc * kUR + wrow + 64 * r + 2 * lane);
+        } else {
+#pragma unroll
+          for (int r = 0; r < RP; ++r) q[cc][r] = make_double2(0.0, 0.0);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + s);
+#pragma unroll
+      for (int cc = 0; cc < kCols; ++cc) {
+        const double2 ct = sct[g * kCols + cc];
+#pragma unroll
+        for (int r = 0; r < RP; ++r) {
+          ac[r].x = fma(q[cc][r].x, ct.x, ac[r].x);
+          ac[r].y = fma(q[cc][r].y, ct.x, ac[r].y);
+          at[r].x = fma(q[cc][r].x, ct.y, at[r].x);
+          at[r].y = fma(q[cc][r].y, ct.y, at[r].y);
+        }
+      }
+    }
+    const int xs = xuse & 1;
+    mbar_wait(xfull + xs, (xuse >> 1) & 1);
+    const double* xb = xbuf + static_cast<size_t>(xs) * 2 * kUR;
+    double2 wv[RP], av[RP];
+#pragma unroll
+    for (int r = 0; r < RP; ++r) {
+      wv[r] = *reinterpret_cast<const double2*>(xb + wrow + 64 * r + 2 * lane);
+      av[r] = *reinterpret_cast<const double2*>(xb + kUR + wrow + 64 * r + 2 * lane);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(xempty + xs);
+#pragma unroll
+    for (int r = 0; r < RP; ++r) {
+      const int64_t row = c * kUR + wrow + 64 * r + 2 * lane;
+      double2 qn, wn;
+      qn.x = (wv[r].x - ac[r].x) / p.alpha;
+      qn.y = (wv[r].y - ac[r].y) / p.alpha;
+      const double ax = p.divide ? av[r].x / p.alpha : av[r].x;
+      const double ay = p.divide ? av[r].y / p.alpha : av[r].y;
+      wn.x = ax - fma(qn.x, tj, at[r].x);
+      wn.y = ay - fma(qn.y, tj, at[r].y);
+      *reinterpret_cast<double2*>(qout + row) = qn;
+      *reinterpret_cast<double2*>(p.w + row) = wn;
+    }
+  }
+  if (nfull * kUR < p.m && (nfull % gridDim.x) == blockIdx.x)
+    upd_chunk<RP, true>(p, sct, tj, nfull * kUR + wrow, lane);
 }
 
 // ---------------------------------------------------------------------------
@@ -244,10 +387,31 @@ int set_smem(const void* fn, size_t smem) {
 
 bool misaligned(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) != 0; }
 
+// K2 variant: TMA-staged by default, KLS_UPDATE=ldg selects the LDG kernel.
+bool update_tma() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("KLS_UPDATE");
+    v = (e && e[0] == 'l') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 template <int NC>
 int launch_update(const UpdParams& p, const double* host_coef, cudaStream_t st) {
   CoefPack<NC> pk;
   if (NC > 0) std::memcpy(pk.v, host_coef, sizeof(double) * (2 * p.j + 1));
+  const int jp = (p.j + kCols - 1) / kCols * kCols;
+  const size_t tsmem = 256 + sizeof(double2) * (jp + 1) +
+                       sizeof(double) * (static_cast<size_t>(kUStages) * kCols * kUR + 4 * kUR);
+  if (update_tma() && p.j > 0 && p.m >= kUR && tsmem <= 227 * 1024 && !misaligned(p.Q) &&
+      !misaligned(p.w) && !misaligned(p.aw) && (p.ldq % 2) == 0) {
+    int rc = set_smem(reinterpret_cast<const void*>(dcgs2_update_tma_kernel<NC>), tsmem);
+    if (rc) return rc;
+    const int grid = static_cast<int>(std::min<int64_t>((p.m + kUR - 1) / kUR, sm_count()));
+    dcgs2_update_tma_kernel<NC><<<grid, kUThreads, tsmem, st>>>(p, pk);
+    return check_launch("dcgs2_update_tma_kernel");
+  }
   const size_t smem = sizeof(double2) * static_cast<size_t>((p.j + kCols - 1) / kCols * kCols + 1);
   int rc = set_smem(reinterpret_cast<const void*>(dcgs2_update_kernel<kUpdRP, NC>), smem);
   if (rc) return rc;
