@@ -72,11 +72,17 @@ def main():
     summary = {"launch_list": launches(a.launches)}
     if a.report:
         kern = full(a.report)
-        algo = {"gram_kernel": 8 * a.m * (a.j + 2), "dcgs2_update_kernel": 8 * a.m * (a.j + 4),
-                "stencil7_kernel": 16 * a.m}
+        algo = {"gram": 8 * a.m * (a.j + 2), "update": 8 * a.m * (a.j + 4), "stencil7": 16 * a.m}
+
+        def family(name):
+            for key in ("gram", "update", "stencil7"):
+                if key in name:
+                    return key
+            return None
+
         for d in kern:
-            base = d["kernel"].split("<")[0]
-            d["algorithmic_bytes"] = algo.get(base)
+            d["family"] = family(d["kernel"])
+            d["algorithmic_bytes"] = algo.get(d["family"])
             dram = d.get("dram__bytes_read.sum", 0) + d.get("dram__bytes_write.sum", 0)
             d["dram_bytes"] = dram
             if d["algorithmic_bytes"]:
@@ -85,9 +91,9 @@ def main():
         summary["ncu_full"] = kern
         summary["capture"] = {"m": a.m, "j": a.j}
         # per-kernel traffic entries bench.py reads
-        for name, key in (("gram_kernel", "gram"), ("dcgs2_update_kernel", "update")):
+        for key in ("gram", "update", "stencil7"):
             for d in kern:
-                if d["kernel"].startswith(name):
+                if d["family"] == key:
                     summary[key] = {"dram_bytes": d["dram_bytes"], "j": a.j,
                                     "algorithmic_bytes": d["algorithmic_bytes"],
                                     "traffic_over_algorithmic": d["traffic_over_algorithmic"]}
