@@ -48,6 +48,9 @@ def parse():
     ap.add_argument("--dims", default=",".join(map(str, FULL_DIMS)))
     ap.add_argument("--n", type=int, default=100, help="Arnoldi iterations per expansion")
     ap.add_argument("--scheme", default="dcgs2", choices=("dcgs2", "cgs2"))
+    ap.add_argument("--operator", default="stencil", choices=("stencil", "csr"),
+                    help="matrix-free stencil (the reference's laplace3d) or the same "
+                         "operator as a device-assembled CSR matrix")
     ap.add_argument("--sample-dims", default=",".join(map(str, SAMPLE_DIMS)))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -238,7 +241,7 @@ def run_ours(args):
 
     dims = dims_of(args.dims)
     m = dims[0] * dims[1] * dims[2]
-    op = kls.laplace3d(*dims)
+    op = kls.laplace3d(*dims) if args.operator == "stencil" else kls.laplace3d_csr_operator(*dims)
     lo, hi = op.row_lo, op.row_hi
     # start vector: the global PCG64(1729) stream, this rank's rows
     full = np.random.Generator(np.random.PCG64(1729)).standard_normal(m)
@@ -353,7 +356,9 @@ def run_ours(args):
         "dtype": "f64",
         "data": "synthetic: PCG64(1729) standard-normal start vector, matrix-free 3-D Poisson",
         "config": {"workload": workload_name(dims, args.n, args.scheme), "m": m, "n": args.n,
-                   "scheme": args.scheme, "operator": "laplace3d 7-point, matrix-free",
+                   "scheme": args.scheme,
+                   "operator": ("laplace3d 7-point, matrix-free" if args.operator == "stencil"
+                                else "laplace3d 7-point as device-assembled CSR (int32 cols)"),
                    "parallelism": f"row-shard over {world} GPU(s), 1 allreduce/iteration",
                    "l2": "inputs larger than L2 (Q = %.1f GB)" % (8 * m * (args.n + 1) / 1e9)},
         "hbm_gbs": total_bytes / sec / 1e9 / world,

@@ -132,6 +132,20 @@ int kls_resid_norms(const double* b, const double* ax, const double* x, int64_t 
 int kls_tsgemm_inplace(double* V, int64_t ldv, int64_t m, int32_t k, const double* Z,
                        void* stream);
 
+/* ---- device-side operator construction -------------------
+ * CSR of a row block [row_lo, row_lo + nrows) built directly in HBM, entry
+ * for entry identical to the reference's host assembly; columns are stored
+ * relative to the global row col_base (the rank's extended-vector origin);
+ * rowptr (nrows + 1 entries) starts at 0.  *_nnz give the block's size. */
+int64_t kls_lap7_nnz(int64_t nx, int64_t ny, int64_t nz, int64_t row_lo, int64_t row_hi);
+/* StencilLaplace3D.to_csr (problems.py:307-331). */
+int kls_build_lap7_csr(int64_t nx, int64_t ny, int64_t nz, int64_t row_lo, int64_t nrows,
+                       int64_t col_base, int64_t* rowptr, int32_t* col, double* val, void* stream);
+int64_t kls_mant5_nnz(int64_t k, int64_t row_lo, int64_t row_hi);
+/* manteuffel_build (problems.py:208-245); diff = 1/h^2, conv = beta/(2h). */
+int kls_build_mant5_csr(int64_t k, int64_t row_lo, int64_t nrows, int64_t col_base, double diff,
+                        double conv, int64_t* rowptr, int32_t* col, double* val, void* stream);
+
 /* ---- cross-GPU exchange over NVLink peer memory ---------------------------
  * Symmetric buffers (same layout on every rank, mapped into every peer) of
  * kls_peer_buffer_bytes(cap) bytes; bufs[r] is rank r's buffer as seen from

@@ -46,6 +46,10 @@ SIGNATURES = {
     "kls_resid_norms": (ctypes.c_int, [c_dp, c_dp, c_dp, i64, c_dp, c_dp, sz, c_dp]),
     "kls_tsgemm_inplace": (ctypes.c_int, [c_dp, i64, i64, i32, c_dp, c_dp]),
     "kls_peer_buffer_bytes": (sz, [i32]),
+    "kls_lap7_nnz": (i64, [i64, i64, i64, i64, i64]),
+    "kls_build_lap7_csr": (ctypes.c_int, [i64, i64, i64, i64, i64, i64, c_dp, c_dp, c_dp, c_dp]),
+    "kls_mant5_nnz": (i64, [i64, i64, i64]),
+    "kls_build_mant5_csr": (ctypes.c_int, [i64, i64, i64, i64, f64, f64, c_dp, c_dp, c_dp, c_dp]),
     "kls_peer_allreduce": (ctypes.c_int, [c_dp, i32, c_dp, c_dp, i32, i32, i32, ctypes.c_uint64,
                                           c_dp, c_dp]),
     "kls_peer_signal": (ctypes.c_int, [c_dp, i32, i32, i32, ctypes.c_uint64, c_dp]),
@@ -55,7 +59,8 @@ SIGNATURES = {
 
 # entry points that launch no kernel (not counted as GPU launches)
 _NO_LAUNCH = frozenset({"kls_version", "kls_last_error", "kls_device_sm_count", "kls_stream_sync",
-                        "kls_host_device_ptr", "kls_workspace_bytes", "kls_peer_buffer_bytes"})
+                        "kls_host_device_ptr", "kls_workspace_bytes", "kls_peer_buffer_bytes",
+                        "kls_lap7_nnz", "kls_mant5_nnz"})
 
 _lock = threading.Lock()
 _lib = None

@@ -380,15 +380,39 @@ class CsrOperator(LinearOperator):
         self.halo_hi = max(0, max(cmax + 1, hi) - hi)
         base = lo - self.halo_lo  # global row of ext[0] (HaloVector.ext_ptr)
         dev = runtime.device()
-        self._rowptr = torch.from_numpy(csr.indptr[lo : hi + 1] - s).to(dev)
-        self._col = torch.from_numpy((cols - base).astype(np.int32)).to(dev)
-        self._val = torch.from_numpy(np.ascontiguousarray(csr.data[s:e])).to(dev)
-        self._rowptr_p = self._rowptr.data_ptr()
-        self._col_p = self._col.data_ptr()
-        self._val_p = self._val.data_ptr()
+        self._set_arrays(torch.from_numpy(csr.indptr[lo : hi + 1] - s).to(dev),
+                         torch.from_numpy((cols - base).astype(np.int32)).to(dev),
+                         torch.from_numpy(np.ascontiguousarray(csr.data[s:e])).to(dev))
+
+    def _set_arrays(self, rowptr, col, val):
+        self._rowptr, self._col, self._val = rowptr, col, val
+        self._rowptr_p = rowptr.data_ptr()
+        self._col_p = col.data_ptr()
+        self._val_p = val.data_ptr()
         self._plan = None
         if self.comm.world > 1:
             self._plan = self._halo_plan()
+
+    @classmethod
+    def _device_built(cls, n, band, nnz_fn, build_fn, comm=None):
+        """Row block assembled in HBM by a libklsgpu builder.  ``band`` is the
+        operator's half bandwidth (halo rows on each side)."""
+        if n >= 2**31:
+            raise DimensionError("column indices must fit in int32")
+        self = cls.__new__(cls)
+        LinearOperator.__init__(self, n, comm)
+        self.csr = None
+        lo, hi = self.row_lo, self.row_hi
+        self.halo_lo = min(band, lo)
+        self.halo_hi = min(band, n - hi)
+        nnz = int(nnz_fn(lo, hi))
+        dev = runtime.device()
+        rowptr = torch.empty(hi - lo + 1, dtype=torch.int64, device=dev)
+        col = torch.empty(max(nnz, 1), dtype=torch.int32, device=dev)
+        val = torch.empty(max(nnz, 1), dtype=torch.float64, device=dev)
+        build_fn(lo, hi - lo, lo - self.halo_lo, rowptr.data_ptr(), col.data_ptr(), val.data_ptr())
+        self._set_arrays(rowptr, col, val)
+        return self
 
     def _needs_halo(self):
         return self.halo_lo > 0 or self.halo_hi > 0
@@ -432,11 +456,21 @@ class CsrOperator(LinearOperator):
     def to_dense(self, max_order=4000):
         if self.n > max_order:
             raise MemoryError(f"dense assembly of order {self.n} refused (limit {max_order})")
+        if self.csr is None:
+            return LinearOperator.to_dense(self, max_order)
         return self.csr.to_dense()
 
     def frobenius_norm(self, samples=None, seed=None):
+        """||data||_F: exact from the host CSR (problems.py:150-151), or summed
+        on the device (and over ranks) for a device-built operator."""
         if self._fro is None:
-            self._fro = self.csr.frobenius_norm()
+            if self.csr is not None:
+                self._fro = self.csr.frobenius_norm()
+            else:
+                from . import kernels
+
+                v = self._val[: int(self._rowptr[-1].item())]
+                self._fro = float(np.sqrt(kernels.dot(v, v, comm=self.comm) if v.numel() else 0.0))
         return self._fro
 
 
@@ -695,6 +729,41 @@ class StencilLaplace3D(LinearOperator):
 
 def laplace3d(nx, ny, nz, comm=None):
     return StencilLaplace3D(nx, ny, nz, comm)
+
+
+def laplace3d_csr_operator(nx, ny, nz, comm=None):
+    """The 7-point Laplacian as a CSR operator assembled on the device —
+    the same entries as CsrOperator(laplace3d(nx, ny, nz).to_csr()) without
+    the host COO assembly."""
+    lib = _lib.load()
+    st = runtime.stream_handle()
+
+    def nnz(lo, hi):
+        return lib.kls_lap7_nnz(nx, ny, nz, lo, hi)
+
+    def build(lo, nrows, base, rp, cp, vp):
+        _lib.call("kls_build_lap7_csr", nx, ny, nz, lo, nrows, base, rp, cp, vp, st)
+
+    return CsrOperator._device_built(nx * ny * nz, ny * nz, nnz, build, comm)
+
+
+def manteuffel_operator(spec, comm=None):
+    """CsrOperator(manteuffel_build(spec)) assembled on the device (same
+    entries and rounding; diff and conv computed on the host as the
+    reference does, problems.py:235-236)."""
+    lib = _lib.load()
+    st = runtime.stream_handle()
+    k = spec.k
+    diff = 1.0 / (spec.h * spec.h)
+    conv = spec.beta / (2.0 * spec.h)
+
+    def nnz(lo, hi):
+        return lib.kls_mant5_nnz(k, lo, hi)
+
+    def build(lo, nrows, base, rp, cp, vp):
+        _lib.call("kls_build_mant5_csr", k, lo, nrows, base, diff, conv, rp, cp, vp, st)
+
+    return CsrOperator._device_built(k * k, k, nnz, build, comm)
 
 
 # ---------------------------------------------------------------------------

@@ -215,3 +215,30 @@ def test_errors_surface_as_exceptions(cuda):
 
     with pytest.raises(_lib.KlsGpuError):
         _lib.call("kls_gram_dcgs2", None, 1, 10, 3, None, None, None, None, 0, None)
+
+
+@pytest.mark.parametrize("dims", [(5, 4, 6), (1, 1, 1), (3, 1, 7), (8, 8, 8), (17, 9, 33)])
+def test_device_built_laplace_csr_matches_host(cuda, rng, dims):
+    from paper_2104_01253_b200 import laplace3d, laplace3d_csr_operator
+
+    dev = laplace3d_csr_operator(*dims)
+    ptr, idx, dat = oracle.laplace3d_csr(*dims)
+    assert np.array_equal(dev._rowptr.cpu().numpy(), ptr)
+    assert np.array_equal(dev._col.cpu().numpy()[: ptr[-1]], idx)
+    assert np.array_equal(dev._val.cpu().numpy()[: ptr[-1]], dat)
+    x = rng.standard_normal(int(np.prod(dims)))
+    assert np.array_equal(dev.apply(x).cpu().numpy(), laplace3d(*dims).apply(x).cpu().numpy())
+    assert dev.frobenius_norm() == pytest.approx(float(np.linalg.norm(dat)), rel=1e-14)
+
+
+@pytest.mark.parametrize("k,beta", [(1, 0.5), (2, 0.5), (7, 0.3), (10, 0.5), (31, 0.0)])
+def test_device_built_manteuffel_matches_host(cuda, rng, k, beta):
+    from paper_2104_01253_b200 import ManteuffelSpec, manteuffel_operator
+
+    dev = manteuffel_operator(ManteuffelSpec(k=k, beta=beta))
+    ptr, idx, dat = oracle.manteuffel_csr(k, beta)
+    assert np.array_equal(dev._rowptr.cpu().numpy(), ptr)
+    assert np.array_equal(dev._col.cpu().numpy()[: ptr[-1]], idx)
+    assert np.array_equal(dev._val.cpu().numpy()[: ptr[-1]], dat)
+    x = rng.standard_normal(k * k)
+    assert np.array_equal(dev.apply(x).cpu().numpy(), oracle.csr_matvec(ptr, idx, dat, x))
