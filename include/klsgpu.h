@@ -105,6 +105,16 @@ int kls_mv_times_mat_add_mv_host(double* Y, int64_t ldy, int64_t m, int32_t l, c
 int kls_csr_spmv(const int64_t* rowptr, const int32_t* col, const double* val, int64_t nrows,
                  const double* x, double* y, void* stream);
 
+/* ELL copy of a CSR block with <= width (<= 8) entries per row: entry k of
+ * row i at k*ld + i (coalesced streams); elen[i] = row length. */
+int kls_csr_to_ell(const int64_t* rowptr, const int32_t* col, const double* val, int64_t nrows,
+                   int32_t width, int64_t ld, int32_t* ecol, double* eval, uint8_t* elen,
+                   void* stream);
+/* y = A x from that layout, bit-identical to kls_csr_spmv (same per-row
+ * entry order, same reduceat summation). */
+int kls_ell_spmv(const int32_t* ecol, const double* eval, const uint8_t* elen, int32_t width,
+                 int64_t nrows, int64_t ld, const double* x, double* y, void* stream);
+
 /* Matrix-free 7-point Laplacian, bit-identical to StencilLaplace3D._matvec
  * (problems.py:296-305) on nx local x-planes of a (.., ny, nz) grid; x_lo /
  * x_hi are the neighbouring planes of other ranks (NULL at the boundary). */

@@ -39,6 +39,8 @@ SIGNATURES = {
         [c_dp, i64, i64, i32, c_dp, i64, i32, c_dp, f64, f64, c_dp, c_dp, sz, c_dp],
     ),
     "kls_csr_spmv": (ctypes.c_int, [c_dp, c_dp, c_dp, i64, c_dp, c_dp, c_dp]),
+    "kls_csr_to_ell": (ctypes.c_int, [c_dp, c_dp, c_dp, i64, i32, i64, c_dp, c_dp, c_dp, c_dp]),
+    "kls_ell_spmv": (ctypes.c_int, [c_dp, c_dp, c_dp, i32, i64, i64, c_dp, c_dp, c_dp]),
     "kls_stencil7": (ctypes.c_int, [c_dp, c_dp, c_dp, c_dp, i64, i64, i64, c_dp]),
     "kls_dense_gemv": (ctypes.c_int, [c_dp, i64, i64, c_dp, c_dp, c_dp]),
     "kls_scale": (ctypes.c_int, [c_dp, c_dp, i64, f64, i32, c_dp]),

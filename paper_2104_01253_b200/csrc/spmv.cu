@@ -53,19 +53,127 @@ __device__ double csr_pairwise(const int32_t* __restrict__ col, const double* __
   return __dadd_rn(csr_pairwise(col, val, x, s, n2), csr_pairwise(col, val, x, s + n2, n - n2));
 }
 
+// One warp per 32 consecutive rows.  The warp first copies the rows'
+// contiguous slice of column indices and values into shared memory with
+// coalesced loads (the 12 B/nnz stream is read once, in full sectors), then
+// each lane forms its row's products — all gathers of a row issued together —
+// and sums them in reduceat order: p0 + (((-0.0 + p1) + p2) + ...).  Rows
+// longer than 8 entries, or warps whose slice exceeds the staging buffer,
+// use the general pairwise routine on global memory.
+constexpr int kSpmvStage = 32 * 8;  // staged entries per warp
+
 __global__ void __launch_bounds__(kThreads) csr_spmv_kernel(const int64_t* __restrict__ rowptr,
                                                             const int32_t* __restrict__ col,
                                                             const double* __restrict__ val,
                                                             int64_t nrows,
                                                             const double* __restrict__ x,
                                                             double* __restrict__ y) {
+  __shared__ int32_t scol[kWarps][kSpmvStage];
+  __shared__ double sval[kWarps][kSpmvStage];
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = static_cast<int64_t>(gridDim.x) * kWarps;
+  for (int64_t r0 = (static_cast<int64_t>(blockIdx.x) * kWarps + warp) * 32; r0 < nrows;
+       r0 += nwarps * 32) {
+    const int64_t i = r0 + lane;
+    const bool live = i < nrows;
+    const int64_t s = live ? __ldg(rowptr + i) : 0;
+    const int64_t e = live ? __ldg(rowptr + i + 1) : 0;
+    const int64_t wlast = min(r0 + 32, nrows);
+    const int64_t ws = __shfl_sync(0xffffffffu, s, 0);
+    const int64_t we = __ldg(rowptr + wlast);
+    const int64_t total = we - ws;
+    const bool staged = total <= kSpmvStage;
+    if (staged) {
+      for (int64_t k = lane; k < total; k += 32) {
+        scol[warp][k] = __ldg(col + ws + k);
+        sval[warp][k] = __ldg(val + ws + k);
+      }
+    }
+    __syncwarp();
+    const int64_t n = e - s;
+    double acc = 0.0;
+    if (live && n > 0 && n <= 8) {
+      int32_t c[8];
+      double v[8];
+      const int64_t o = s - ws;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        if (staged) {
+          c[k] = k < n ? scol[warp][o + k] : 0;
+          v[k] = k < n ? sval[warp][o + k] : 0.0;
+        } else {
+          c[k] = k < n ? __ldg(col + s + k) : 0;
+          v[k] = k < n ? __ldg(val + s + k) : 0.0;
+        }
+      }
+      double p[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) p[k] = k < n ? __dmul_rn(v[k], __ldg(x + c[k])) : 0.0;
+      double r = -0.0;
+#pragma unroll
+      for (int k = 1; k < 8; ++k)
+        if (k < n) r = __dadd_rn(r, p[k]);
+      acc = __dadd_rn(p[0], r);
+    } else if (live && n > 8) {
+      acc = __dadd_rn(csr_prod(col, val, x, s), csr_pairwise(col, val, x, s + 1, n - 1));
+    }
+    if (live) y[i] = acc;
+    __syncwarp();
+  }
+}
+
+// ELL copy of a CSR block for short-row operators (stencils, 5/7-point):
+// entry k of row i at k * ld + i, so lane-consecutive rows read consecutive
+// addresses (fully coalesced 4 B / 8 B streams).  Per-row entry order is the
+// CSR order, so the product is still formed in reduceat order and stays
+// bit-identical to CsrMatrix.matvec.
+__global__ void csr_to_ell_kernel(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+                                  const double* __restrict__ val, int64_t nrows, int32_t width,
+                                  int64_t ld, int32_t* __restrict__ ecol, double* __restrict__ eval,
+                                  uint8_t* __restrict__ elen) {
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nrows;
        i += stride) {
-    const int64_t s = __ldg(rowptr + i);
-    const int64_t e = __ldg(rowptr + i + 1);
+    const int64_t s = rowptr[i];
+    const int n = static_cast<int>(rowptr[i + 1] - s);
+    elen[i] = static_cast<uint8_t>(n);
+    for (int k = 0; k < width; ++k) {
+      ecol[k * ld + i] = k < n ? col[s + k] : 0;
+      eval[k * ld + i] = k < n ? val[s + k] : 0.0;
+    }
+  }
+}
+
+template <int W>
+__global__ void __launch_bounds__(kThreads) ell_spmv_kernel(const int32_t* __restrict__ ecol,
+                                                            const double* __restrict__ eval,
+                                                            const uint8_t* __restrict__ elen,
+                                                            int64_t nrows, int64_t ld,
+                                                            const double* __restrict__ x,
+                                                            double* __restrict__ y) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nrows;
+       i += stride) {
+    const int n = __ldg(elen + i);
+    int32_t c[W];
+    double v[W];
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+      c[k] = k < n ? __ldg(ecol + k * ld + i) : 0;
+      v[k] = k < n ? __ldg(eval + k * ld + i) : 0.0;
+    }
+    double p[W];
+#pragma unroll
+    for (int k = 0; k < W; ++k) p[k] = k < n ? __dmul_rn(v[k], __ldg(x + c[k])) : 0.0;
     double acc = 0.0;
-    if (e > s) acc = __dadd_rn(csr_prod(col, val, x, s), csr_pairwise(col, val, x, s + 1, e - s - 1));
+    if (n > 0) {
+      double r = -0.0;
+#pragma unroll
+      for (int k = 1; k < W; ++k)
+        if (k < n) r = __dadd_rn(r, p[k]);
+      acc = __dadd_rn(p[0], r);
+    }
     y[i] = acc;
   }
 }
@@ -111,8 +219,10 @@ KLS_API int kls_csr_spmv(const int64_t* rowptr, const int32_t* col, const double
   if (nrows < 0 || rowptr == nullptr || x == nullptr || y == nullptr)
     return fail(KLS_EINVAL, "csr_spmv: bad arguments");
   if (nrows == 0) return KLS_OK;
-  csr_spmv_kernel<<<grid_1d(nrows, 8), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
-      rowptr, col, val, nrows, x, y);
+  const int64_t blocks = ceil_div(nrows, 32 * kWarps);
+  const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(blocks, 8LL * sm_count())));
+  csr_spmv_kernel<<<grid, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(rowptr, col, val, nrows,
+                                                                            x, y);
   return check_launch("csr_spmv_kernel");
 }
 
@@ -149,4 +259,37 @@ KLS_API int kls_dense_gemv(const double* a, int64_t lda, int64_t n, const double
   const int grid = static_cast<int>(std::min<int64_t>(blocks, 8LL * sm_count()));
   dense_gemv_kernel<<<grid, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(a, lda, n, x, y);
   return check_launch("dense_gemv_kernel");
+}
+
+// Convert a CSR block whose rows hold <= width (<= 8) entries to the ELL
+// layout above (ecol / eval: width * ld entries, elen: nrows bytes).
+KLS_API int kls_csr_to_ell(const int64_t* rowptr, const int32_t* col, const double* val,
+                           int64_t nrows, int32_t width, int64_t ld, int32_t* ecol, double* eval,
+                           uint8_t* elen, void* stream) {
+  if (rowptr == nullptr || nrows < 0 || width < 1 || width > 8 || ld < nrows || ecol == nullptr ||
+      eval == nullptr || elen == nullptr)
+    return fail(KLS_EINVAL, "csr_to_ell: bad arguments");
+  if (nrows == 0) return KLS_OK;
+  csr_to_ell_kernel<<<grid_1d(nrows, 8), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+      rowptr, col, val, nrows, width, ld, ecol, eval, elen);
+  return check_launch("csr_to_ell_kernel");
+}
+
+// y = A x from the ELL layout; bit-identical to kls_csr_spmv on the same rows.
+KLS_API int kls_ell_spmv(const int32_t* ecol, const double* eval, const uint8_t* elen,
+                         int32_t width, int64_t nrows, int64_t ld, const double* x, double* y,
+                         void* stream) {
+  if (ecol == nullptr || eval == nullptr || elen == nullptr || x == nullptr || y == nullptr ||
+      nrows < 0 || ld < nrows || width < 1 || width > 8)
+    return fail(KLS_EINVAL, "ell_spmv: bad arguments");
+  if (nrows == 0) return KLS_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int grid = grid_1d(nrows, 8);
+  if (width <= 4)
+    ell_spmv_kernel<4><<<grid, kThreads, 0, st>>>(ecol, eval, elen, nrows, ld, x, y);
+  else if (width <= 6)
+    ell_spmv_kernel<6><<<grid, kThreads, 0, st>>>(ecol, eval, elen, nrows, ld, x, y);
+  else
+    ell_spmv_kernel<8><<<grid, kThreads, 0, st>>>(ecol, eval, elen, nrows, ld, x, y);
+  return check_launch("ell_spmv_kernel");
 }

@@ -384,12 +384,30 @@ class CsrOperator(LinearOperator):
                          torch.from_numpy((cols - base).astype(np.int32)).to(dev),
                          torch.from_numpy(np.ascontiguousarray(csr.data[s:e])).to(dev))
 
+    # rows of at most this many entries are also stored as ELL (coalesced
+    # streams, same products and summation order as the CSR kernel)
+    ELL_MAX_WIDTH = 8
+
     def _set_arrays(self, rowptr, col, val):
         self._rowptr, self._col, self._val = rowptr, col, val
         self._rowptr_p = rowptr.data_ptr()
         self._col_p = col.data_ptr()
         self._val_p = val.data_ptr()
         self._plan = None
+        self._ell = None
+        nrows = rowptr.numel() - 1
+        if nrows > 0:
+            width = int((rowptr[1:] - rowptr[:-1]).max().item())
+            if 1 <= width <= self.ELL_MAX_WIDTH:
+                ld = runtime.pad_rows(nrows)
+                dev = rowptr.device
+                ecol = torch.empty(width * ld, dtype=torch.int32, device=dev)
+                evals = torch.empty(width * ld, dtype=torch.float64, device=dev)
+                elen = torch.empty(ld, dtype=torch.uint8, device=dev)
+                _lib.call("kls_csr_to_ell", self._rowptr_p, self._col_p, self._val_p, nrows, width,
+                          ld, ecol.data_ptr(), evals.data_ptr(), elen.data_ptr(),
+                          runtime.stream_handle())
+                self._ell = (ecol, evals, elen, width, ld)
         if self.comm.world > 1:
             self._plan = self._halo_plan()
 
@@ -446,10 +464,18 @@ class CsrOperator(LinearOperator):
         _p2p(ops)
 
     def apply_bytes(self):
-        """x and y, plus values (8), column indices (4) and row pointers (8)."""
+        """x and y, plus values (8) and column indices (4) per stored entry,
+        and row pointers (8) or ELL row lengths (1) per row."""
+        if self._ell is not None:
+            return 16 * self.m_local + 12 * self._ell[3] * self.m_local + self.m_local
         return 16 * self.m_local + 12 * int(self._col.numel()) + 8 * (self.m_local + 1)
 
     def _launch(self, x, y, st):
+        if self._ell is not None:
+            ecol, evals, elen, width, ld = self._ell
+            _lib.call("kls_ell_spmv", ecol.data_ptr(), evals.data_ptr(), elen.data_ptr(), width,
+                      self.m_local, ld, x.ext_ptr, y.data_ptr(), st)
+            return
         _lib.call("kls_csr_spmv", self._rowptr_p, self._col_p, self._val_p, self.m_local,
                   x.ext_ptr, y.data_ptr(), st)
 

@@ -227,7 +227,11 @@ def test_device_built_laplace_csr_matches_host(cuda, rng, dims):
     assert np.array_equal(dev._col.cpu().numpy()[: ptr[-1]], idx)
     assert np.array_equal(dev._val.cpu().numpy()[: ptr[-1]], dat)
     x = rng.standard_normal(int(np.prod(dims)))
-    assert np.array_equal(dev.apply(x).cpu().numpy(), laplace3d(*dims).apply(x).cpu().numpy())
+    # the CSR product sums in reduceat order (not the stencil's), like the
+    # reference's CsrOperator(laplace3d(...).to_csr())
+    assert np.array_equal(dev.apply(x).cpu().numpy(), oracle.csr_matvec(ptr, idx, dat, x))
+    assert np.allclose(dev.apply(x).cpu().numpy(), laplace3d(*dims).apply(x).cpu().numpy(),
+                       rtol=1e-13, atol=1e-13)
     assert dev.frobenius_norm() == pytest.approx(float(np.linalg.norm(dat)), rel=1e-14)
 
 
