@@ -174,6 +174,30 @@ class Engine:
             return float(self._finish(1)[0])
         return None
 
+    def add_combination(self, y, x, k, coef):
+        """y = x + Q(:, 0:k) coef (host coefficients ride in the launch)."""
+        if y.data_ptr() != x.data_ptr():
+            y.copy_(x)
+        if k == 0:
+            return
+        c = np.ascontiguousarray(coef[:k], dtype=np.float64)
+        trace.note("mtm", 8 * self.ml * (k + 2))
+        if k <= _PACK:
+            _lib.call("kls_mv_times_mat_add_mv_host", y.data_ptr(), self.ld, self.ml, 1, self.qptr,
+                      self.ld, k, c.ctypes.data, 1.0, 1.0, None, self.ws, self.wsb, self.st)
+        else:
+            dev = self.stage.push(c)
+            _lib.call("kls_mv_times_mat_add_mv", y.data_ptr(), self.ld, self.ml, 1, self.qptr,
+                      self.ld, k, dev.data_ptr(), 1.0, 1.0, None, self.ws, self.wsb, self.st)
+
+    def resid_norms(self, b, ax, x):
+        """[||b - ax||^2, ||x||^2, ||b||^2] over all ranks, one pass."""
+        out = self._out(3)
+        trace.note("resid_norms", 24 * self.ml)
+        _lib.call("kls_resid_norms", b.data_ptr(), ax.data_ptr(), x.data_ptr(), self.ml, out,
+                  self.ws, self.wsb, self.st)
+        return self._finish(3)
+
     def divide_into(self, dst, src, alpha):
         trace.note("scale", 16 * self.ml)
         _lib.call("kls_scale", src.data_ptr(), dst.data_ptr(), self.ml, float(alpha), 0, self.st)
