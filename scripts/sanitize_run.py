@@ -1,0 +1,17 @@
+"""Small end-to-end run for compute-sanitizer (memcheck / racecheck):
+every kernel family on odd sizes, TMA paths included (m >= 1024)."""
+import os, sys
+import numpy as np
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2104_01253_b200 as kls
+rng = np.random.default_rng(0)
+op = kls.laplace3d(13, 11, 17)             # m = 2431 (odd, > 1024: TMA path + ragged tail)
+s = rng.standard_normal(op.n)
+for scheme in ("dcgs2", "cgs2"):
+    kls.arnoldi_expand(op, s, scheme, 12)
+mop = kls.manteuffel_operator(kls.ManteuffelSpec(k=37))  # device-built CSR + ELL
+kls.gmres_solve(mop, rng.standard_normal(mop.n), kls.GmresConfig(max_iters=30, restart=10, rtol=1e-12, scheme="dcgs2"))
+kls.qr_factorize(rng.standard_normal((3001, 9)), "dcgs2")
+kls.krylov_schur_run(kls.CsrOperator(kls.manteuffel_build(kls.ManteuffelSpec(k=6))),
+                     kls.KrylovSchurConfig(max_basis=12, scheme="dcgs2", max_restarts=3), seed=1)
+print("sanitize run ok")
