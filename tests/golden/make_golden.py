@@ -232,6 +232,30 @@ def main():
         out[f"vals{i}"], out[f"vecs{i}"] = vals, vecs
         out[f"st{i}"], out[f"sz{i}"] = srt.t, srt.z
     np.savez_compressed(os.path.join(OUT, "schur.npz"), **out)
+
+    # -- kls-bench CLI outputs (data rows) and the QR-sweep generator ----------
+    import contextlib
+    import io
+    from kls import cli
+
+    out = {}
+    runs = {
+        "sync": ["sync-count", "--rows", "600", "--cols", "20"],
+        "qr": ["qr-stability", "--rows", "120", "--cols", "12", "--kappa-list", "1e0,1e4,1e8"],
+        "arnoldi": ["arnoldi-stability", "--manteuffel-k", "12", "--steps", "30", "--stride", "10"],
+        "gmres": ["gmres", "--laplace-dims", "6,5,4", "--steps", "25", "--restart", "10"],
+        "eig": ["eig", "--manteuffel-k", "6", "--restart-list", "12,20", "--max-restarts", "10"],
+    }
+    for name, argv in runs.items():
+        argv = argv + ["--scheme", "dcgs2", "--scheme", "cgs2"]
+        buf = io.StringIO()
+        with contextlib.redirect_stdout(buf):
+            rc = cli.main(argv)
+        out[f"{name}_argv"] = np.array(argv)
+        out[f"{name}_rc"] = rc
+        out[f"{name}_csv"] = np.array(buf.getvalue())
+    out["kappa_matrix"] = kls.synthetic_kappa(60, 8, 1e6, seed=3)
+    np.savez_compressed(os.path.join(OUT, "cli.npz"), **out)
     print("golden fixtures written to", OUT)
 
 
