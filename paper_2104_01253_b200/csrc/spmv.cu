@@ -186,6 +186,27 @@ __global__ void __launch_bounds__(kTileZ * kTileY) stencil7_kernel(
   stencil7_march(x, x_lo, x_hi, y, nx, ny, nz, xa, xb);
 }
 
+__global__ void __launch_bounds__(32 * kSTY) stencil7_smem_kernel(
+    const double* __restrict__ x, const double* __restrict__ x_lo, const double* __restrict__ x_hi,
+    double* __restrict__ y, int64_t nx, int32_t ny, int32_t nz, int32_t xchunk) {
+  __shared__ double tile[kSTY + 2][kSTZ + 2];
+  const int64_t xa = static_cast<int64_t>(blockIdx.z) * xchunk;
+  const int64_t xb = xa + xchunk < nx ? xa + xchunk : nx;
+  if (xa >= xb) return;  // uniform per CTA: no thread reaches a barrier
+  stencil7_tile_march(x, x_lo, x_hi, y, nx, ny, nz, xa, xb, tile);
+}
+
+// stencil variant: 1 = shared-memory tiles (default), 0 = register march
+// (KLS_STENCIL=reg)
+int stencil_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("KLS_STENCIL");
+    v = (e && e[0] == 'r') ? 0 : 1;
+  }
+  return v;
+}
+
 // dense y = A x, A row-major n x n (DenseOperator, problems.py:68-85):
 // one warp per row
 __global__ void __launch_bounds__(kThreads) dense_gemv_kernel(const double* __restrict__ a,
@@ -241,8 +262,17 @@ KLS_API int kls_stencil7(const double* x, const double* x_lo, const double* x_hi
     const char* e = getenv("KLS_STENCIL_XCHUNK");
     env_chunk = e ? atoi(e) : 0;
   }
-  const int64_t xchunk = std::min<int64_t>(env_chunk > 0 ? env_chunk : 16, nx);
   dim3 grid;
+  if (stencil_variant() == 1) {
+    const int64_t xc = std::min<int64_t>(env_chunk > 0 ? env_chunk : 32, nx);
+    if (!stencil7_grid(nx, ny, nz, xc, grid, kSTZ, kSTY))
+      return fail(KLS_EINVAL, "stencil7: grid too large");
+    stencil7_smem_kernel<<<grid, dim3(32, kSTY), 0, static_cast<cudaStream_t>(stream)>>>(
+        x, x_lo, x_hi, y, nx, static_cast<int32_t>(ny), static_cast<int32_t>(nz),
+        static_cast<int32_t>(xc));
+    return check_launch("stencil7_smem_kernel");
+  }
+  const int64_t xchunk = std::min<int64_t>(env_chunk > 0 ? env_chunk : 16, nx);
   if (!stencil7_grid(nx, ny, nz, xchunk, grid)) return fail(KLS_EINVAL, "stencil7: grid too large");
   stencil7_kernel<<<grid, dim3(kTileZ, kTileY), 0, static_cast<cudaStream_t>(stream)>>>(
       x, x_lo, x_hi, y, nx, static_cast<int32_t>(ny), static_cast<int32_t>(nz),
