@@ -114,11 +114,12 @@ __global__ void peer_signal_kernel(Peers p, int target_mask, uint64_t epoch) {
 
 // Stencil with peer halos: CTAs whose chunk touches a rank boundary wait for
 // the neighbour's flag, then read its plane over NVLink.
-__global__ void __launch_bounds__(kTileZ * kTileY) stencil7_peer_kernel(
+__global__ void __launch_bounds__(32 * kSTY) stencil7_peer_kernel(
     const double* __restrict__ x, const double* x_lo, const double* x_hi, double* __restrict__ y,
     int64_t nx, int32_t ny, int32_t nz, int32_t xchunk, const uint64_t* flag_lo,
     const uint64_t* flag_hi, uint64_t epoch, int* err) {
   __shared__ int s_ok;
+  __shared__ double tile[kSTY + 2][kSTZ + 2];
   const int64_t xa = static_cast<int64_t>(blockIdx.z) * xchunk;
   const int64_t xb = xa + xchunk < nx ? xa + xchunk : nx;
   const bool need_lo = xa == 0 && x_lo != nullptr;
@@ -134,7 +135,8 @@ __global__ void __launch_bounds__(kTileZ * kTileY) stencil7_peer_kernel(
     __syncthreads();
     if (!s_ok) return;
   }
-  stencil7_march(x, x_lo, x_hi, y, nx, ny, nz, xa, xb);
+  if (xa >= xb) return;
+  stencil7_tile_march(x, x_lo, x_hi, y, nx, ny, nz, xa, xb, tile);
 }
 
 int make_peers(Peers& p, void* const* bufs, int rank, int world, int cap) {
@@ -200,11 +202,11 @@ KLS_API int kls_stencil7_peer(const double* x, const double* x_lo, const double*
   const uint64_t* flags = reinterpret_cast<const uint64_t*>(static_cast<char*>(mybuf)) + kMaxPeers;
   const uint64_t* flag_lo = rank > 0 ? flags + (rank - 1) : flags;
   const uint64_t* flag_hi = flags + (rank + 1 < kMaxPeers ? rank + 1 : rank);
-  const int64_t xchunk = std::min<int64_t>(16, nx);
+  const int64_t xchunk = std::min<int64_t>(32, nx);
   dim3 grid;
-  if (ny > INT32_MAX || nz > INT32_MAX || !stencil7_grid(nx, ny, nz, xchunk, grid))
+  if (ny > INT32_MAX || nz > INT32_MAX || !stencil7_grid(nx, ny, nz, xchunk, grid, kSTZ, kSTY))
     return fail(KLS_EINVAL, "stencil7_peer: grid too large");
-  stencil7_peer_kernel<<<grid, dim3(kTileZ, kTileY), 0, static_cast<cudaStream_t>(stream)>>>(
+  stencil7_peer_kernel<<<grid, dim3(32, kSTY), 0, static_cast<cudaStream_t>(stream)>>>(
       x, x_lo, x_hi, y, nx, static_cast<int32_t>(ny), static_cast<int32_t>(nz),
       static_cast<int32_t>(xchunk), flag_lo, flag_hi, epoch, err);
   return check_launch("stencil7_peer_kernel");
