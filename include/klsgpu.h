@@ -170,6 +170,15 @@ size_t kls_peer_buffer_bytes(int32_t cap);
 int kls_peer_allreduce(const double* src, int32_t nv, double* out, void* const* bufs, int32_t rank,
                        int32_t world, int32_t cap, uint64_t epoch, int* err, void* stream);
 
+/* kls_gram_dcgs2 fused with the step's global reduction: the kernel's last
+ * CTA performs the one-shot peer exchange itself and writes the rank-ordered
+ * global sum of the 2j+3 scalars to out — compute and collective in one
+ * launch (j <= 1024, 2j+3 <= cap). */
+int kls_gram_dcgs2_peer(const double* Q, int64_t ldq, int64_t m, int32_t j, const double* w,
+                        const double* aw, double* out, void* ws, size_t ws_bytes,
+                        void* const* bufs, int32_t rank, int32_t world, int32_t cap,
+                        uint64_t epoch, int* err, void* stream);
+
 /* Raise this rank's halo flag (= epoch) in the buffers of the ranks set in
  * target_mask, ordered after all prior work on the stream. */
 int kls_peer_signal(void* const* bufs, int32_t rank, int32_t world, int32_t target_mask,

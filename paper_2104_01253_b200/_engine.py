@@ -110,6 +110,8 @@ class Engine:
 
     def gram_dcgs2(self, j, w, aw):
         """[Q(:,0:j), w]^T [w, aw] and aw.aw over all ranks: 2j+3 values."""
+        if self.peer is not None and j <= 1024 and 2 * j + 3 <= self.res_np.size:
+            return self._gram_dcgs2_fused(j, w, aw)
         out = self._out(2 * j + 3)
         rec = trace._active
         if rec is None:
@@ -121,6 +123,27 @@ class Engine:
                 _lib.call("kls_gram_dcgs2", self.qptr, self.ld, self.ml, j, w.data_ptr(),
                           aw.data_ptr(), out, self.ws, self.wsb, self.st)
         return self._finish(2 * j + 3)
+
+    def _gram_dcgs2_fused(self, j, w, aw):
+        """N > 1: Gram + one-shot NVLink allreduce in one kernel; the global
+        sum lands in the mapped result buffer."""
+        link = self.peer
+        link.ar_epoch += 1
+        args = ("kls_gram_dcgs2_peer", self.qptr, self.ld, self.ml, j, w.data_ptr(), aw.data_ptr(),
+                self.res_dev, self.ws, self.wsb, link.ptrs, link.rank, link.world, link.CAP,
+                link.ar_epoch, link.err_dev, self.st)
+        rec = trace._active
+        if rec is None:
+            _lib.call(*args)
+        else:
+            rec.note("gram", 8 * self.ml * (j + 2))
+            with rec.span("gram"):
+                _lib.call(*args)
+        link.comm.allreduce_calls += 1
+        _lib.call("kls_stream_sync", self.st)
+        link.check()
+        runtime.XFER["d2h"] += 8 * (2 * j + 3)
+        return self.res_np[: 2 * j + 3].copy()
 
     def project(self, k, x, xnorm=True):
         """Q(:,0:k)^T x (and x.x) over all ranks: k (+1) values."""

@@ -54,6 +54,8 @@ SIGNATURES = {
     "kls_build_mant5_csr": (ctypes.c_int, [i64, i64, i64, i64, f64, f64, c_dp, c_dp, c_dp, c_dp]),
     "kls_peer_allreduce": (ctypes.c_int, [c_dp, i32, c_dp, c_dp, i32, i32, i32, ctypes.c_uint64,
                                           c_dp, c_dp]),
+    "kls_gram_dcgs2_peer": (ctypes.c_int, [c_dp, i64, i64, i32, c_dp, c_dp, c_dp, c_dp, sz, c_dp,
+                                           i32, i32, i32, ctypes.c_uint64, c_dp, c_dp]),
     "kls_peer_signal": (ctypes.c_int, [c_dp, i32, i32, i32, ctypes.c_uint64, c_dp]),
     "kls_stencil7_peer": (ctypes.c_int, [c_dp, c_dp, c_dp, c_dp, i64, i64, i64, c_dp, i32,
                                          ctypes.c_uint64, c_dp, c_dp]),

@@ -22,57 +22,13 @@
 //   double slot[2][cap]
 // Every spin has a wall-clock timeout (globaltimer) so a missing peer turns
 // into an error code instead of a hung GPU.
+#include "peer.cuh"
 #include "stencil.cuh"
 
 namespace {
 
 using namespace kls;
-
-constexpr int kMaxPeers = 8;
-constexpr size_t kDataOff = 256;
-constexpr uint64_t kTimeoutNs = 20ull * 1000 * 1000 * 1000;
-
-struct Peers {
-  char* buf[kMaxPeers];  // symmetric buffer base of every rank (peer-mapped)
-  int rank;
-  int world;
-  int cap;  // doubles per slot
-};
-
-__device__ __forceinline__ uint64_t* ar_flags(char* b) { return reinterpret_cast<uint64_t*>(b); }
-__device__ __forceinline__ uint64_t* halo_flags(char* b) {
-  return reinterpret_cast<uint64_t*>(b) + kMaxPeers;
-}
-__device__ __forceinline__ double* slot(char* b, int cap, uint64_t epoch) {
-  return reinterpret_cast<double*>(b + kDataOff) + (epoch & 1) * static_cast<size_t>(cap);
-}
-
-__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
-  uint64_t v;
-  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-
-__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-
-__device__ __forceinline__ uint64_t now_ns() {
-  uint64_t t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-
-// spin until *flag >= epoch; false on timeout
-__device__ __forceinline__ bool wait_flag(const uint64_t* flag, uint64_t epoch) {
-  if (ld_acquire_sys(flag) >= epoch) return true;
-  const uint64_t t0 = now_ns();
-  while (ld_acquire_sys(flag) < epoch) {
-    if (now_ns() - t0 > kTimeoutNs) return false;
-    __nanosleep(64);
-  }
-  return true;
-}
+using namespace kls::peer;
 
 __global__ void __launch_bounds__(kThreads) peer_allreduce_kernel(const double* __restrict__ src,
                                                                   int nv, double* out, Peers p,

@@ -103,9 +103,10 @@ int launch_gram(GramParams p, size_t ws_bytes, cudaStream_t st) {
 // Output is column-major with (k + (bext != NULL)) rows and nx columns, then
 // one slot for x_last . x_last when xnorm != 0.  Mirrors kernels.mv_trans_mv
 // (kernels.py:44-60) for the block shapes the solvers use.
-KLS_API int kls_mv_trans_mv(const double* Q, int64_t ldq, int64_t m, int32_t k,
+static int mv_trans_mv_impl(const double* Q, int64_t ldq, int64_t m, int32_t k,
                             const double* bext, const double* x0, const double* x1, int32_t nx,
-                            int32_t xnorm, double* out, void* ws, size_t ws_bytes, void* stream) {
+                            int32_t xnorm, double* out, void* ws, size_t ws_bytes, void* stream,
+                            const peer::Peers* peers, uint64_t epoch, int* err) {
   if (m < 0 || k < 0 || (k > 0 && (Q == nullptr || ldq < m)) || x0 == nullptr || out == nullptr ||
       ws == nullptr || (nx != 1 && nx != 2) || (nx == 2 && x1 == nullptr))
     return fail(KLS_EINVAL, "mv_trans_mv: bad arguments (m=%lld k=%d nx=%d)", (long long)m, k, nx);
@@ -118,6 +119,8 @@ KLS_API int kls_mv_trans_mv(const double* Q, int64_t ldq, int64_t m, int32_t k,
   unsigned int* ticket = static_cast<unsigned int*>(ws);
   double* partials = reinterpret_cast<double*>(static_cast<char*>(ws) + kTicketBytes);
   const size_t pws = ws_bytes;
+  if (peers != nullptr && k > kPanel)
+    return fail(KLS_EINVAL, "mv_trans_mv: the fused peer exchange needs k <= %d", kPanel);
   // panels of <= kPanel columns; extras ride on the last panel
   int c0 = 0;
   do {
@@ -138,11 +141,22 @@ KLS_API int kls_mv_trans_mv(const double* Q, int64_t ldq, int64_t m, int32_t k,
     p.bext_row = k;
     p.partials = partials;
     p.ticket = ticket;
+    p.peers.world = 0;
+    p.epoch = epoch;
+    p.err = err;
+    if (peers != nullptr) p.peers = *peers;
     const int rc = nx == 1 ? launch_gram<1>(p, pws, st) : launch_gram<2>(p, pws, st);
     if (rc) return rc;
     c0 += kp;
   } while (c0 < k);
   return KLS_OK;
+}
+
+KLS_API int kls_mv_trans_mv(const double* Q, int64_t ldq, int64_t m, int32_t k,
+                            const double* bext, const double* x0, const double* x1, int32_t nx,
+                            int32_t xnorm, double* out, void* ws, size_t ws_bytes, void* stream) {
+  return mv_trans_mv_impl(Q, ldq, m, k, bext, x0, x1, nx, xnorm, out, ws, ws_bytes, stream,
+                          nullptr, 0, nullptr);
 }
 
 // The DCGS2 Arnoldi step reduction (arnoldi.py:362-370 plus the guard norm of
@@ -152,6 +166,26 @@ KLS_API int kls_gram_dcgs2(const double* Q, int64_t ldq, int64_t m, int32_t j, c
                            const double* aw, double* out, void* ws, size_t ws_bytes,
                            void* stream) {
   return kls_mv_trans_mv(Q, ldq, m, j, w, w, aw, 2, 1, out, ws, ws_bytes, stream);
+}
+
+// kls_gram_dcgs2 fused with the step's global reduction: the kernel's last
+// CTA exchanges the local 2j+3 sums with every rank over NVLink peer memory
+// (symmetric buffers bufs[0..world), as kls_peer_allreduce) and writes the
+// rank-ordered global sum to out — compute and collective in one launch.
+KLS_API int kls_gram_dcgs2_peer(const double* Q, int64_t ldq, int64_t m, int32_t j,
+                                const double* w, const double* aw, double* out, void* ws,
+                                size_t ws_bytes, void* const* bufs, int32_t rank, int32_t world,
+                                int32_t cap, uint64_t epoch, int* err, void* stream) {
+  if (bufs == nullptr || err == nullptr || world < 2 || world > peer::kMaxPeers || rank < 0 ||
+      rank >= world || 2 * j + 3 > cap)
+    return fail(KLS_EINVAL, "gram_dcgs2_peer: bad peer arguments");
+  peer::Peers pr;
+  for (int r = 0; r < peer::kMaxPeers; ++r) pr.buf[r] = r < world ? static_cast<char*>(bufs[r]) : nullptr;
+  pr.rank = rank;
+  pr.world = world;
+  pr.cap = cap;
+  return mv_trans_mv_impl(Q, ldq, m, j, w, w, aw, 2, 1, out, ws, ws_bytes, stream, &pr, epoch,
+                          err);
 }
 
 // Workspace bytes that cover any reduction launch with up to kmax basis

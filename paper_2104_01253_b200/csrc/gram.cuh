@@ -2,6 +2,7 @@
 // streaming; gram_tma.cu: cp.async.bulk / mbarrier staged).
 #pragma once
 
+#include "peer.cuh"
 #include "reduce.cuh"
 
 namespace kls {
@@ -22,6 +23,12 @@ struct GramParams {
   int32_t bext_row;  // output row of bext
   double* partials;  // [gridDim.x][nv]
   unsigned int* ticket;
+  // fused one-shot allreduce over NVLink peers (peers.world > 1): the last
+  // CTA exchanges the CTA-summed vector with every rank and writes the
+  // rank-ordered global sum to `out`
+  peer::Peers peers;
+  uint64_t epoch;
+  int* err;
 };
 
 constexpr int kG = 4;  // Q columns reduced together
@@ -144,6 +151,13 @@ __device__ __forceinline__ void gram_epilogue(const GramParams& p, const double*
 
   // last CTA: fixed-order sum over CTAs (4 interleaved accumulators)
   const int nb = gridDim.x;
+  const bool fused = p.peers.world > 1;
+  double* mine = fused ? peer::slot(p.peers.buf[p.peers.rank], p.peers.cap, p.epoch) : nullptr;
+  auto dst_of = [&](int i) -> int64_t {
+    if (i < nq) return static_cast<int64_t>(i % NX) * p.out_ld + p.col0 + i / NX;
+    if (has_b && i < nq + NX) return static_cast<int64_t>(i - nq) * p.out_ld + p.bext_row;
+    return static_cast<int64_t>(NX) * p.out_ld;
+  };
   for (int i = threadIdx.x; i < nv; i += blockDim.x) {
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
     int b = 0;
@@ -155,17 +169,39 @@ __device__ __forceinline__ void gram_epilogue(const GramParams& p, const double*
     }
     for (; b < nb; ++b) a0 += __ldcg(p.partials + static_cast<int64_t>(b) * nv + i);
     const double s = (a0 + a1) + (a2 + a3);
-    int64_t dst;
-    if (i < nq) {
-      dst = static_cast<int64_t>(i % NX) * p.out_ld + p.col0 + i / NX;
-    } else if (has_b && i < nq + NX) {
-      dst = static_cast<int64_t>(i - nq) * p.out_ld + p.bext_row;
-    } else {
-      dst = static_cast<int64_t>(NX) * p.out_ld;
-    }
-    p.out[dst] = s;
+    if (fused)
+      mine[i] = s;
+    else
+      p.out[dst_of(i)] = s;
   }
   if (threadIdx.x == 0) *p.ticket = 0u;
+  if (!fused) return;
+  // one-shot exchange: publish, signal every peer, wait for every peer, then
+  // sum the N slots in rank order (identical bits on every rank)
+  __shared__ int s_ok;
+  if (threadIdx.x == 0) s_ok = 1;
+  __syncthreads();
+  if (threadIdx.x < p.peers.world) {
+    __threadfence_system();
+    peer::st_release_sys(peer::ar_flags(p.peers.buf[threadIdx.x]) + p.peers.rank, p.epoch);
+    if (!peer::wait_flag(peer::ar_flags(p.peers.buf[p.peers.rank]) + threadIdx.x, p.epoch))
+      atomicExch(&s_ok, 0);
+  }
+  __syncthreads();
+  if (!s_ok) {
+    if (threadIdx.x == 0) *p.err = 1;
+    for (int i = threadIdx.x; i < nv; i += blockDim.x)
+      p.out[dst_of(i)] = __longlong_as_double(0x7ff8000000000000ll);
+    return;
+  }
+  for (int i = threadIdx.x; i < nv; i += blockDim.x) {
+    double s = 0.0;
+    for (int r = 0; r < p.peers.world; ++r) {
+      const volatile double* v = peer::slot(p.peers.buf[r], p.peers.cap, p.epoch);
+      s += v[i];
+    }
+    p.out[dst_of(i)] = s;
+  }
 }
 
 template <int NX>
