@@ -86,6 +86,18 @@ int kls_dcgs2_update_host(double* Q, int64_t ldq, int64_t m, int32_t j, double* 
                           const double* aw, const double* coef_host, double alpha, int32_t divide,
                           void* stream);
 
+/* Device-side scalar step (arnoldi.py:379-400): from g = [c, beta, s, s_piv,
+ * aw.aw] (device) write coef = [c, s/alpha, t_piv, alpha] (device, 2j+2;
+ * qr != 0: the QR form of ortho.py:369) and copy g to gout (mapped host
+ * memory or NULL) — lets the update be queued one step ahead of the host. */
+int kls_dcgs2_scalars(const double* g, int32_t j, int32_t qr, double* coef, double* gout,
+                      void* stream);
+/* kls_dcgs2_update with coef_alpha = [c, t, alpha] on the device (from
+ * kls_dcgs2_scalars). */
+int kls_dcgs2_update_dev(double* Q, int64_t ldq, int64_t m, int32_t j, double* w,
+                         const double* aw, const double* coef_alpha, int32_t divide,
+                         void* stream);
+
 /* Y(:,0:l) <- scale*Y + sign*B(:,0:k) S — kernels.mv_times_mat_add_mv
  * (kernels.py:63-84) for l = 1 or 2; S is k x l column-major on the device.
  * nrm_out (optional, device) receives ||Y(:, l-1)||^2 of the result, fusing

@@ -50,11 +50,18 @@ class Engine:
         self.vbuf = torch.empty((capacity, self.ld), dtype=torch.float64, device=dev)
         self.qptr = self.vbuf.data_ptr()
         nres = 2 * capacity + 8
+        self.nres = nres
         self.stage = runtime.Staging(nres)
-        # pinned result buffer the reducing kernels write into directly
-        self.res_host = torch.zeros(nres, dtype=torch.float64, pin_memory=True)
-        self.res_np = self.res_host.numpy()
+        # pinned result buffer the reducing kernels write into directly; the
+        # second half is the other slot of the lookahead double buffer
+        self.res_host = torch.zeros(3 * nres, dtype=torch.float64, pin_memory=True)
+        self.res_np = self.res_host.numpy()[:nres]
         self.res_dev = _mapped(self.res_host.data_ptr())
+        self.slot_np = [self.res_host.numpy()[nres * (1 + s) : nres * (2 + s)] for s in (0, 1)]
+        self.slot_dev = [self.res_dev + 8 * nres * (1 + s) for s in (0, 1)]
+        self.gdev = torch.empty(nres, dtype=torch.float64, device=dev)
+        self.cdev = torch.empty(nres, dtype=torch.float64, device=dev)
+        self.slot_ev = [torch.cuda.Event(), torch.cuda.Event()]
         self.ws, self.wsb = runtime.workspace_for(self.st, capacity + 1)
         # N > 1: the per-step reduction goes over NVLink peer memory when
         # available (csrc/comm.cu), else through NCCL
@@ -144,6 +151,57 @@ class Engine:
         link.check()
         runtime.XFER["d2h"] += 8 * (2 * j + 3)
         return self.res_np[: 2 * j + 3].copy()
+
+    # -- one-step lookahead --------------------------------------
+    def gram_ahead(self, j, w, aw, slot, qr=False):
+        """Queue Gram_j (+ the cross-rank reduction) and the device scalar
+        step; the reduced vector lands in mapped slot `slot`, the update
+        coefficients in self.cdev.  Nothing waits."""
+        count = 2 * j + 3
+        rec = trace._active
+        if rec is not None:
+            rec.note("gram", 8 * self.ml * (j + 2))
+        if self.peer is not None and j <= 1024 and count <= self.peer.CAP:
+            link = self.peer
+            link.ar_epoch += 1
+            link.comm.allreduce_calls += 1
+            args = ("kls_gram_dcgs2_peer", self.qptr, self.ld, self.ml, j, w.data_ptr(),
+                    aw.data_ptr(), self.gdev.data_ptr(), self.ws, self.wsb, link.ptrs, link.rank,
+                    link.world, link.CAP, link.ar_epoch, link.err_dev, self.st)
+        else:
+            args = ("kls_gram_dcgs2", self.qptr, self.ld, self.ml, j, w.data_ptr(), aw.data_ptr(),
+                    self.gdev.data_ptr(), self.ws, self.wsb, self.st)
+        if rec is not None and rec.events:
+            with rec.span("gram"):
+                _lib.call(*args)
+        else:
+            _lib.call(*args)
+        if self.world > 1 and self.peer is None:
+            self.comm.allreduce_(self.gdev[:count])
+        _lib.call("kls_dcgs2_scalars", self.gdev.data_ptr(), j, 1 if qr else 0,
+                  self.cdev.data_ptr(), self.slot_dev[slot], self.st)
+        self.slot_ev[slot].record()
+
+    def wait_slot(self, slot, count):
+        """Block until the queued Gram of `slot` has landed; its 2j+3 values."""
+        self.slot_ev[slot].synchronize()
+        if self.peer is not None:
+            self.peer.check()
+        runtime.XFER["d2h"] += 8 * count
+        return self.slot_np[slot][:count].copy()
+
+    def update_ahead(self, j, w, aw, divide):
+        """The fused update with the device-computed coefficients."""
+        rec = trace._active
+        if rec is not None:
+            rec.note("update", 8 * self.ml * (j + 4))
+        args = ("kls_dcgs2_update_dev", self.qptr, self.ld, self.ml, j, w.data_ptr(),
+                aw.data_ptr(), self.cdev.data_ptr(), 1 if divide else 0, self.st)
+        if rec is not None and rec.events:
+            with rec.span("update"):
+                _lib.call(*args)
+        else:
+            _lib.call(*args)
 
     def project(self, k, x, xnorm=True):
         """Q(:,0:k)^T x (and x.x) over all ranks: k (+1) values."""

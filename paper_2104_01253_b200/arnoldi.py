@@ -14,6 +14,8 @@ Other reference schemes are outside the hot path and
 raise UnknownSchemeError.
 """
 
+import os
+
 import numpy as np
 import torch
 
@@ -186,6 +188,11 @@ class _DelayedArnoldi(_BaseArnoldi):
         self._pending = False
         self._wscale = 0.0
         self._k = None
+        # one-step lookahead: (slot,) of a queued Gram of the
+        # current pending vector, or None
+        self._lookahead = os.environ.get("KLS_LOOKAHEAD", "1") != "0"
+        self._ahead = None
+        self._slot = 0
         if start is not None:
             self._w.local.copy_(op.take(start, "start vector"))
             nrm = float(np.sqrt(e.sqnorm(self._w.local)))  # local norm, not counted
@@ -234,6 +241,8 @@ class _DelayedArnoldi(_BaseArnoldi):
             return True
 
         j = self.nbasis
+        if self._lookahead:
+            return self._step_ahead(j)
         g = e.gram_dcgs2(j, self._w.local, self._aw)
         self._rec(_ledger.MV_TRANS_MV, 2 * m * (j + 1) * 2)
         res = dcgs2_host_step(g, j, m, self._wscale, self._k, self._h, self.ledger)
@@ -253,6 +262,52 @@ class _DelayedArnoldi(_BaseArnoldi):
         self._wscale = vscale
         return True
 
+    def _step_ahead(self, j):
+        """The same step with a one-step lookahead: the update (with
+        device-computed coefficients), the operator and the next Gram pass are
+        queued before the host looks at this step's scalars, so the GPU never
+        waits for the host.  The host then runs the reference's guards and H /
+        K bookkeeping on the same scalars; on a breakdown the speculative work
+        is discarded (it never touches finalized basis columns)."""
+        e = self.eng
+        m = self.m
+        w, aw = self._w, self._aw
+        if self._ahead is None:
+            e.gram_ahead(j, w.local, aw, self._slot)
+        slot = self._slot
+        # speculation: this step's update and operator, then the next Gram
+        e.update_ahead(j, w.local, aw, divide=True)
+        self.op.napply += 1
+        e.apply(w, aw)
+        nxt = None
+        if j + 2 < self.capacity:
+            nxt = 1 - slot
+            e.gram_ahead(j + 1, w.local, aw, nxt)
+        g = e.wait_slot(slot, 2 * j + 3)
+        self._rec(_ledger.MV_TRANS_MV, 2 * m * (j + 1) * 2)
+        try:
+            res = dcgs2_host_step(g, j, m, self._wscale, self._k, self._h, self.ledger)
+        except BreakdownError:
+            self._ahead = None
+            self.op.napply -= 1
+            raise
+        if j > 0:
+            self.hcols = j
+        if res is None:  # happy breakdown: drop the speculative column and apply
+            self._ahead = None
+            self.op.napply -= 1
+            self._pending = False
+            return self._mark_happy()
+        _, _, alpha, vscale, self._k = res
+        if self.start_norm is None:
+            self.start_norm = alpha
+        self.nbasis += 1
+        self._wscale = vscale
+        self._ahead = nxt
+        if nxt is not None:
+            self._slot = nxt
+        return True
+
     def _release_w(self):
         rel = getattr(self._w, "release", None)
         if rel is not None:
@@ -260,6 +315,7 @@ class _DelayedArnoldi(_BaseArnoldi):
 
     def _flush(self):
         """CGS2 pass on the pending vector (arnoldi.py:425-455): 2 reductions."""
+        self._ahead = None  # a queued lookahead Gram of the pending vector is moot
         if not self._pending:
             self._release_w()
             return

@@ -44,11 +44,12 @@ struct UpdParams {
   const double* coef;  // c[0:j], t[0:j+1]
   double alpha;
   int32_t divide;      // aw / alpha (Arnoldi) or aw as is (QR)
+  const double* alpha_dev;  // when set, alpha is read from device memory
 };
 
 template <int RP, bool CHECK>
 __device__ __forceinline__ void upd_chunk(const UpdParams& p, const double2* sct, double tj,
-                                          int64_t wbase, int lane) {
+                                          double alpha, int64_t wbase, int lane) {
   double2 ac[RP], at[RP];
 #pragma unroll
   for (int r = 0; r < RP; ++r) {
@@ -87,10 +88,10 @@ __device__ __forceinline__ void upd_chunk(const UpdParams& p, const double2* sct
     const double2 w = load_pair_rw<CHECK>(p.w, row, p.m);
     const double2 a = load_pair<CHECK>(p.aw, row, p.m);
     double2 qn, wn;
-    qn.x = (w.x - ac[r].x) / p.alpha;
-    qn.y = (w.y - ac[r].y) / p.alpha;
-    const double ax = p.divide ? a.x / p.alpha : a.x;
-    const double ay = p.divide ? a.y / p.alpha : a.y;
+    qn.x = (w.x - ac[r].x) / alpha;
+    qn.y = (w.y - ac[r].y) / alpha;
+    const double ax = p.divide ? a.x / alpha : a.x;
+    const double ay = p.divide ? a.y / alpha : a.y;
     wn.x = ax - fma(qn.x, tj, at[r].x);
     wn.y = ay - fma(qn.y, tj, at[r].y);
     store_pair<CHECK>(qout, row, p.m, qn);
@@ -107,6 +108,7 @@ __global__ void __launch_bounds__(kThreads, kUpdBlocksPerSm)
   for (int k = threadIdx.x; k < jpad; k += kThreads)
     sct[k] = k < p.j ? make_double2(coef[k], coef[p.j + k]) : make_double2(0.0, 0.0);
   const double tj = coef[2 * p.j];
+  const double alpha = p.alpha_dev != nullptr ? *p.alpha_dev : p.alpha;
   __syncthreads();
   constexpr int64_t WROWS = 64 * RP;
   constexpr int64_t CROWS = WROWS * kWarps;
@@ -117,9 +119,9 @@ __global__ void __launch_bounds__(kThreads, kUpdBlocksPerSm)
     const int64_t cbase = ch * CROWS;
     const int64_t wbase = cbase + warp * WROWS;
     if (cbase + CROWS <= p.m)
-      upd_chunk<RP, false>(p, sct, tj, wbase, lane);
+      upd_chunk<RP, false>(p, sct, tj, alpha, wbase, lane);
     else
-      upd_chunk<RP, true>(p, sct, tj, wbase, lane);
+      upd_chunk<RP, true>(p, sct, tj, alpha, wbase, lane);
   }
 }
 
@@ -151,6 +153,7 @@ __global__ void __launch_bounds__(kUThreads, 1)
   for (int k = threadIdx.x; k < jpad; k += blockDim.x)
     sct[k] = k < p.j ? make_double2(coef[k], coef[p.j + k]) : make_double2(0.0, 0.0);
   const double tj = coef[2 * p.j];
+  const double alpha = p.alpha_dev != nullptr ? *p.alpha_dev : p.alpha;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int ng = (p.j + kCols - 1) / kCols;
@@ -250,10 +253,10 @@ __global__ void __launch_bounds__(kUThreads, 1)
     for (int r = 0; r < RP; ++r) {
       const int64_t row = c * kUR + wrow + 64 * r + 2 * lane;
       double2 qn, wn;
-      qn.x = (wv[r].x - ac[r].x) / p.alpha;
-      qn.y = (wv[r].y - ac[r].y) / p.alpha;
-      const double ax = p.divide ? av[r].x / p.alpha : av[r].x;
-      const double ay = p.divide ? av[r].y / p.alpha : av[r].y;
+      qn.x = (wv[r].x - ac[r].x) / alpha;
+      qn.y = (wv[r].y - ac[r].y) / alpha;
+      const double ax = p.divide ? av[r].x / alpha : av[r].x;
+      const double ay = p.divide ? av[r].y / alpha : av[r].y;
       wn.x = ax - fma(qn.x, tj, at[r].x);
       wn.y = ay - fma(qn.y, tj, at[r].y);
       *reinterpret_cast<double2*>(qout + row) = qn;
@@ -261,7 +264,7 @@ __global__ void __launch_bounds__(kUThreads, 1)
     }
   }
   if (nfull * kUR < p.m && (nfull % gridDim.x) == blockIdx.x)
-    upd_chunk<RP, true>(p, sct, tj, nfull * kUR + wrow, lane);
+    upd_chunk<RP, true>(p, sct, tj, alpha, nfull * kUR + wrow, lane);
 }
 
 // ---------------------------------------------------------------------------
@@ -421,13 +424,14 @@ int launch_update(const UpdParams& p, const double* host_coef, cudaStream_t st) 
 }
 
 int update_common(double* Q, int64_t ldq, int64_t m, int32_t j, double* w, const double* aw,
-                  const double* coef, double alpha, int32_t divide, bool host, void* stream) {
+                  const double* coef, double alpha, int32_t divide, bool host, void* stream,
+                  const double* alpha_dev = nullptr) {
   if (Q == nullptr || w == nullptr || aw == nullptr || coef == nullptr || m < 0 || j < 0 ||
       ldq < m || (ldq & 1))
     return fail(KLS_EINVAL, "dcgs2_update: bad arguments");
   if (misaligned(Q) || misaligned(w) || misaligned(aw))
     return fail(KLS_EINVAL, "dcgs2_update: operands must be 16-byte aligned");
-  UpdParams p{Q, ldq, m, j, w, aw, host ? nullptr : coef, alpha, divide};
+  UpdParams p{Q, ldq, m, j, w, aw, host ? nullptr : coef, alpha, divide, alpha_dev};
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int nc = 2 * j + 1;
   if (!host) return launch_update<0>(p, nullptr, st);
@@ -501,6 +505,17 @@ KLS_API int kls_dcgs2_update_host(double* Q, int64_t ldq, int64_t m, int32_t j, 
                                   const double* aw, const double* coef_host, double alpha,
                                   int32_t divide, void* stream) {
   return update_common(Q, ldq, m, j, w, aw, coef_host, alpha, divide, true, stream);
+}
+
+// Same with everything on the device: coef = [c(0:j), t(0:j+1), alpha]
+// (2j+2 doubles, as written by kls_dcgs2_scalars), so the update can be
+// queued before the host has seen the step's scalars.
+KLS_API int kls_dcgs2_update_dev(double* Q, int64_t ldq, int64_t m, int32_t j, double* w,
+                                 const double* aw, const double* coef_alpha, int32_t divide,
+                                 void* stream) {
+  if (coef_alpha == nullptr) return fail(KLS_EINVAL, "dcgs2_update_dev: null coefficients");
+  return update_common(Q, ldq, m, j, w, aw, coef_alpha, 0.0, divide, false, stream,
+                       coef_alpha + 2 * j + 1);
 }
 
 // Y(:, 0:l) <- scale * Y + sign * B(:, 0:k) S  with S (k x l, column-major,
