@@ -325,6 +325,35 @@ def run_ours(args):
                "d2h_bytes_per_step": int(sum_over_ranks(d2h)),
                "path": "kls.arnoldi_expand(op, pinned host start) -> (V on device, H on host)"}
 
+    # ---- collective latency (2j+3 = 203 doubles, back to back) ----------------
+    coll = None
+    if world > 1:
+        coll = {}
+        n_ar, reps = 2 * args.n + 3, 200
+        src = torch.zeros(n_ar, dtype=torch.float64, device="cuda")
+        out = torch.zeros(n_ar, dtype=torch.float64, device="cuda")
+        link = runtime.peer_link(op.comm)
+        st = runtime.stream_handle()
+        for name in ("peer", "nccl"):
+            if name == "peer" and link is None:
+                continue
+            for rep in range(2):  # warm-up pass, timed pass
+                barrier()
+                torch.cuda.synchronize()
+                a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a0.record()
+                for _ in range(reps):
+                    if name == "peer":
+                        link.allreduce(src.data_ptr(), n_ar, out.data_ptr(), st)
+                    else:
+                        dist.all_reduce(src)
+                a1.record()
+                torch.cuda.synchronize()
+            coll[f"{name}_allreduce_us"] = max_over_ranks(a0.elapsed_time(a1) * 1e3 / reps)
+        coll["doubles"] = n_ar
+        coll["note"] = ("the step's reduction runs fused into K1 (kls_gram_dcgs2_peer); these are "
+                        "standalone back-to-back latencies of the same payload")
+
     # ---- roofline of the dominant kernel -------------------------------------
     peak, peak_src = measured_peak()
     kern = "gram" if gram_s >= upd_s else "update"
@@ -367,6 +396,7 @@ def run_ours(args):
         "phase_ms_per_iter": {"gram": 1e3 * gram_s / iters, "update": 1e3 * upd_s / iters,
                               "apply": 1e3 * app_s / iters},
         "allreduce_us_per_iter": 1e6 * ar_s / iters if world > 1 else 0.0,
+        "collective_latency": coll,
         "halo_us_per_iter": 1e6 * halo_s / iters if world > 1 else 0.0,
         "roofline": roofline,
         "e2e": e2e,
