@@ -17,6 +17,21 @@ from . import ledger as _ledger
 from .errors import DimensionError
 
 
+def _aligned_block(B):
+    """B itself when it is a column-major view the kernels accept (16-byte
+    aligned columns, even leading dimension), else a padded copy."""
+    m, k = B.shape
+    ok = B.stride(0) == 1 and (k <= 1 or B.stride(1) >= m)
+    if ok:
+        ld = B.stride(1) if k > 1 else max(m + (m & 1), 2)
+        ok = B.data_ptr() % 16 == 0 and (k <= 1 or ld % 2 == 0)
+    if ok:
+        return B
+    buf = torch.zeros((max(k, 1), runtime.pad_rows(m)), dtype=torch.float64, device=B.device)
+    buf[:k, :m].copy_(B.T)
+    return buf[:k, :m].T
+
+
 def _cols(B, name):
     """(pointer, ld, k) of a column-major (m, k) device view."""
     if not isinstance(B, torch.Tensor) or not B.is_cuda:
@@ -70,6 +85,8 @@ def mv_trans_mv(B, X, ledger=None, comm=None, m_global=None):
     the partial results share a single allreduce.
     """
     comm = comm or runtime.comm()
+    if isinstance(B, torch.Tensor) and B.dim() == 2 and B.is_cuda:
+        B = _aligned_block(B)
     bp, ldb, k, m = _cols(B, "B")
     Xv = X[:, None] if X.dim() == 1 else X
     if Xv.shape[0] != m:
@@ -80,8 +97,8 @@ def mv_trans_mv(B, X, ledger=None, comm=None, m_global=None):
     st = runtime.stream_handle()
     for c in range(0, l, 2):
         nx = min(2, l - c)
-        x0 = Xv[:, c].contiguous()
-        x1 = Xv[:, c + 1].contiguous() if nx == 2 else None
+        x0 = Xv[:, c].clone()  # fresh, aligned allocations
+        x1 = Xv[:, c + 1].clone() if nx == 2 else None
         _lib.call("kls_mv_trans_mv", bp, ldb, m, k, None, x0.data_ptr(),
                   None if x1 is None else x1.data_ptr(), nx, 0,
                   out[c * k :].data_ptr() if k else out.data_ptr(), ws, wsb, st)
@@ -95,8 +112,11 @@ def mv_trans_mv(B, X, ledger=None, comm=None, m_global=None):
 def mv_times_mat_add_mv(Y, B, S, sign=1.0, scale=1.0, ledger=None, comm=None, m_global=None):
     """Y <- scale*Y + sign*B@S in place (zero reductions); returns Y."""
     comm = comm or runtime.comm()
+    if isinstance(B, torch.Tensor) and B.dim() == 2 and B.is_cuda:
+        B = _aligned_block(B)
     bp, ldb, k, m = _cols(B, "B")
     Yv = Y[:, None] if Y.dim() == 1 else Y
+    Yw = _aligned_block(Yv) if Yv.is_cuda else Yv
     S = np.asarray(S, dtype=np.float64)
     if S.ndim == 1:
         S = S[:, None]
@@ -111,8 +131,10 @@ def mv_times_mat_add_mv(Y, B, S, sign=1.0, scale=1.0, ledger=None, comm=None, m_
     st = runtime.stream_handle()
     for c in range(0, l, 2):
         lc = min(2, l - c)
-        yp, ldy, _, _ = _cols(Yv[:, c : c + lc], "Y")
+        yp, ldy, _, _ = _cols(Yw[:, c : c + lc], "Y")
         sp = Sd[c * k :].data_ptr() if k else None
         _lib.call("kls_mv_times_mat_add_mv", yp, ldy, m, lc, bp if k else None, ldb, k, sp,
                   float(sign), float(scale), None, None, 0, st)
+    if Yw is not Yv:
+        Yv.copy_(Yw)
     return Y

@@ -278,3 +278,61 @@ def test_qr_hand_worked_pending_state(cuda):
     assert st._r[1, 1] == pytest.approx(5.0, rel=1e-15)
     assert np.allclose(host(st.q)[:, 1], [0.6, 0.8, 0.0], atol=1e-15)
     assert np.allclose(st._r, g["hand_R"], rtol=1e-15, atol=1e-15)
+
+
+def test_config3_full_size_properties(cuda):
+    """Config 3's operator at full size (m = 1.3e8, 12 steps): size-independent
+    properties — orthonormal basis, Arnoldi relation, reduction and apply
+    counts — and agreement of the one-step lookahead with the synchronous
+    step (identical host decisions, H within rounding)."""
+    import os
+
+    K = kls()
+    op = K.laplace3d(496, 512, 512)
+    g = torch.Generator(device="cuda")
+    g.manual_seed(1729)
+    start = torch.randn(op.n, dtype=torch.float64, device="cuda", generator=g)
+    led = K.SyncLedger()
+    V, H = K.arnoldi_expand(op, start, "dcgs2", steps=12, ledger=led)
+    assert V.shape == (op.n, 13) and H.shape == (13, 12)
+    assert K.loss_of_orthogonality(V) <= 1e-13
+    assert K.representation_error_arnoldi(op, V, H) <= 1e-14
+    assert led.reductions <= 14 and led.kernel_counts["MvTransMv"] == 13
+    del V
+    os.environ["KLS_LOOKAHEAD"] = "0"
+    try:
+        _, H0 = K.arnoldi_expand(op, start, "dcgs2", steps=12)
+    finally:
+        os.environ.pop("KLS_LOOKAHEAD")
+    assert np.max(np.abs(H - H0)) <= 1e-12 * np.max(np.abs(H0))
+
+
+def test_kernels_module_contract(cuda, rng):
+    """kernels.py (reference kernels.py:28-84): one reduction per
+    mv_trans_mv whatever its width, including an empty block; none for
+    mv_times_mat_add_mv; reference flop counts."""
+    from paper_2104_01253_b200 import kernels, ledger as L
+
+    m = 1001
+    B = torch.from_numpy(np.asfortranarray(rng.standard_normal((m, 5)))).cuda()
+    B = B.T.contiguous().T  # column-major view
+    X = torch.from_numpy(rng.standard_normal((m, 3))).cuda().T.contiguous().T
+    led = L.SyncLedger()
+    G = kernels.mv_trans_mv(B, X, ledger=led)
+    assert np.allclose(G, B.cpu().numpy().T @ X.cpu().numpy(), rtol=1e-12, atol=1e-12)
+    assert led.reductions == 1 and led.flops == 2 * m * 5 * 3
+    led = L.SyncLedger()
+    out = kernels.mv_trans_mv(B[:, :0], X[:, :1], ledger=led)
+    assert out.shape == (0, 1) and led.reductions == 1 and led.flops == 0
+    Y = X[:, :2].clone().T.contiguous().T
+    S = rng.standard_normal((5, 2))
+    want = Y.cpu().numpy() - B.cpu().numpy() @ S
+    led = L.SyncLedger()
+    kernels.mv_times_mat_add_mv(Y, B, S, sign=-1.0, ledger=led)
+    assert np.allclose(Y.cpu().numpy(), want, rtol=1e-12, atol=1e-12)
+    assert led.reductions == 0 and led.kernel_counts[L.MV_TIMES_MAT_ADD_MV] == 1
+    x = X[:, 0].contiguous()
+    led = L.SyncLedger()
+    assert kernels.norm2(x, ledger=led) == pytest.approx(float(np.linalg.norm(x.cpu().numpy())),
+                                                        rel=1e-13)
+    assert led.reductions == 1 and led.kernel_counts[L.MV_DOT] == 1
