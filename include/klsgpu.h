@@ -93,10 +93,11 @@ int kls_dcgs2_update_host(double* Q, int64_t ldq, int64_t m, int32_t j, double* 
 int kls_dcgs2_scalars(const double* g, int32_t j, int32_t qr, double* coef, double* gout,
                       void* stream);
 /* kls_dcgs2_update with coef_alpha = [c, t, alpha] on the device (from
- * kls_dcgs2_scalars). */
-int kls_dcgs2_update_dev(double* Q, int64_t ldq, int64_t m, int32_t j, double* w,
-                         const double* aw, const double* coef_alpha, int32_t divide,
-                         void* stream);
+ * kls_dcgs2_scalars), writing w' to w_out and leaving w intact (a
+ * speculative step can be discarded). */
+int kls_dcgs2_update_dev(double* Q, int64_t ldq, int64_t m, int32_t j, const double* w,
+                         double* w_out, const double* aw, const double* coef_alpha,
+                         int32_t divide, void* stream);
 
 /* Y(:,0:l) <- scale*Y + sign*B(:,0:k) S — kernels.mv_times_mat_add_mv
  * (kernels.py:63-84) for l = 1 or 2; S is k x l column-major on the device.

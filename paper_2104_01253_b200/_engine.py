@@ -190,13 +190,15 @@ class Engine:
         runtime.XFER["d2h"] += 8 * count
         return self.slot_np[slot][:count].copy()
 
-    def update_ahead(self, j, w, aw, divide):
-        """The fused update with the device-computed coefficients."""
+    def update_ahead(self, j, w, w_out, aw, divide):
+        """The fused update with the device-computed coefficients; w' goes
+        to w_out (w stays intact)."""
         rec = trace._active
         if rec is not None:
             rec.note("update", 8 * self.ml * (j + 4))
         args = ("kls_dcgs2_update_dev", self.qptr, self.ld, self.ml, j, w.data_ptr(),
-                aw.data_ptr(), self.cdev.data_ptr(), 1 if divide else 0, self.st)
+                w_out.data_ptr(), aw.data_ptr(), self.cdev.data_ptr(), 1 if divide else 0,
+                self.st)
         if rec is not None and rec.events:
             with rec.span("update"):
                 _lib.call(*args)

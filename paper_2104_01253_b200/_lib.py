@@ -30,7 +30,8 @@ SIGNATURES = {
     "kls_gram_dcgs2": (ctypes.c_int, [c_dp, i64, i64, i32, c_dp, c_dp, c_dp, c_dp, sz, c_dp]),
     "kls_dcgs2_update": (ctypes.c_int, [c_dp, i64, i64, i32, c_dp, c_dp, c_dp, f64, i32, c_dp]),
     "kls_dcgs2_scalars": (ctypes.c_int, [c_dp, i32, i32, c_dp, c_dp, c_dp]),
-    "kls_dcgs2_update_dev": (ctypes.c_int, [c_dp, i64, i64, i32, c_dp, c_dp, c_dp, i32, c_dp]),
+    "kls_dcgs2_update_dev": (ctypes.c_int, [c_dp, i64, i64, i32, c_dp, c_dp, c_dp, c_dp, i32,
+                                            c_dp]),
     "kls_dcgs2_update_host": (ctypes.c_int, [c_dp, i64, i64, i32, c_dp, c_dp, c_dp, f64, i32, c_dp]),
     "kls_mv_times_mat_add_mv": (
         ctypes.c_int,

@@ -193,6 +193,12 @@ class _DelayedArnoldi(_BaseArnoldi):
         self._lookahead = os.environ.get("KLS_LOOKAHEAD", "1") != "0"
         self._ahead = None
         self._slot = 0
+        # the lookahead writes the next pending vector and its image into a
+        # second pair of buffers, so a discarded step leaves w / aw intact
+        self._w2 = self._aw2 = None
+        if self._lookahead:
+            self._w2 = op.new_vector()
+            self._aw2 = torch.zeros(e.ld, dtype=torch.float64, device=e.vbuf.device)[: e.ml]
         if start is not None:
             self._w.local.copy_(op.take(start, "start vector"))
             nrm = float(np.sqrt(e.sqnorm(self._w.local)))  # local norm, not counted
@@ -225,6 +231,8 @@ class _DelayedArnoldi(_BaseArnoldi):
             j = self.nbasis
             if getattr(self._w, "leased", True) is False:  # released by a finalize
                 self._w = self.op.new_vector()
+                if self._w2 is not None:
+                    self._w2 = self.op.new_vector()
             w = self._w
             self.op.napply += 1
             e.apply(e.col(j - 1), w.local)
@@ -271,18 +279,19 @@ class _DelayedArnoldi(_BaseArnoldi):
         is discarded (it never touches finalized basis columns)."""
         e = self.eng
         m = self.m
-        w, aw = self._w, self._aw
+        w, aw, w2, aw2 = self._w, self._aw, self._w2, self._aw2
         if self._ahead is None:
             e.gram_ahead(j, w.local, aw, self._slot)
         slot = self._slot
-        # speculation: this step's update and operator, then the next Gram
-        e.update_ahead(j, w.local, aw, divide=True)
+        # speculation: this step's update and operator (into the spare
+        # buffers), then the next Gram
+        e.update_ahead(j, w.local, w2.local, aw, divide=True)
         self.op.napply += 1
-        e.apply(w, aw)
+        e.apply(w2, aw2)
         nxt = None
         if j + 2 < self.capacity:
             nxt = 1 - slot
-            e.gram_ahead(j + 1, w.local, aw, nxt)
+            e.gram_ahead(j + 1, w2.local, aw2, nxt)
         g = e.wait_slot(slot, 2 * j + 3)
         self._rec(_ledger.MV_TRANS_MV, 2 * m * (j + 1) * 2)
         try:
@@ -303,15 +312,18 @@ class _DelayedArnoldi(_BaseArnoldi):
             self.start_norm = alpha
         self.nbasis += 1
         self._wscale = vscale
+        self._w, self._w2 = w2, w
+        self._aw, self._aw2 = aw2, aw
         self._ahead = nxt
         if nxt is not None:
             self._slot = nxt
         return True
 
     def _release_w(self):
-        rel = getattr(self._w, "release", None)
-        if rel is not None:
-            rel()
+        for v in (self._w, self._w2):
+            rel = getattr(v, "release", None)
+            if rel is not None:
+                rel()
 
     def _flush(self):
         """CGS2 pass on the pending vector (arnoldi.py:425-455): 2 reductions."""

@@ -45,6 +45,7 @@ struct UpdParams {
   double alpha;
   int32_t divide;      // aw / alpha (Arnoldi) or aw as is (QR)
   const double* alpha_dev;  // when set, alpha is read from device memory
+  double* w_out;            // where w' goes (== w for the in-place update)
 };
 
 template <int RP, bool CHECK>
@@ -95,7 +96,7 @@ __device__ __forceinline__ void upd_chunk(const UpdParams& p, const double2* sct
     wn.x = ax - fma(qn.x, tj, at[r].x);
     wn.y = ay - fma(qn.y, tj, at[r].y);
     store_pair<CHECK>(qout, row, p.m, qn);
-    store_pair<CHECK>(p.w, row, p.m, wn);
+    store_pair<CHECK>(p.w_out, row, p.m, wn);
   }
 }
 
@@ -260,7 +261,7 @@ __global__ void __launch_bounds__(kUThreads, 1)
       wn.x = ax - fma(qn.x, tj, at[r].x);
       wn.y = ay - fma(qn.y, tj, at[r].y);
       *reinterpret_cast<double2*>(qout + row) = qn;
-      *reinterpret_cast<double2*>(p.w + row) = wn;
+      *reinterpret_cast<double2*>(p.w_out + row) = wn;
     }
   }
   if (nfull * kUR < p.m && (nfull % gridDim.x) == blockIdx.x)
@@ -425,13 +426,16 @@ int launch_update(const UpdParams& p, const double* host_coef, cudaStream_t st) 
 
 int update_common(double* Q, int64_t ldq, int64_t m, int32_t j, double* w, const double* aw,
                   const double* coef, double alpha, int32_t divide, bool host, void* stream,
-                  const double* alpha_dev = nullptr) {
+                  const double* alpha_dev = nullptr, double* w_out = nullptr) {
   if (Q == nullptr || w == nullptr || aw == nullptr || coef == nullptr || m < 0 || j < 0 ||
       ldq < m || (ldq & 1))
     return fail(KLS_EINVAL, "dcgs2_update: bad arguments");
   if (misaligned(Q) || misaligned(w) || misaligned(aw))
     return fail(KLS_EINVAL, "dcgs2_update: operands must be 16-byte aligned");
-  UpdParams p{Q, ldq, m, j, w, aw, host ? nullptr : coef, alpha, divide, alpha_dev};
+  if (w_out != nullptr && misaligned(w_out))
+    return fail(KLS_EINVAL, "dcgs2_update: w_out must be 16-byte aligned");
+  UpdParams p{Q, ldq, m, j, w, aw, host ? nullptr : coef, alpha, divide, alpha_dev,
+              w_out != nullptr ? w_out : w};
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int nc = 2 * j + 1;
   if (!host) return launch_update<0>(p, nullptr, st);
@@ -509,13 +513,15 @@ KLS_API int kls_dcgs2_update_host(double* Q, int64_t ldq, int64_t m, int32_t j, 
 
 // Same with everything on the device: coef = [c(0:j), t(0:j+1), alpha]
 // (2j+2 doubles, as written by kls_dcgs2_scalars), so the update can be
-// queued before the host has seen the step's scalars.
-KLS_API int kls_dcgs2_update_dev(double* Q, int64_t ldq, int64_t m, int32_t j, double* w,
-                                 const double* aw, const double* coef_alpha, int32_t divide,
-                                 void* stream) {
-  if (coef_alpha == nullptr) return fail(KLS_EINVAL, "dcgs2_update_dev: null coefficients");
-  return update_common(Q, ldq, m, j, w, aw, coef_alpha, 0.0, divide, false, stream,
-                       coef_alpha + 2 * j + 1);
+// queued before the host has seen the step's scalars.  w' goes to w_out
+// (w is left intact, so a speculative step can be discarded).
+KLS_API int kls_dcgs2_update_dev(double* Q, int64_t ldq, int64_t m, int32_t j, const double* w,
+                                 double* w_out, const double* aw, const double* coef_alpha,
+                                 int32_t divide, void* stream) {
+  if (coef_alpha == nullptr || w_out == nullptr)
+    return fail(KLS_EINVAL, "dcgs2_update_dev: null coefficients or output");
+  return update_common(Q, ldq, m, j, const_cast<double*>(w), aw, coef_alpha, 0.0, divide, false,
+                       stream, coef_alpha + 2 * j + 1, w_out);
 }
 
 // Y(:, 0:l) <- scale * Y + sign * B(:, 0:k) S  with S (k x l, column-major,

@@ -336,3 +336,35 @@ def test_kernels_module_contract(cuda, rng):
     assert kernels.norm2(x, ledger=led) == pytest.approx(float(np.linalg.norm(x.cpu().numpy())),
                                                         rel=1e-13)
     assert led.reductions == 1 and led.kernel_counts[L.MV_DOT] == 1
+
+
+@pytest.mark.parametrize("lookahead", ["0", "1"])
+def test_happy_breakdown_mid_run_matches_oracle(cuda, lookahead, monkeypatch):
+    """A start vector with 4 active eigencomponents hits a happy breakdown
+    mid-run: H, the zero-padded extended basis, napply and the reduction
+    count follow the reference with and without the one-step lookahead
+    (the speculative update is discarded)."""
+    monkeypatch.setenv("KLS_LOOKAHEAD", lookahead)
+    K = kls()
+    d = np.arange(1.0, 41.0)
+    start = np.zeros(40)
+    start[[2, 9, 17, 30]] = [1.0, -2.0, 0.5, 3.0]
+    op = K.DenseOperator(np.diag(d))
+    led = K.SyncLedger()
+    exp = K.arnoldi(op, start, "dcgs2", capacity=12, ledger=led)
+    steps = 0
+    while exp.step():
+        steps += 1
+    assert exp.happy
+    be = exp.basis_extended.cpu().numpy()
+    V, H = exp.finalize()
+    cnt = oracle.Counts()
+    ox = oracle.kls_oracle.Dcgs2Expansion(lambda x: d * x, start, 12, cnt)
+    while ox.step():
+        pass
+    Vr, Hr = ox.finalize()
+    assert H.shape == Hr.shape and np.max(np.abs(H - Hr)) <= 1e-12 * np.max(np.abs(Hr))
+    assert np.max(np.abs(V.cpu().numpy() - Vr)) <= 1e-12
+    assert op.napply == cnt.napply
+    assert led.reductions == cnt.reductions
+    assert np.all(be[:, -1] == 0.0)
