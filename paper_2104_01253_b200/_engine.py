@@ -211,9 +211,15 @@ class Engine:
         if n == 0:
             return np.zeros(0)
         out = self._out(n)
-        trace.note("project", 8 * self.ml * (k + 1))
-        _lib.call("kls_mv_trans_mv", self.qptr if k else None, self.ld, self.ml, k, None,
-                  x.data_ptr(), None, 1, 1 if xnorm else 0, out, self.ws, self.wsb, self.st)
+        args = ("kls_mv_trans_mv", self.qptr if k else None, self.ld, self.ml, k, None,
+                x.data_ptr(), None, 1, 1 if xnorm else 0, out, self.ws, self.wsb, self.st)
+        rec = trace._active
+        if rec is None:
+            _lib.call(*args)
+        else:
+            rec.note("project", 8 * self.ml * (k + 1))
+            with rec.span("project"):
+                _lib.call(*args)
         return self._finish(n)
 
     def sqnorm(self, x):
@@ -242,17 +248,23 @@ class Engine:
     def subtract_projection(self, y, k, coef, want_norm=False):
         """y <- y - Q(:,0:k) coef; optionally return ||y||^2 over all ranks."""
         nrm = self._out(1) if want_norm else None
-        trace.note("mtm", 8 * self.ml * (k + 2))
         if k <= _PACK:
             c = np.ascontiguousarray(coef, dtype=np.float64) if k else None
             runtime.XFER["h2d"] += 8 * k
-            _lib.call("kls_mv_times_mat_add_mv_host", y.data_ptr(), self.ld, self.ml, 1,
-                      self.qptr if k else None, self.ld, k, c.ctypes.data if k else None,
-                      -1.0, 1.0, nrm, self.ws, self.wsb, self.st)
+            args = ("kls_mv_times_mat_add_mv_host", y.data_ptr(), self.ld, self.ml, 1,
+                    self.qptr if k else None, self.ld, k, c.ctypes.data if k else None,
+                    -1.0, 1.0, nrm, self.ws, self.wsb, self.st)
         else:
             dev = self.stage.push(coef)
-            _lib.call("kls_mv_times_mat_add_mv", y.data_ptr(), self.ld, self.ml, 1, self.qptr,
-                      self.ld, k, dev.data_ptr(), -1.0, 1.0, nrm, self.ws, self.wsb, self.st)
+            args = ("kls_mv_times_mat_add_mv", y.data_ptr(), self.ld, self.ml, 1, self.qptr,
+                    self.ld, k, dev.data_ptr(), -1.0, 1.0, nrm, self.ws, self.wsb, self.st)
+        rec = trace._active
+        if rec is None:
+            _lib.call(*args)
+        else:
+            rec.note("mtm", 8 * self.ml * (k + 2))
+            with rec.span("mtm"):
+                _lib.call(*args)
         if want_norm:
             return float(self._finish(1)[0])
         return None
