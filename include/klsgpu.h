@@ -112,6 +112,16 @@ int kls_mv_times_mat_add_mv_host(double* Y, int64_t ldy, int64_t m, int32_t l, c
                                  double scale, double* nrm_out, void* ws, size_t ws_bytes,
                                  void* stream);
 
+/* CGS2 comparator, fused first update + second projection of
+ * Cgs2State.push (reference ortho.py:148-151, i.e. MvTimesMatAddMv followed
+ * by MvTransMv, kernels.py:40-84): v <- v - Q(:,0:k) s in place, then
+ * out[0:k] = Q^T v and, when xnorm != 0, out[k] = v.v.  The chunk's Q rows
+ * are re-read from L2, so the pair costs one HBM pass over Q.  1 <= k <= 2048;
+ * s is host memory (carried in the launch) when s_on_host != 0, else device. */
+int kls_project_gram(const double* Q, int64_t ldq, int64_t m, int32_t k, double* v,
+                     const double* s, int32_t s_on_host, int32_t xnorm, double* out, void* ws,
+                     size_t ws_bytes, void* stream);
+
 /* y = A x for CSR rows (int64 row pointer, int32 columns, fp64 values),
  * bit-identical to CsrMatrix.matvec (problems.py:127-136): products, then
  * numpy's reduceat/pairwise summation order per row. */

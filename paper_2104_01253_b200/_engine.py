@@ -269,6 +269,27 @@ class Engine:
             return float(self._finish(1)[0])
         return None
 
+    def subtract_and_project(self, y, k, coef):
+        """y <- y - Q(:,0:k) coef, then Q(:,0:k)^T y over all ranks: CGS2's
+        first update and second projection in one pass (kls_project_gram)."""
+        if k == 0:
+            return np.zeros(0)
+        if k > _PACK:
+            self.subtract_projection(y, k, coef)
+            return self.project(k, y, xnorm=False)
+        c = np.ascontiguousarray(coef, dtype=np.float64)
+        runtime.XFER["h2d"] += 8 * k
+        args = ("kls_project_gram", self.qptr, self.ld, self.ml, k, y.data_ptr(), c.ctypes.data,
+                1, 0, self._out(k), self.ws, self.wsb, self.st)
+        rec = trace._active
+        if rec is None:
+            _lib.call(*args)
+        else:
+            rec.note("project_gram", 8 * self.ml * (k + 2))
+            with rec.span("project_gram"):
+                _lib.call(*args)
+        return self._finish(k)
+
     def add_combination(self, y, x, k, coef):
         """y = x + Q(:, 0:k) coef (host coefficients ride in the launch)."""
         if y.data_ptr() != x.data_ptr():

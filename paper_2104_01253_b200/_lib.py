@@ -27,6 +27,7 @@ SIGNATURES = {
     "kls_host_device_ptr": (ctypes.c_int, [c_dp, ctypes.POINTER(ctypes.c_void_p)]),
     "kls_workspace_bytes": (sz, [i64, i32]),
     "kls_mv_trans_mv": (ctypes.c_int, [c_dp, i64, i64, i32, c_dp, c_dp, c_dp, i32, i32, c_dp, c_dp, sz, c_dp]),
+    "kls_project_gram": (ctypes.c_int, [c_dp, i64, i64, i32, c_dp, c_dp, i32, i32, c_dp, c_dp, sz, c_dp]),
     "kls_gram_dcgs2": (ctypes.c_int, [c_dp, i64, i64, i32, c_dp, c_dp, c_dp, c_dp, sz, c_dp]),
     "kls_dcgs2_update": (ctypes.c_int, [c_dp, i64, i64, i32, c_dp, c_dp, c_dp, f64, i32, c_dp]),
     "kls_dcgs2_scalars": (ctypes.c_int, [c_dp, i32, i32, c_dp, c_dp, c_dp]),

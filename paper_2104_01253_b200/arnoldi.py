@@ -403,9 +403,8 @@ class _ImmediateArnoldi(_BaseArnoldi):
             raise ValueError("non-finite column")
         scale = float(np.sqrt(scale2))
         self._rec(_ledger.MV_TRANS_MV, 2 * m * j)
-        e.subtract_projection(v, j, s)
+        c = e.subtract_and_project(v, j, s)  # one pass over Q for both
         self._rec(_ledger.MV_TIMES_MAT_ADD_MV, 2 * m * j)
-        c = e.project(j, v, xnorm=False) if j else np.zeros(0)
         self._rec(_ledger.MV_TRANS_MV, 2 * m * j)
         nrm2 = e.subtract_projection(v, j, c, want_norm=True)
         self._rec(_ledger.MV_TIMES_MAT_ADD_MV, 2 * m * j)

@@ -39,5 +39,6 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+
 }  // namespace tma
 }  // namespace kls

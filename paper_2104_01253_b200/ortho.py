@@ -142,9 +142,8 @@ class Cgs2State(QrState):
         self._check_finite(scale2)
         scale = float(np.sqrt(scale2))
         self.ledger.record(_ledger.MV_TRANS_MV, flops=2 * m * j)
-        e.subtract_projection(v, j, s)
+        c = e.subtract_and_project(v, j, s)  # one pass over Q for both
         self.ledger.record(_ledger.MV_TIMES_MAT_ADD_MV, flops=2 * m * j)
-        c = e.project(j, v, xnorm=False) if j else np.zeros(0)
         self.ledger.record(_ledger.MV_TRANS_MV, flops=2 * m * j)
         nrm2 = e.subtract_projection(v, j, c, want_norm=True)
         self.ledger.record(_ledger.MV_TIMES_MAT_ADD_MV, flops=2 * m * j)

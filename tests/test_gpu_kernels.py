@@ -133,6 +133,40 @@ def test_mv_times_mat_add_mv_with_fused_norm(cuda, rng, l, k):
     assert np.isclose(nrm.item(), want[:, -1] @ want[:, -1], rtol=1e-12)
 
 
+@pytest.mark.parametrize("m", [1, 7, 512, 5003, 200001])
+@pytest.mark.parametrize("k", [1, 3, 4, 9, 20, 40, 100, 130, 200, 256, 1500])
+@pytest.mark.parametrize("host", [0, 1])
+def test_project_gram_matches_numpy(cuda, rng, m, k, host):
+    """CGS2's fused w = v - Q s, c = Q^T w (+ w.w): reference ortho.py:149-151."""
+    if m * k > 5e7:
+        pytest.skip("size")
+    lib, rt = _lib()
+    Q = rng.standard_normal((m, k))
+    v = rng.standard_normal(m)
+    s = rng.standard_normal(k)
+    qb, ld = _colmajor(Q)
+    vd = torch.from_numpy(v.copy()).cuda()
+    out = torch.full((k + 1,), np.nan, dtype=torch.float64, device="cuda")
+    ws, wsb = rt.workspace(k + 1)
+    sd = torch.from_numpy(s).cuda()
+    sp = s.ctypes.data if host else sd.data_ptr()
+    lib.call("kls_project_gram", qb.data_ptr(), ld, m, k, vd.data_ptr(), sp, host, 1,
+             out.data_ptr(), ws, wsb, rt.stream_handle())
+    w = v - Q @ s
+    got_w = vd.cpu().numpy()
+    assert np.allclose(got_w, w, rtol=1e-13, atol=1e-12 * np.sqrt(k))
+    got = out.cpu().numpy()
+    want = np.concatenate([Q.T @ got_w, [got_w @ got_w]])
+    tol = np.concatenate([_dot_tol(Q, got_w[:, None]).ravel(), [1e-15 * m * (got_w @ got_w)]])
+    assert np.all(np.abs(got - want) <= tol + 1e-300)
+    # deterministic
+    vd2 = torch.from_numpy(v.copy()).cuda()
+    out2 = torch.empty_like(out)
+    lib.call("kls_project_gram", qb.data_ptr(), ld, m, k, vd2.data_ptr(), sp, host, 1,
+             out2.data_ptr(), ws, wsb, rt.stream_handle())
+    assert torch.equal(out, out2) and torch.equal(vd, vd2)
+
+
 def test_csr_spmv_bitwise_ragged(cuda):
     """Rows of 0..300 nonzeros: numpy's reduceat/pairwise order, bit for bit."""
     from paper_2104_01253_b200 import CsrMatrix, CsrOperator
