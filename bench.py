@@ -216,12 +216,15 @@ def measured_peak():
 def ncu_traffic(kernel):
     """dram bytes per launch of `kernel` from the committed ncu --set full
     summary (profiles/ncu_summary.json), with the launch's algorithmic bytes."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
-            d = json.load(f)
-        return d.get(kernel)
-    except Exception:
-        return None
+    for name in ("ncu_summary.json", "ncu_summary_cgs2.json"):
+        try:
+            with open(os.path.join(ROOT, "profiles", name)) as f:
+                d = json.load(f)
+        except Exception:
+            continue
+        if d.get(kernel):
+            return d[kernel]
+    return None
 
 
 def run_ours(args):

@@ -62,6 +62,7 @@ class Engine:
         self.gdev = torch.empty(nres, dtype=torch.float64, device=dev)
         self.cdev = torch.empty(nres, dtype=torch.float64, device=dev)
         self.slot_ev = [torch.cuda.Event(), torch.cuda.Event()]
+        self.tstream = torch.cuda.current_stream()  # the stream self.st names
         self.ws, self.wsb = runtime.workspace_for(self.st, capacity + 1)
         # N > 1: the per-step reduction goes over NVLink peer memory when
         # available (csrc/comm.cu), else through NCCL
@@ -180,7 +181,7 @@ class Engine:
             self.comm.allreduce_(self.gdev[:count])
         _lib.call("kls_dcgs2_scalars", self.gdev.data_ptr(), j, 1 if qr else 0,
                   self.cdev.data_ptr(), self.slot_dev[slot], self.st)
-        self.slot_ev[slot].record()
+        self.slot_ev[slot].record(self.tstream)
 
     def wait_slot(self, slot, count):
         """Block until the queued Gram of `slot` has landed; its 2j+3 values."""

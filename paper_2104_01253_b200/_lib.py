@@ -105,13 +105,18 @@ def load():
     return _lib
 
 
+_fns = {}
+
+
 def call(name, *args):
     """Invoke a status-returning entry point; raise KlsGpuError on failure."""
     global _launches
-    lib = load()
-    rc = getattr(lib, name)(*args)
+    fn = _fns.get(name)
+    if fn is None:
+        fn = _fns[name] = getattr(load(), name)
+    rc = fn(*args)
     if rc != 0:
-        msg = lib.kls_last_error().decode(errors="replace")
+        msg = load().kls_last_error().decode(errors="replace")
         raise KlsGpuError(f"{name} failed ({rc}): {msg}")
     if name not in _NO_LAUNCH:
         _launches += 1

@@ -63,7 +63,9 @@ def dcgs2_host_step(g, j, m, wscale, k_prev, h, ledger):
     ledger.record(_ledger.MV_TIMES_MAT_ADD_MV, flops=2 * m * j)  # u = w - Q c
     t_piv = (s_piv - float(c @ s)) / (alpha * alpha)
     ledger.add_flops(2 * j)
-    t_full = np.append(s / alpha, t_piv)
+    t_full = np.empty(j + 1)
+    np.divide(s, alpha, out=t_full[:j])
+    t_full[j] = t_piv
     if j > 0:
         h[:j, j - 1] = k_prev + c
         h[j, j - 1] = alpha

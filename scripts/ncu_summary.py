@@ -72,10 +72,11 @@ def main():
     summary = {"launch_list": launches(a.launches)}
     if a.report:
         kern = full(a.report)
-        algo = {"gram": 8 * a.m * (a.j + 2), "update": 8 * a.m * (a.j + 4), "stencil7": 16 * a.m}
+        algo = {"project_gram": 8 * a.m * (a.j + 2), "gram": 8 * a.m * (a.j + 2),
+                "update": 8 * a.m * (a.j + 4), "stencil7": 16 * a.m, "mtm": 8 * a.m * (a.j + 2)}
 
         def family(name):
-            for key in ("gram", "update", "stencil7"):
+            for key in ("project_gram", "gram", "update", "stencil7", "mtm"):
                 if key in name:
                     return key
             return None
@@ -91,7 +92,7 @@ def main():
         summary["ncu_full"] = kern
         summary["capture"] = {"m": a.m, "j": a.j}
         # per-kernel traffic entries bench.py reads
-        for key in ("gram", "update", "stencil7"):
+        for key in ("project_gram", "gram", "update", "stencil7", "mtm"):
             for d in kern:
                 if d["family"] == key:
                     summary[key] = {"dram_bytes": d["dram_bytes"], "j": a.j,
