@@ -178,6 +178,83 @@ __global__ void __launch_bounds__(kThreads) ell_spmv_kernel(const int32_t* __res
   }
 }
 
+// Software-pipelined ELL product (default): while a thread gathers x for
+// row i it already has the ELL entries of its next row in flight, so the
+// streaming loads (HBM) overlap the gathers (mostly L1/L2).  The entry
+// streams bypass L1 (they are used once) to leave it to the x gathers.
+// Same arithmetic, same order as ell_spmv_kernel: bit-identical.
+__device__ __forceinline__ int32_t ld_na_s32(const int32_t* p) {
+  int32_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double ld_na_f64(const double* p) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ int ld_na_u8(const uint8_t* p) {
+  uint16_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.u8 %0, [%1];" : "=h"(v) : "l"(p));
+  return static_cast<int>(v);
+}
+
+#ifndef KLS_ELL_BLOCKS
+#define KLS_ELL_BLOCKS 4
+#endif
+constexpr int kEllBlocks = KLS_ELL_BLOCKS;
+
+template <int W>
+struct EllRow {
+  int n;
+  int32_t c[W];
+  double v[W];
+};
+
+template <int W>
+__device__ __forceinline__ void ell_fetch(EllRow<W>& r, const int32_t* ecol, const double* eval,
+                                          const uint8_t* elen, int64_t ld, int64_t i) {
+  r.n = ld_na_u8(elen + i);
+#pragma unroll
+  for (int k = 0; k < W; ++k) {
+    r.c[k] = k < r.n ? ld_na_s32(ecol + k * ld + i) : 0;
+    r.v[k] = k < r.n ? ld_na_f64(eval + k * ld + i) : 0.0;
+  }
+}
+
+template <int W>
+__global__ void __launch_bounds__(kThreads, kEllBlocks) ell_spmv_pipe_kernel(
+    const int32_t* __restrict__ ecol, const double* __restrict__ eval,
+    const uint8_t* __restrict__ elen, int64_t nrows, int64_t ld, const double* __restrict__ x,
+    double* __restrict__ y) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= nrows) return;
+  EllRow<W> cur;
+  ell_fetch<W>(cur, ecol, eval, elen, ld, i);
+  while (true) {
+    const int64_t nx = i + stride;
+    EllRow<W> nxt;
+    nxt.n = 0;
+    if (nx < nrows) ell_fetch<W>(nxt, ecol, eval, elen, ld, nx);
+    double p[W];
+#pragma unroll
+    for (int k = 0; k < W; ++k) p[k] = k < cur.n ? __dmul_rn(cur.v[k], __ldg(x + cur.c[k])) : 0.0;
+    double acc = 0.0;
+    if (cur.n > 0) {
+      double r = -0.0;
+#pragma unroll
+      for (int k = 1; k < W; ++k)
+        if (k < cur.n) r = __dadd_rn(r, p[k]);
+      acc = __dadd_rn(p[0], r);
+    }
+    y[i] = acc;
+    if (nx >= nrows) break;
+    cur = nxt;
+    i = nx;
+  }
+}
+
 __global__ void __launch_bounds__(kTileZ * kTileY) stencil7_kernel(
     const double* __restrict__ x, const double* __restrict__ x_lo, const double* __restrict__ x_hi,
     double* __restrict__ y, int64_t nx, int32_t ny, int32_t nz, int32_t xchunk) {
@@ -314,12 +391,27 @@ KLS_API int kls_ell_spmv(const int32_t* ecol, const double* eval, const uint8_t*
     return fail(KLS_EINVAL, "ell_spmv: bad arguments");
   if (nrows == 0) return KLS_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const int grid = grid_1d(nrows, 8);
+  static const bool plain = [] {
+    const char* e = getenv("KLS_ELL");
+    return e != nullptr && e[0] == 'p';
+  }();
+  if (plain) {
+    const int grid = grid_1d(nrows, 8);
+    if (width <= 4)
+      ell_spmv_kernel<4><<<grid, kThreads, 0, st>>>(ecol, eval, elen, nrows, ld, x, y);
+    else if (width <= 6)
+      ell_spmv_kernel<6><<<grid, kThreads, 0, st>>>(ecol, eval, elen, nrows, ld, x, y);
+    else
+      ell_spmv_kernel<8><<<grid, kThreads, 0, st>>>(ecol, eval, elen, nrows, ld, x, y);
+    return check_launch("ell_spmv_kernel");
+  }
+  // one wave of resident CTAs; each thread walks its rows with a one-row lookahead
+  const int grid = grid_1d(nrows, kEllBlocks);
   if (width <= 4)
-    ell_spmv_kernel<4><<<grid, kThreads, 0, st>>>(ecol, eval, elen, nrows, ld, x, y);
+    ell_spmv_pipe_kernel<4><<<grid, kThreads, 0, st>>>(ecol, eval, elen, nrows, ld, x, y);
   else if (width <= 6)
-    ell_spmv_kernel<6><<<grid, kThreads, 0, st>>>(ecol, eval, elen, nrows, ld, x, y);
+    ell_spmv_pipe_kernel<6><<<grid, kThreads, 0, st>>>(ecol, eval, elen, nrows, ld, x, y);
   else
-    ell_spmv_kernel<8><<<grid, kThreads, 0, st>>>(ecol, eval, elen, nrows, ld, x, y);
-  return check_launch("ell_spmv_kernel");
+    ell_spmv_pipe_kernel<8><<<grid, kThreads, 0, st>>>(ecol, eval, elen, nrows, ld, x, y);
+  return check_launch("ell_spmv_pipe_kernel");
 }
