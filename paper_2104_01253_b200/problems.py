@@ -296,6 +296,27 @@ class DenseOperator(LinearOperator):
         return self._fro
 
 
+class DeviceFunctionOperator(LinearOperator):
+    """A user operator given as a device function: ``fn(x)`` maps this rank's
+    rows of x (a float64 CUDA tensor) to this rank's rows of A x, with torch
+    ops or the caller's own kernels, on the current stream.  The counterpart
+    of subclassing the reference's LinearOperator with a numpy ``_matvec``
+    (problems.py:12-33): the vector never leaves the GPU.  With more than one
+    rank, ``fn`` sees only the local rows and does its own neighbour
+    exchange."""
+
+    def __init__(self, n, fn, comm=None):
+        super().__init__(n, comm)
+        self.fn = fn
+
+    def _launch(self, x, y, st):
+        out = self.fn(x.local)
+        if not isinstance(out, torch.Tensor) or out.shape != (self.m_local,) or not out.is_cuda:
+            raise DimensionError(
+                f"operator function must return a CUDA vector of length {self.m_local}")
+        y.copy_(out)
+
+
 # ---------------------------------------------------------------------------
 # CSR storage (host) and the device CSR operator
 

@@ -69,6 +69,7 @@ def config2(cpu, max_iters):
     for be in (True, False):
         cfg = kls.GmresConfig(max_iters=max_iters, restart=50, rtol=1e-6, scheme="dcgs2",
                               backward_errors=be)
+        kls.gmres_solve(op, b, cfg)  # warm-up (engine buffers, stream, caches)
         led = kls.SyncLedger()
         t, res = gtime(lambda: kls.gmres_solve(op, b, cfg, ledger=led))
         d = {"config": 2, "m": op.n, "restart": 50, "rtol": 1e-6, "backward_errors": be,

@@ -368,3 +368,22 @@ def test_happy_breakdown_mid_run_matches_oracle(cuda, lookahead, monkeypatch):
     assert op.napply == cnt.napply
     assert led.reductions == cnt.reductions
     assert np.all(be[:, -1] == 0.0)
+
+
+@pytest.mark.parametrize("scheme", ["dcgs2", "cgs2"])
+def test_device_function_operator(cuda, scheme):
+    """A user operator written as a device function (the counterpart of a
+    reference LinearOperator subclass with a numpy _matvec): a diagonal
+    plus shift, against the oracle with the same matvec in numpy."""
+    K = kls()
+    n = 4001
+    d = np.linspace(1.0, 3.0, n)
+    dd = torch.from_numpy(d).cuda()
+    op = K.DeviceFunctionOperator(n, lambda x: dd * x + 0.5 * torch.roll(x, 1))
+    start = np.random.Generator(np.random.PCG64(3)).standard_normal(n)
+    V, H = K.arnoldi_expand(op, start, scheme, steps=15)
+    _, Hr, _ = getattr(oracle, f"{scheme}_arnoldi")(lambda x: d * x + 0.5 * np.roll(x, 1), start, 15)
+    assert_h_close(H, Hr)
+    assert op.napply == (16 if scheme == "dcgs2" else 15)  # delayed: steps + 1
+    with pytest.raises(K.DimensionError):
+        K.DeviceFunctionOperator(n, lambda x: x[:-1]).apply(start)
