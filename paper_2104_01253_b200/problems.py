@@ -376,6 +376,26 @@ class CsrMatrix:
     def frobenius_norm(self):
         return float(np.linalg.norm(self.data))
 
+    def matvec(self, x):
+        """y = A x (problems.py:127-136) computed on the device by
+        kls_csr_spmv — bit-identical to the reference's reduceat order — and
+        returned as a host array, as the reference returns it."""
+        x = np.asarray(x, dtype=np.float64)
+        if x.shape != (self.ncols,):
+            raise DimensionError(f"operand of length {self.ncols} expected, got {x.shape}")
+        dev = runtime.device()
+        rp = torch.from_numpy(np.ascontiguousarray(self.indptr, dtype=np.int64)).to(dev)
+        ci = torch.from_numpy(np.ascontiguousarray(self.indices, dtype=np.int32)).to(dev)
+        va = torch.from_numpy(np.ascontiguousarray(self.data, dtype=np.float64)).to(dev)
+        xd = torch.zeros(max(self.ncols, 1), dtype=torch.float64, device=dev)
+        xd[: self.ncols] = torch.from_numpy(x).to(dev)
+        y = torch.empty(max(self.nrows, 1), dtype=torch.float64, device=dev)
+        if self.nrows:
+            _lib.call("kls_csr_spmv", rp.data_ptr(), ci.data_ptr() if self.nnz else None,
+                      va.data_ptr() if self.nnz else None, self.nrows, xd.data_ptr(),
+                      y.data_ptr(), runtime.stream_handle())
+        return y[: self.nrows].cpu().numpy()
+
 
 class CsrOperator(LinearOperator):
     """Device-resident CSR operator (problems.py:154-174).

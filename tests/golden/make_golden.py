@@ -256,8 +256,38 @@ def main():
         out[f"{name}_csv"] = np.array(buf.getvalue())
     out["kappa_matrix"] = kls.synthetic_kappa(60, 8, 1e6, seed=3)
     np.savez_compressed(os.path.join(OUT, "cli.npz"), **out)
+
+    mtx_corpus(kls)
     print("golden fixtures written to", OUT)
 
 
+def mtx_corpus(kls):
+    """The reference's Matrix Market corpus (pkg/tests/data/*.mtx) with its
+    parse results, for the host-side parser tests -> mtx_corpus.json."""
+    import glob
+    import json
+
+    data = os.path.join(os.path.dirname(REF), "tests", "data")
+    corpus = {}
+    for path in sorted(glob.glob(os.path.join(data, "*.mtx"))):
+        entry = {"text": open(path).read()}
+        try:
+            csr = kls.parse_matrix_market(path)
+            entry.update(ok=True, nrows=int(csr.nrows), ncols=int(csr.ncols),
+                         indptr=csr.indptr.tolist(), indices=csr.indices.tolist(),
+                         data=csr.data.tolist())
+        except kls.MatrixMarketError as err:
+            entry.update(ok=False, line=err.line)
+        corpus[os.path.basename(path)] = entry
+    with open(os.path.join(OUT, "mtx_corpus.json"), "w") as f:
+        json.dump(corpus, f, indent=1, sort_keys=True)
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["--only", "mtx"]:
+        sys.path.insert(0, REF)
+        import kls
+
+        mtx_corpus(kls)
+    else:
+        main()

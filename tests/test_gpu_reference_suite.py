@@ -765,3 +765,71 @@ def test_acceptance_10_eigen_count_agreement(cuda):
             res = K.krylov_schur_run(K.CsrOperator(csr), cfg, seed=ACC_SEED, exact=table)
             counts[scheme] = K.match_eigenvalues(res.values.real, table, 1e-7).n_matched
         assert abs(counts["cgs2"] - counts["dcgs2"]) <= 2, (restart, counts)
+
+
+# ---------------------------------------------------------------------------
+# test_problems.py (device products)
+
+
+def test_csr_matvec_matches_dense(cuda, rng):
+    """test_problems.py:47-57: CsrMatrix.matvec, now a device product"""
+    K = kls()
+    csr = K.CsrMatrix.from_coo(4, 4, [0, 1, 1, 3], [1, 0, 3, 2], [1.5, -2.0, 0.5, 4.0])
+    x = rng.standard_normal(4)
+    assert np.allclose(csr.matvec(x), csr.to_dense() @ x, atol=1e-15)
+    csr = K.CsrMatrix.from_coo(3, 3, [2], [0], [7.0])
+    assert csr.matvec(np.array([1.0, 2.0, 3.0])).tolist() == [0.0, 0.0, 7.0]
+    rect = K.CsrMatrix.from_coo(3, 5, [0, 2, 2], [4, 1, 3], [1.0, 2.0, 3.0])
+    x = rng.standard_normal(5)
+    assert np.allclose(rect.matvec(x), rect.to_dense() @ x, atol=1e-15)
+
+
+def test_laplace_stencil_cases(cuda, rng):
+    """test_problems.py:134-185"""
+    K = kls()
+    assert host(K.laplace3d(1, 1, 1).apply(np.array([1.0])))[0] == pytest.approx(6.0)
+    op = K.laplace3d(4, 4, 4)
+    a = op.to_csr()
+    for x in (np.ones(op.n), rng.standard_normal(op.n)):
+        assert np.allclose(host(op.apply(x)), a.matvec(x), atol=1e-13)
+    op = K.laplace3d(3, 4, 5)
+    for _ in range(3):
+        x, y = rng.standard_normal(op.n), rng.standard_normal(op.n)
+        assert abs(host(op.apply(x)) @ y - x @ host(op.apply(y))) <= 1e-13 * (
+            np.linalg.norm(x) * np.linalg.norm(y))
+    op = K.laplace3d(5, 4, 3)
+    assert op.frobenius_norm() == pytest.approx(np.linalg.norm(op.to_csr().to_dense()), rel=1e-14)
+    op = K.laplace3d(6, 6, 6)
+    exact = np.linalg.norm(op.to_csr().to_dense())
+    assert K.LinearOperator.frobenius_norm(op, samples=64, seed=1) == pytest.approx(exact, rel=0.25)
+    op = K.laplace3d(2, 2, 2)
+    op.apply(np.ones(8))
+    op.apply(np.ones(8))
+    assert op.napply == 2
+    with pytest.raises(K.DimensionError):
+        op.apply(np.ones(9))
+
+
+def test_square_operator_guard(cuda):
+    """test_problems.py:276-283"""
+    K = kls()
+    rect = K.CsrMatrix.from_coo(2, 3, [0, 1], [2, 0], [1.0, 2.0])
+    with pytest.raises(K.DimensionError):
+        K.CsrOperator(rect)
+    with pytest.raises(K.DimensionError):
+        K.DenseOperator(np.ones((2, 3)))
+
+
+def test_metric_device_paths(cuda, rng):
+    """test_metrics.py:61-77 on device bases"""
+    K = kls()
+    op = mant(6)
+    v, h = K.arnoldi_expand(op, rng.standard_normal(op.n), "cgs2", steps=12)
+    assert K.representation_error_arnoldi(op, v, h) <= 1e-14
+    h2 = h.copy()
+    h2[0, 0] += 1.0
+    assert K.representation_error_arnoldi(op, v, h2) == pytest.approx(
+        1.0 / np.linalg.norm(op.to_dense()), rel=1e-6)
+    v, h = K.arnoldi_expand(op, rng.standard_normal(op.n), "dcgs2", steps=15)
+    a1 = K.representation_error_arnoldi(op, v, h)
+    assert a1 == pytest.approx(K.representation_error_arnoldi(op, v.clone(), h.copy()), abs=1e-15)
