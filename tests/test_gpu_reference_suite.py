@@ -833,3 +833,16 @@ def test_metric_device_paths(cuda, rng):
     v, h = K.arnoldi_expand(op, rng.standard_normal(op.n), "dcgs2", steps=15)
     a1 = K.representation_error_arnoldi(op, v, h)
     assert a1 == pytest.approx(K.representation_error_arnoldi(op, v.clone(), h.copy()), abs=1e-15)
+
+
+def test_flop_lead_coefficients_at_scale(cuda):
+    """test_ledger.py:120-134 for the device schemes (m = 1e5, n = 100)"""
+    K = kls()
+    m, n = 100_000, 100
+    a = np.random.Generator(np.random.PCG64(8)).standard_normal((m, n))
+    for scheme in SCHEMES:
+        led = K.SyncLedger()
+        K.qr_factorize(a, scheme, ledger=led)
+        lead = led.flops / (m * n * n)
+        expect = K.predicted_counts(scheme, n).flop_lead
+        assert abs(lead - expect) <= 0.1 * expect, (scheme, lead, expect)
