@@ -10,6 +10,8 @@ kls_dcgs2_update in its QR form (w' = a - Q s_full, no 1/alpha);
 Q lives on the device; R and the scalar bookkeeping on the host.
 """
 
+import os
+
 import numpy as np
 import torch
 
@@ -65,12 +67,18 @@ class QrState:
     def r(self):
         return self._r[: self.npushed, : self.npushed]
 
-    def _take(self, a):
-        """Copy column a into device scratch; returns its global ||a||^2."""
+    def _take(self, a, readonly=False):
+        """Column a on the device: a CUDA float64 column is used in place when
+        the caller only reads it (readonly), else copied into scratch."""
         e = self.eng
         if isinstance(a, torch.Tensor) and a.is_cuda:
             if a.dim() != 1 or a.numel() != e.ml:
                 raise DimensionError(f"column of local length {e.ml} expected, got {tuple(a.shape)}")
+            if self.npushed >= self.n_cap:
+                raise DimensionError("state capacity exhausted")
+            if (readonly and a.dtype == torch.float64 and a.is_contiguous()
+                    and a.data_ptr() % 16 == 0 and a.device == e.vbuf.device):
+                return a  # read in place: the kernels never write the pushed column
             self._a.copy_(a)
         else:
             a = np.asarray(a, dtype=np.float64)
@@ -168,11 +176,18 @@ class Dcgs2State(QrState):
         self._s = None  # first-projection coefficients of the pending column
         self._wscale = 0.0
         self._pending = False
+        # the update is queued with device-computed coefficients before the
+        # host has checked the step (as _DelayedArnoldi._step_ahead); w' goes
+        # to a spare buffer so a breakdown leaves the pending column intact
+        self._lookahead = os.environ.get("KLS_LOOKAHEAD", "1") != "0"
+        self._w2 = (torch.zeros(e.ld, dtype=torch.float64, device=e.vbuf.device)[: e.ml]
+                    if self._lookahead else None)
+        self._slot = 0
 
     def push(self, a):
         e = self.eng
         m = self.m
-        x = self._take(a)
+        x = self._take(a, readonly=True)
         if not self._pending:
             nrm2 = e.sqnorm(x)  # local norm of the column, not counted
             self._check_finite(nrm2)
@@ -184,7 +199,14 @@ class Dcgs2State(QrState):
             return
         j = self.ncols
         # [Q, w]^T [w, a] plus a.a (the next pending column's local scale)
-        g = e.gram_dcgs2(j, self._w, x)
+        if self._lookahead:
+            slot = self._slot
+            self._slot = 1 - slot
+            e.gram_ahead(j, self._w, x, slot, qr=True)
+            e.update_ahead(j, self._w, self._w2, x, divide=False)
+            g = e.wait_slot(slot, 2 * j + 3)
+        else:
+            g = e.gram_dcgs2(j, self._w, x)
         self._check_finite(g[2 * j + 2])
         self.ledger.record(_ledger.MV_TRANS_MV, flops=2 * m * (j + 1) * 2)
         c = g[:j].copy()
@@ -208,7 +230,10 @@ class Dcgs2State(QrState):
         s_full = np.append(s_new, s_piv)
         self.ledger.record(_ledger.MV_TIMES_MAT_ADD_MV, flops=2 * m * (j + 1))
         # one pass: Q(:, j) = (w - Q c)/alpha ; w = a - Q s_new - q_j s_piv
-        e.dcgs2_update(j, self._w, x, c, s_full, alpha, divide=False)
+        if self._lookahead:  # already queued; adopt its w'
+            self._w, self._w2 = self._w2, self._w
+        else:
+            e.dcgs2_update(j, self._w, x, c, s_full, alpha, divide=False)
         self._emit_host(self._s + c, alpha)
         self._s = s_full
         self._wscale = float(np.sqrt(g[2 * j + 2]))
