@@ -1,5 +1,5 @@
 import cProfile, io, json, os, pstats, sys, time
-import numpy as np, torch
+import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2104_01253_b200 as kls
 k = int(sys.argv[1]) if len(sys.argv) > 1 else 3163

@@ -44,7 +44,6 @@ def _worker(rank, world, port, k, steps, out):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from paper_2104_01253_b200.arnoldi import dcgs2_host_step
-        from paper_2104_01253_b200.errors import BreakdownError  # noqa: F401
         from paper_2104_01253_b200.ledger import MV_TRANS_MV, SyncLedger
         from paper_2104_01253_b200.problems import ManteuffelSpec, halo_plan, manteuffel_build
         from paper_2104_01253_b200.runtime import block_range
