@@ -185,6 +185,18 @@ int kls_build_mant5_csr(int64_t k, int64_t row_lo, int64_t nrows, int64_t col_ba
  * this GPU.  All spins time out after 20 s and set *err instead of hanging. */
 size_t kls_peer_buffer_bytes(int32_t cap);
 
+/* Peer buffers for hosts without a collective allocator (the reference's
+ * mpi4py-style SPMD launch; SURVEY.md §8b kls_comm_init): allocate and zero
+ * this rank's buffer and get its IPC handle (kls_ipc_handle_bytes() bytes),
+ * exchange handles over the caller's bootstrap, open every peer's handle,
+ * and pass the resulting pointer table as `bufs` below (own rank: its own
+ * buffer).  Close peers and free the own buffer when done. */
+size_t kls_ipc_handle_bytes(void);
+int kls_peer_buffer_alloc(size_t bytes, void** buf, void* handle);
+int kls_peer_buffer_open(const void* handle, void** peer_buf);
+int kls_peer_buffer_close(void* peer_buf);
+int kls_peer_buffer_free(void* buf);
+
 /* The DCGS2 step's single global reduction (ledger site
  * kernels.py:57-59) as a one-shot NVLink exchange: sum over ranks of nv
  * doubles at src, accumulated in rank order (bitwise identical on all ranks),

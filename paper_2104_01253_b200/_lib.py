@@ -28,6 +28,11 @@ SIGNATURES = {
     "kls_workspace_bytes": (sz, [i64, i32]),
     "kls_mv_trans_mv": (ctypes.c_int, [c_dp, i64, i64, i32, c_dp, c_dp, c_dp, i32, i32, c_dp, c_dp, sz, c_dp]),
     "kls_project_gram": (ctypes.c_int, [c_dp, i64, i64, i32, c_dp, c_dp, i32, i32, c_dp, c_dp, sz, c_dp]),
+    "kls_ipc_handle_bytes": (sz, []),
+    "kls_peer_buffer_alloc": (ctypes.c_int, [sz, ctypes.POINTER(ctypes.c_void_p), c_dp]),
+    "kls_peer_buffer_open": (ctypes.c_int, [c_dp, ctypes.POINTER(ctypes.c_void_p)]),
+    "kls_peer_buffer_close": (ctypes.c_int, [c_dp]),
+    "kls_peer_buffer_free": (ctypes.c_int, [c_dp]),
     "kls_gram_dcgs2": (ctypes.c_int, [c_dp, i64, i64, i32, c_dp, c_dp, c_dp, c_dp, sz, c_dp]),
     "kls_dcgs2_update": (ctypes.c_int, [c_dp, i64, i64, i32, c_dp, c_dp, c_dp, f64, i32, c_dp]),
     "kls_dcgs2_scalars": (ctypes.c_int, [c_dp, i32, i32, c_dp, c_dp, c_dp]),
@@ -68,7 +73,9 @@ SIGNATURES = {
 # entry points that launch no kernel (not counted as GPU launches)
 _NO_LAUNCH = frozenset({"kls_version", "kls_last_error", "kls_device_sm_count", "kls_stream_sync",
                         "kls_host_device_ptr", "kls_workspace_bytes", "kls_peer_buffer_bytes",
-                        "kls_lap7_nnz", "kls_mant5_nnz"})
+                        "kls_lap7_nnz", "kls_mant5_nnz", "kls_ipc_handle_bytes",
+                        "kls_peer_buffer_alloc", "kls_peer_buffer_open", "kls_peer_buffer_close",
+                        "kls_peer_buffer_free"})
 
 _lock = threading.Lock()
 _lib = None

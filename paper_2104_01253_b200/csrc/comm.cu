@@ -23,6 +23,8 @@
 // Every spin has a wall-clock timeout (globaltimer) so a missing peer turns
 // into an error code instead of a hung GPU.
 #include "peer.cuh"
+
+#include <cstring>
 #include "stencil.cuh"
 
 namespace {
@@ -108,6 +110,53 @@ int make_peers(Peers& p, void* const* bufs, int rank, int world, int cap) {
 }
 
 }  // namespace
+
+// ---- peer buffers for callers without a collective allocator --------------
+// (C / C++ hosts: one process per GPU, handles exchanged over the caller's
+// own bootstrap — MPI, a socket, NCCL's unique-id channel.)
+
+KLS_API size_t kls_ipc_handle_bytes(void) { return sizeof(cudaIpcMemHandle_t); }
+
+// Allocate and zero a peer buffer of `bytes` on the current device; writes
+// its IPC handle (kls_ipc_handle_bytes() bytes) to `handle`.
+KLS_API int kls_peer_buffer_alloc(size_t bytes, void** buf, void* handle) {
+  if (buf == nullptr || handle == nullptr || bytes == 0)
+    return fail(KLS_EINVAL, "peer_buffer_alloc: bad arguments");
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, bytes);
+  if (e == cudaSuccess) e = cudaMemset(p, 0, bytes);
+  cudaIpcMemHandle_t h;
+  if (e == cudaSuccess) e = cudaIpcGetMemHandle(&h, p);
+  if (e != cudaSuccess) {
+    if (p != nullptr) cudaFree(p);
+    return fail(KLS_ECUDA, "peer_buffer_alloc: %s", cudaGetErrorString(e));
+  }
+  std::memcpy(handle, &h, sizeof(h));
+  *buf = p;
+  return KLS_OK;
+}
+
+// Map another rank's peer buffer (from its handle) into this device.
+KLS_API int kls_peer_buffer_open(const void* handle, void** peer_buf) {
+  if (handle == nullptr || peer_buf == nullptr) return fail(KLS_EINVAL, "peer_buffer_open: bad arguments");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  cudaError_t e = cudaIpcOpenMemHandle(peer_buf, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) return fail(KLS_ECUDA, "peer_buffer_open: %s", cudaGetErrorString(e));
+  return KLS_OK;
+}
+
+KLS_API int kls_peer_buffer_close(void* peer_buf) {
+  cudaError_t e = cudaIpcCloseMemHandle(peer_buf);
+  if (e != cudaSuccess) return fail(KLS_ECUDA, "peer_buffer_close: %s", cudaGetErrorString(e));
+  return KLS_OK;
+}
+
+KLS_API int kls_peer_buffer_free(void* buf) {
+  cudaError_t e = cudaFree(buf);
+  if (e != cudaSuccess) return fail(KLS_ECUDA, "peer_buffer_free: %s", cudaGetErrorString(e));
+  return KLS_OK;
+}
 
 // Bytes of a symmetric peer buffer holding `cap` doubles per slot.
 KLS_API size_t kls_peer_buffer_bytes(int32_t cap) {

@@ -1,0 +1,111 @@
+"""Multi-GPU check of the C-ABI peer path without torch's symmetric memory:
+every rank allocates its peer buffer with kls_peer_buffer_alloc, the IPC
+handles are exchanged (here over torch.distributed objects; a C host would
+use MPI or a socket), peers are opened with kls_peer_buffer_open, and the
+one-shot allreduce (kls_peer_allreduce) and the fused Gram + allreduce
+(kls_gram_dcgs2_peer) run on that pointer table.  Rank 0 prints one JSON
+line; exit 1 on a mismatch.
+
+    torchrun --nproc-per-node N scripts/peer_capi_check.py
+"""
+
+import ctypes
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def main():
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist.init_process_group("gloo")
+    rank, world = dist.get_rank(), dist.get_world_size()
+    from paper_2104_01253_b200 import _lib, runtime
+
+    lib = _lib.load()
+    cap = 512
+    nbytes = lib.kls_peer_buffer_bytes(cap)
+    hbytes = lib.kls_ipc_handle_bytes()
+    handle = (ctypes.c_char * hbytes)()
+    mine = ctypes.c_void_p()
+    _lib.call("kls_peer_buffer_alloc", nbytes, ctypes.byref(mine), handle)
+    handles = [None] * world
+    dist.all_gather_object(handles, bytes(handle))
+    ptrs = []
+    for r in range(world):
+        if r == rank:
+            ptrs.append(mine.value)
+        else:
+            p = ctypes.c_void_p()
+            h = (ctypes.c_char * hbytes).from_buffer_copy(handles[r])
+            _lib.call("kls_peer_buffer_open", h, ctypes.byref(p))
+            ptrs.append(p.value)
+    table = (ctypes.c_void_p * world)(*ptrs)
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    st = runtime.stream_handle()
+    ok = True
+    res = {"world": world}
+
+    # one-shot allreduce, several epochs, rank-ordered sum bitwise on all ranks
+    for epoch in range(1, 6):
+        n = 37 * epoch
+        vals = [np.random.default_rng(1000 * epoch + r).standard_normal(n) for r in range(world)]
+        src = torch.from_numpy(vals[rank]).cuda()
+        out = torch.empty(n, dtype=torch.float64, device="cuda")
+        _lib.call("kls_peer_allreduce", src.data_ptr(), n, out.data_ptr(), table, rank, world, cap,
+                  epoch, err.data_ptr(), st)
+        torch.cuda.synchronize()
+        want = vals[0].copy()
+        for r in range(1, world):
+            want = want + vals[r]
+        ok = ok and np.array_equal(out.cpu().numpy(), want) and int(err.item()) == 0
+    res["allreduce_ok"] = ok
+
+    # fused Gram + allreduce over a row-sharded basis
+    m_local, j = 50_001, 9
+    g = np.random.default_rng(7)
+    Q = g.standard_normal((world * m_local, j))
+    w = g.standard_normal(world * m_local)
+    aw = g.standard_normal(world * m_local)
+    lo, hi = rank * m_local, (rank + 1) * m_local
+    ld = runtime.pad_rows(m_local)
+    qb = torch.zeros((j, ld), dtype=torch.float64, device="cuda")
+    qb[:, :m_local] = torch.from_numpy(np.ascontiguousarray(Q[lo:hi].T)).cuda()
+    wd = torch.from_numpy(w[lo:hi].copy()).cuda()
+    awd = torch.from_numpy(aw[lo:hi].copy()).cuda()
+    out = torch.empty(2 * j + 3, dtype=torch.float64, device="cuda")
+    ws, wsb = runtime.workspace(j + 2)
+    _lib.call("kls_gram_dcgs2_peer", qb.data_ptr(), ld, m_local, j, wd.data_ptr(), awd.data_ptr(),
+              out.data_ptr(), ws, wsb, table, rank, world, cap, 6, err.data_ptr(), st)
+    torch.cuda.synchronize()
+    left = np.hstack([Q, w[:, None]])
+    want = np.concatenate([left.T @ w, left.T @ aw, [aw @ aw]])
+    got = out.cpu().numpy()
+    allg = [None] * world
+    dist.all_gather_object(allg, got.tobytes())
+    same = all(a == allg[0] for a in allg)
+    close = np.allclose(got, want, rtol=1e-12, atol=1e-10)
+    res.update(gram_close=bool(close), gram_bitwise_across_ranks=same)
+    ok = ok and close and same and int(err.item()) == 0
+
+    dist.barrier()
+    for r in range(world):
+        if r != rank:
+            _lib.call("kls_peer_buffer_close", ctypes.c_void_p(ptrs[r]))
+    dist.barrier()
+    _lib.call("kls_peer_buffer_free", mine)
+    res["ok"] = bool(ok)
+    if rank == 0:
+        print(json.dumps(res), flush=True)
+    dist.destroy_process_group()
+    sys.exit(0 if ok else 1)
+
+
+if __name__ == "__main__":
+    main()
