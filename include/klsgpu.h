@@ -205,6 +205,14 @@ int kls_peer_buffer_free(void* buf);
 int kls_peer_allreduce(const double* src, int32_t nv, double* out, void* const* bufs, int32_t rank,
                        int32_t world, int32_t cap, uint64_t epoch, int* err, void* stream);
 
+/* kls_gram_dcgs2 with the step's device scalar arithmetic (kls_dcgs2_scalars)
+ * fused into the kernel's last CTA: out <- g (2j+3), coef <- [c, s/alpha
+ * (QR: s), t_piv, alpha] (2j+2), gout <- g (mapped host memory or NULL).
+ * j <= 1024.  One launch per step for arnoldi.py:362-400 / ortho.py:378-399. */
+int kls_gram_dcgs2_step(const double* Q, int64_t ldq, int64_t m, int32_t j, const double* w,
+                        const double* aw, double* out, double* coef, double* gout, int32_t qr,
+                        void* ws, size_t ws_bytes, void* stream);
+
 /* kls_gram_dcgs2 fused with the step's global reduction: the kernel's last
  * CTA performs the one-shot peer exchange itself and writes the rank-ordered
  * global sum of the 2j+3 scalars to out — compute and collective in one
@@ -213,6 +221,14 @@ int kls_gram_dcgs2_peer(const double* Q, int64_t ldq, int64_t m, int32_t j, cons
                         const double* aw, double* out, void* ws, size_t ws_bytes,
                         void* const* bufs, int32_t rank, int32_t world, int32_t cap,
                         uint64_t epoch, int* err, void* stream);
+
+/* kls_gram_dcgs2_step fused with the peer allreduce: Gram pass, the step's
+ * one global reduction and the scalar step in a single launch. */
+int kls_gram_dcgs2_peer_step(const double* Q, int64_t ldq, int64_t m, int32_t j,
+                             const double* w, const double* aw, double* out, double* coef,
+                             double* gout, int32_t qr, void* ws, size_t ws_bytes,
+                             void* const* bufs, int32_t rank, int32_t world, int32_t cap,
+                             uint64_t epoch, int* err, void* stream);
 
 /* Raise this rank's halo flag (= epoch) in the buffers of the ranks set in
  * target_mask, ordered after all prior work on the stream. */

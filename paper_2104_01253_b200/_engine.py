@@ -162,14 +162,22 @@ class Engine:
         rec = trace._active
         if rec is not None:
             rec.note("gram", 8 * self.ml * (j + 2))
+        fused = j <= 1024  # scalar step fused into the Gram kernel's last CTA
+        qflag = 1 if qr else 0
         if self.peer is not None and j <= 1024 and count <= self.peer.CAP:
             link = self.peer
             link.ar_epoch += 1
             link.comm.allreduce_calls += 1
-            args = ("kls_gram_dcgs2_peer", self.qptr, self.ld, self.ml, j, w.data_ptr(),
-                    aw.data_ptr(), self.gdev.data_ptr(), self.ws, self.wsb, link.ptrs, link.rank,
-                    link.world, link.CAP, link.ar_epoch, link.err_dev, self.st)
+            args = ("kls_gram_dcgs2_peer_step", self.qptr, self.ld, self.ml, j, w.data_ptr(),
+                    aw.data_ptr(), self.gdev.data_ptr(), self.cdev.data_ptr(), self.slot_dev[slot],
+                    qflag, self.ws, self.wsb, link.ptrs, link.rank, link.world, link.CAP,
+                    link.ar_epoch, link.err_dev, self.st)
+        elif self.world == 1 and fused:
+            args = ("kls_gram_dcgs2_step", self.qptr, self.ld, self.ml, j, w.data_ptr(),
+                    aw.data_ptr(), self.gdev.data_ptr(), self.cdev.data_ptr(), self.slot_dev[slot],
+                    qflag, self.ws, self.wsb, self.st)
         else:
+            fused = False
             args = ("kls_gram_dcgs2", self.qptr, self.ld, self.ml, j, w.data_ptr(), aw.data_ptr(),
                     self.gdev.data_ptr(), self.ws, self.wsb, self.st)
         if rec is not None and rec.events:
@@ -177,10 +185,11 @@ class Engine:
                 _lib.call(*args)
         else:
             _lib.call(*args)
-        if self.world > 1 and self.peer is None:
-            self.comm.allreduce_(self.gdev[:count])
-        _lib.call("kls_dcgs2_scalars", self.gdev.data_ptr(), j, 1 if qr else 0,
-                  self.cdev.data_ptr(), self.slot_dev[slot], self.st)
+        if not fused:
+            if self.world > 1 and self.peer is None:
+                self.comm.allreduce_(self.gdev[:count])
+            _lib.call("kls_dcgs2_scalars", self.gdev.data_ptr(), j, qflag, self.cdev.data_ptr(),
+                      self.slot_dev[slot], self.st)
         self.slot_ev[slot].record(self.tstream)
 
     def wait_slot(self, slot, count):

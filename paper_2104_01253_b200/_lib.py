@@ -33,6 +33,12 @@ SIGNATURES = {
     "kls_peer_buffer_open": (ctypes.c_int, [c_dp, ctypes.POINTER(ctypes.c_void_p)]),
     "kls_peer_buffer_close": (ctypes.c_int, [c_dp]),
     "kls_peer_buffer_free": (ctypes.c_int, [c_dp]),
+    "kls_gram_dcgs2_step": (ctypes.c_int, [c_dp, i64, i64, i32, c_dp, c_dp, c_dp, c_dp, c_dp, i32,
+                                           c_dp, sz, c_dp]),
+    "kls_gram_dcgs2_peer_step": (ctypes.c_int, [c_dp, i64, i64, i32, c_dp, c_dp, c_dp, c_dp, c_dp,
+                                                i32, c_dp, sz, c_dp, i32, i32, i32,
+                                                ctypes.c_uint64, c_dp,
+                                                c_dp]),
     "kls_gram_dcgs2": (ctypes.c_int, [c_dp, i64, i64, i32, c_dp, c_dp, c_dp, c_dp, sz, c_dp]),
     "kls_dcgs2_update": (ctypes.c_int, [c_dp, i64, i64, i32, c_dp, c_dp, c_dp, f64, i32, c_dp]),
     "kls_dcgs2_scalars": (ctypes.c_int, [c_dp, i32, i32, c_dp, c_dp, c_dp]),

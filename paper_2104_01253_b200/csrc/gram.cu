@@ -106,7 +106,8 @@ int launch_gram(GramParams p, size_t ws_bytes, cudaStream_t st) {
 static int mv_trans_mv_impl(const double* Q, int64_t ldq, int64_t m, int32_t k,
                             const double* bext, const double* x0, const double* x1, int32_t nx,
                             int32_t xnorm, double* out, void* ws, size_t ws_bytes, void* stream,
-                            const peer::Peers* peers, uint64_t epoch, int* err) {
+                            const peer::Peers* peers, uint64_t epoch, int* err,
+                            double* coef = nullptr, double* gout = nullptr, int32_t qr = 0) {
   if (m < 0 || k < 0 || (k > 0 && (Q == nullptr || ldq < m)) || x0 == nullptr || out == nullptr ||
       ws == nullptr || (nx != 1 && nx != 2) || (nx == 2 && x1 == nullptr))
     return fail(KLS_EINVAL, "mv_trans_mv: bad arguments (m=%lld k=%d nx=%d)", (long long)m, k, nx);
@@ -121,6 +122,8 @@ static int mv_trans_mv_impl(const double* Q, int64_t ldq, int64_t m, int32_t k,
   const size_t pws = ws_bytes;
   if (peers != nullptr && k > kPanel)
     return fail(KLS_EINVAL, "mv_trans_mv: the fused peer exchange needs k <= %d", kPanel);
+  if (coef != nullptr && k > kPanel)
+    return fail(KLS_EINVAL, "gram_dcgs2_step: the fused scalar step needs j <= %d", kPanel);
   // panels of <= kPanel columns; extras ride on the last panel
   int c0 = 0;
   do {
@@ -144,6 +147,9 @@ static int mv_trans_mv_impl(const double* Q, int64_t ldq, int64_t m, int32_t k,
     p.peers.world = 0;
     p.epoch = epoch;
     p.err = err;
+    p.coef = last ? coef : nullptr;
+    p.gout = gout;
+    p.qr = qr;
     if (peers != nullptr) p.peers = *peers;
     const int rc = nx == 1 ? launch_gram<1>(p, pws, st) : launch_gram<2>(p, pws, st);
     if (rc) return rc;
@@ -186,6 +192,37 @@ KLS_API int kls_gram_dcgs2_peer(const double* Q, int64_t ldq, int64_t m, int32_t
   pr.cap = cap;
   return mv_trans_mv_impl(Q, ldq, m, j, w, w, aw, 2, 1, out, ws, ws_bytes, stream, &pr, epoch,
                           err);
+}
+
+// kls_gram_dcgs2 with the step's device scalar arithmetic fused into the
+// kernel's last CTA (kls_dcgs2_scalars): g -> out (device), the update
+// coefficients [c, s/alpha (QR: s), t_piv, alpha] -> coef, and g -> gout
+// (mapped host memory, may be NULL).  One launch per step instead of two.
+KLS_API int kls_gram_dcgs2_step(const double* Q, int64_t ldq, int64_t m, int32_t j,
+                                const double* w, const double* aw, double* out, double* coef,
+                                double* gout, int32_t qr, void* ws, size_t ws_bytes, void* stream) {
+  if (coef == nullptr) return fail(KLS_EINVAL, "gram_dcgs2_step: null coefficient buffer");
+  return mv_trans_mv_impl(Q, ldq, m, j, w, w, aw, 2, 1, out, ws, ws_bytes, stream, nullptr, 0,
+                          nullptr, coef, gout, qr);
+}
+
+// The same fused with the peer allreduce (kls_gram_dcgs2_peer): Gram pass,
+// global reduction and scalar step in one launch.
+KLS_API int kls_gram_dcgs2_peer_step(const double* Q, int64_t ldq, int64_t m, int32_t j,
+                                     const double* w, const double* aw, double* out, double* coef,
+                                     double* gout, int32_t qr, void* ws, size_t ws_bytes,
+                                     void* const* bufs, int32_t rank, int32_t world, int32_t cap,
+                                     uint64_t epoch, int* err, void* stream) {
+  if (coef == nullptr || bufs == nullptr || err == nullptr || world < 2 ||
+      world > peer::kMaxPeers || rank < 0 || rank >= world || 2 * j + 3 > cap)
+    return fail(KLS_EINVAL, "gram_dcgs2_peer_step: bad arguments");
+  peer::Peers pr;
+  for (int r = 0; r < peer::kMaxPeers; ++r) pr.buf[r] = r < world ? static_cast<char*>(bufs[r]) : nullptr;
+  pr.rank = rank;
+  pr.world = world;
+  pr.cap = cap;
+  return mv_trans_mv_impl(Q, ldq, m, j, w, w, aw, 2, 1, out, ws, ws_bytes, stream, &pr, epoch,
+                          err, coef, gout, qr);
 }
 
 // Workspace bytes that cover any reduction launch with up to kmax basis

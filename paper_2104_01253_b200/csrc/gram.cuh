@@ -4,6 +4,7 @@
 
 #include "peer.cuh"
 #include "reduce.cuh"
+#include "step.cuh"
 
 namespace kls {
 namespace gram {
@@ -29,6 +30,11 @@ struct GramParams {
   peer::Peers peers;
   uint64_t epoch;
   int* err;
+  // DCGS2 step fusion (single panel, bext == x0): after the final sums the
+  // last CTA also runs the device scalar step on out (dcgs2_scalars_block)
+  double* coef;
+  double* gout;
+  int32_t qr;
 };
 
 constexpr int kG = 4;  // Q columns reduced together
@@ -175,7 +181,13 @@ __device__ __forceinline__ void gram_epilogue(const GramParams& p, const double*
       p.out[dst_of(i)] = s;
   }
   if (threadIdx.x == 0) *p.ticket = 0u;
-  if (!fused) return;
+  if (!fused) {
+    if (p.coef != nullptr) {
+      __syncthreads();
+      dcgs2_scalars_block(p.out, p.bext_row, p.qr, p.coef, p.gout);
+    }
+    return;
+  }
   // one-shot exchange: publish, signal every peer, wait for every peer, then
   // sum the N slots in rank order (identical bits on every rank)
   __shared__ int s_ok;
@@ -201,6 +213,10 @@ __device__ __forceinline__ void gram_epilogue(const GramParams& p, const double*
       s += v[i];
     }
     p.out[dst_of(i)] = s;
+  }
+  if (p.coef != nullptr) {
+    __syncthreads();
+    dcgs2_scalars_block(p.out, p.bext_row, p.qr, p.coef, p.gout);
   }
 }
 

@@ -13,7 +13,7 @@
 // breakdown the speculative device work is discarded.  c.c and c.s are summed
 // in a fixed order, so every rank (same g bits) computes the same
 // coefficients.
-#include "common.cuh"
+#include "step.cuh"
 
 namespace {
 
@@ -23,44 +23,7 @@ __global__ void __launch_bounds__(kThreads) dcgs2_scalars_kernel(const double* _
                                                                  int32_t j, int32_t qr,
                                                                  double* __restrict__ coef,
                                                                  double* gout) {
-  __shared__ double red[2][kWarps];
-  __shared__ double s_alpha;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  double cc = 0.0, cs = 0.0;
-  for (int i = tid; i < j; i += kThreads) {
-    const double c = g[i];
-    cc = fma(c, c, cc);
-    cs = fma(c, g[j + 1 + i], cs);
-  }
-  cc = warp_sum(cc);
-  cs = warp_sum(cs);
-  if (lane == 0) {
-    red[0][warp] = cc;
-    red[1][warp] = cs;
-  }
-  __syncthreads();
-  if (tid == 0) {
-    double scc = 0.0, scs = 0.0;
-    for (int w = 0; w < kWarps; ++w) {
-      scc += red[0][w];
-      scs += red[1][w];
-    }
-    const double beta = g[j];
-    const double s_piv = g[2 * j + 1];
-    const double alpha_sq = beta - scc;
-    const double alpha = sqrt(alpha_sq > 0.0 ? alpha_sq : 2.2250738585072014e-308);
-    coef[2 * j] = qr ? (s_piv - scs) / alpha : (s_piv - scs) / (alpha * alpha);
-    coef[2 * j + 1] = alpha;
-    s_alpha = alpha;
-  }
-  __syncthreads();
-  const double alpha = s_alpha;
-  for (int i = tid; i < j; i += kThreads) {
-    coef[i] = g[i];
-    coef[j + i] = qr ? g[j + 1 + i] : g[j + 1 + i] / alpha;
-  }
-  if (gout != nullptr)
-    for (int i = tid; i < 2 * j + 3; i += kThreads) gout[i] = g[i];
+  dcgs2_scalars_block(g, j, qr, coef, gout);
 }
 
 }  // namespace

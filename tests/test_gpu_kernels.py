@@ -63,6 +63,39 @@ def test_gram_dcgs2_matches_numpy(cuda, rng, m, k):
     assert torch.equal(out, out2)
 
 
+@pytest.mark.parametrize("m", [7, 4097, 100003])
+@pytest.mark.parametrize("j", [1, 5, 33])
+@pytest.mark.parametrize("qr", [0, 1])
+def test_gram_dcgs2_step_fuses_scalars(cuda, rng, m, j, qr):
+    """kls_gram_dcgs2_step == kls_gram_dcgs2 followed by kls_dcgs2_scalars."""
+    if m <= j:
+        pytest.skip("needs a tall basis (alpha^2 = beta - c.c > 0)")
+    lib, rt = _lib()
+    Q = np.linalg.qr(rng.standard_normal((m, j)))[0]
+    w = rng.standard_normal(m)
+    aw = rng.standard_normal(m)
+    qb, ld = _colmajor(Q)
+    wd, awd = torch.from_numpy(w).cuda(), torch.from_numpy(aw).cuda()
+    ws, wsb = rt.workspace(j + 2)
+    st = rt.stream_handle()
+    g1 = torch.empty(2 * j + 3, dtype=torch.float64, device="cuda")
+    c1 = torch.empty(2 * j + 2, dtype=torch.float64, device="cuda")
+    lib.call("kls_gram_dcgs2", qb.data_ptr(), ld, m, j, wd.data_ptr(), awd.data_ptr(), g1.data_ptr(),
+             ws, wsb, st)
+    lib.call("kls_dcgs2_scalars", g1.data_ptr(), j, qr, c1.data_ptr(), None, st)
+    g2 = torch.empty_like(g1)
+    c2 = torch.empty_like(c1)
+    gh = torch.full((2 * j + 3,), np.nan, dtype=torch.float64, device="cuda")
+    lib.call("kls_gram_dcgs2_step", qb.data_ptr(), ld, m, j, wd.data_ptr(), awd.data_ptr(),
+             g2.data_ptr(), c2.data_ptr(), gh.data_ptr(), qr, ws, wsb, st)
+    assert torch.equal(g1, g2) and torch.equal(gh, g2)
+    a, b = c1.cpu().numpy(), c2.cpu().numpy()
+    assert np.allclose(a, b, rtol=1e-14, atol=0.0)
+    c = g1[:j].cpu().numpy()
+    alpha = np.sqrt(g1[j].item() - c @ c)
+    assert b[2 * j + 1] == pytest.approx(alpha, rel=1e-13)
+
+
 @pytest.mark.parametrize("k", [0, 2, 7, 1030])
 def test_mv_trans_mv_generic_panels(cuda, rng, k):
     """k > 1024 exercises the multi-panel path; nx=1 with xnorm."""
