@@ -58,25 +58,127 @@ __global__ void __launch_bounds__(kThreads, 2) gram_kernel(GramParams p) {
   gram_epilogue<NX>(p, sacc, stride, ex, xn);
 }
 
+// Small-m K1 (a few 1e4..1e5 local rows, where the chunked kernels leave
+// most SMs idle and walk the columns as a serial chain): one 64-row block per
+// CTA, the CTA's 8 warps splitting the column groups, so a 1e4-row Gram pass
+// spreads over ~150 SMs and each warp issues its loads at once.  Same
+// per-group butterfly and epilogue as gram_kernel.
+template <int NX, bool CHECK>
+__device__ __forceinline__ void gram_small_block(const GramParams& p, int64_t row, int warp,
+                                                 int lane, double* wacc, double (&ex)[NX],
+                                                 double& xn) {
+  constexpr int V = kG * NX;
+  const double* xs[2] = {p.x0, p.x1};
+  double2 xv[NX];
+#pragma unroll
+  for (int t = 0; t < NX; ++t) xv[t] = load_pair<CHECK>(xs[t], row, p.m);
+  if (warp == 0) {
+    if (p.bext != nullptr) {
+      const double2 b = p.bext == p.x0 ? xv[0] : load_pair<CHECK>(p.bext, row, p.m);
+#pragma unroll
+      for (int t = 0; t < NX; ++t) {
+        ex[t] = fma(b.x, xv[t].x, ex[t]);
+        ex[t] = fma(b.y, xv[t].y, ex[t]);
+      }
+    }
+    if (p.xnorm) {
+      xn = fma(xv[NX - 1].x, xv[NX - 1].x, xn);
+      xn = fma(xv[NX - 1].y, xv[NX - 1].y, xn);
+    }
+  }
+  const int ng = (p.k + kG - 1) / kG;
+#pragma unroll 2
+  for (int g = warp; g < ng; g += kWarps) {
+    double2 q[kG];
+#pragma unroll
+    for (int cc = 0; cc < kG; ++cc) {
+      const int c = g * kG + cc;
+      q[cc] = c < p.k ? load_pair<CHECK>(p.Q + static_cast<int64_t>(c) * p.ldq, row, p.m)
+                      : make_double2(0.0, 0.0);
+    }
+    double acc[V];
+#pragma unroll
+    for (int cc = 0; cc < kG; ++cc)
+#pragma unroll
+      for (int t = 0; t < NX; ++t) {
+        acc[cc * NX + t] = fma(q[cc].x, xv[t].x, 0.0);
+        acc[cc * NX + t] = fma(q[cc].y, xv[t].y, acc[cc * NX + t]);
+      }
+    const double sred = warp_transpose_reduce<V>(acc, lane);
+    if ((lane & (32 / V - 1)) == 0) wacc[g * V + warp_slot<V>(lane)] += sred;
+  }
+}
+
+template <int NX>
+__global__ void __launch_bounds__(kThreads, 2) gram_small_kernel(GramParams p) {
+  extern __shared__ double sacc[];  // [kWarps][ng * kG * NX]
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int stride = (p.k + kG - 1) / kG * kG * NX;
+  double* wacc = sacc + warp * stride;
+  for (int i = lane; i < stride; i += 32) wacc[i] = 0.0;
+  __syncwarp();
+  double ex[NX];
+#pragma unroll
+  for (int t = 0; t < NX; ++t) ex[t] = 0.0;
+  double xn = 0.0;
+  const int64_t nblk = (p.m + 63) / 64;
+  for (int64_t b = blockIdx.x; b < nblk; b += gridDim.x) {
+    const int64_t row = b * 64 + 2 * lane;
+    if (b * 64 + 64 <= p.m)
+      gram_small_block<NX, false>(p, row, warp, lane, wacc, ex, xn);
+    else
+      gram_small_block<NX, true>(p, row, warp, lane, wacc, ex, xn);
+  }
+  gram_epilogue<NX>(p, sacc, stride, ex, xn);
+}
+
+constexpr int64_t kSmallRows = 1 << 15;  // at or below this the small-m K1 is used (scripts/small_probe.py)
 constexpr int kRP = 4;                   // row pairs per lane per chunk
 constexpr int kPanel = 1024;             // max Q columns per launch
 constexpr int kBlocksPerSm = 2;
 
 // K1 variant: 1 = cp.async.bulk staged (gram_tma.cu, the default: 7.3 TB/s
-// vs 7.1 TB/s for LDG at m = 1.3e8, j = 50..100), 0 = 128-bit LDG streaming.
-// KLS_GRAM=ldg|tma overrides it for experiments.
+// vs 7.1 TB/s for LDG at m = 1.3e8, j = 50..100), 0 = 128-bit LDG streaming,
+// 2 = never the small-m kernel.  KLS_GRAM=ldg|tma|big overrides it for
+// experiments.
 int gram_variant() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("KLS_GRAM");
-    v = (e && e[0] == 'l') ? 0 : 1;
+    v = (e && e[0] == 'l') ? 0 : (e && e[0] == 'b') ? 2 : 1;
   }
   return v;
 }
 
 template <int NX>
+int launch_gram_small(GramParams p, size_t ws_bytes, cudaStream_t st) {
+  // ~4 row blocks per CTA: enough CTAs to spread the rows, few enough that
+  // the last CTA's sum over the partials stays short
+  const int64_t nblk = ceil_div(p.m, 64);
+  int grid = static_cast<int>(std::min<int64_t>(std::max<int64_t>(ceil_div(nblk, 4), 32),
+                                                (int64_t)kBlocksPerSm * sm_count()));
+  grid = static_cast<int>(std::min<int64_t>(grid, nblk));
+  if (grid < 1) grid = 1;
+  const int has_b = p.bext != nullptr ? 1 : 0;
+  const int64_t nv = (int64_t)p.k * NX + has_b * NX + (p.xnorm ? 1 : 0);
+  if (!red_ws_fits(ws_bytes, grid, static_cast<int>(nv)))
+    return fail(KLS_ENOSPC, "gram_small: workspace too small");
+  const size_t smem = (size_t)kWarps * ((p.k + kG - 1) / kG) * kG * NX * sizeof(double);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(gram_small_kernel<NX>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return fail(KLS_ECUDA, "gram_small: smem attr: %s", cudaGetErrorString(e));
+  }
+  gram_small_kernel<NX><<<grid, kThreads, smem, st>>>(p);
+  return check_launch("gram_small_kernel");
+}
+
+template <int NX>
 int launch_gram(GramParams p, size_t ws_bytes, cudaStream_t st) {
-  if (gram_variant() == 1 && tma_eligible(p)) return launch_gram_tma<NX>(p, ws_bytes, st);
+  if (p.m <= kSmallRows && p.k > 0 && p.k <= kPanel && gram_variant() != 2)
+    return launch_gram_small<NX>(p, ws_bytes, st);
+  if (gram_variant() != 0 && tma_eligible(p)) return launch_gram_tma<NX>(p, ws_bytes, st);
   constexpr int64_t CROWS = 64 * kRP * kWarps;
   const int64_t nchunks = ceil_div(p.m, CROWS);
   int grid = static_cast<int>(std::min<int64_t>(nchunks, (int64_t)kBlocksPerSm * sm_count()));

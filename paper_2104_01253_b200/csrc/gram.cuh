@@ -155,7 +155,7 @@ __device__ __forceinline__ void gram_epilogue(const GramParams& p, const double*
   if (!s_last) return;
   __threadfence();
 
-  // last CTA: fixed-order sum over CTAs (4 interleaved accumulators)
+  // last CTA: fixed-order sum over CTAs (sum_partials_block)
   const int nb = gridDim.x;
   const bool fused = p.peers.world > 1;
   double* mine = fused ? peer::slot(p.peers.buf[p.peers.rank], p.peers.cap, p.epoch) : nullptr;
@@ -164,22 +164,12 @@ __device__ __forceinline__ void gram_epilogue(const GramParams& p, const double*
     if (has_b && i < nq + NX) return static_cast<int64_t>(i - nq) * p.out_ld + p.bext_row;
     return static_cast<int64_t>(NX) * p.out_ld;
   };
-  for (int i = threadIdx.x; i < nv; i += blockDim.x) {
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    int b = 0;
-    for (; b + 4 <= nb; b += 4) {
-      a0 += __ldcg(p.partials + static_cast<int64_t>(b) * nv + i);
-      a1 += __ldcg(p.partials + static_cast<int64_t>(b + 1) * nv + i);
-      a2 += __ldcg(p.partials + static_cast<int64_t>(b + 2) * nv + i);
-      a3 += __ldcg(p.partials + static_cast<int64_t>(b + 3) * nv + i);
-    }
-    for (; b < nb; ++b) a0 += __ldcg(p.partials + static_cast<int64_t>(b) * nv + i);
-    const double s = (a0 + a1) + (a2 + a3);
+  sum_partials_block(p.partials, nb, nv, [&](int i, double s) {
     if (fused)
       mine[i] = s;
     else
       p.out[dst_of(i)] = s;
-  }
+  });
   if (threadIdx.x == 0) *p.ticket = 0u;
   if (!fused) {
     if (p.coef != nullptr) {

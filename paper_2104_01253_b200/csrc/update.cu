@@ -126,6 +126,76 @@ __global__ void __launch_bounds__(kThreads, kUpdBlocksPerSm)
   }
 }
 
+// Small-m K2 (m_local <= kUpdSmallRows): one 64-row block per CTA, the 8
+// warps splitting the basis columns (k = w, w+8, ...) so every warp has all
+// its loads in flight at once; the warps' partial Q c and Q t are combined in
+// fixed warp order through shared memory, then the row arithmetic of
+// upd_chunk.  A 1e4-row update spreads over ~150 SMs instead of 10.
+constexpr int64_t kUpdSmallRows = 1 << 16;  // scripts/small_probe.py
+
+template <int NC>
+__global__ void __launch_bounds__(kThreads) dcgs2_update_small_kernel(
+    UpdParams p, const __grid_constant__ CoefPack<NC> pk) {
+  extern __shared__ double2 sct[];  // (c_k, t_k), padded to a multiple of kCols
+  __shared__ double2 part[kWarps][2][32];
+  const double* coef = NC > 0 ? pk.v : p.coef;
+  const int jpad = (p.j + kCols - 1) / kCols * kCols;
+  for (int k = threadIdx.x; k < jpad; k += kThreads)
+    sct[k] = k < p.j ? make_double2(coef[k], coef[p.j + k]) : make_double2(0.0, 0.0);
+  const double tj = coef[2 * p.j];
+  const double alpha = p.alpha_dev != nullptr ? *p.alpha_dev : p.alpha;
+  __syncthreads();
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  double* qout = p.Q + static_cast<int64_t>(p.j) * p.ldq;
+  const int64_t nblk = (p.m + 63) / 64;
+  for (int64_t b = blockIdx.x; b < nblk; b += gridDim.x) {
+    const int64_t row = b * 64 + 2 * lane;
+    const bool full = b * 64 + 64 <= p.m;
+    double2 ac = make_double2(0.0, 0.0), at = make_double2(0.0, 0.0);
+#pragma unroll 4
+    for (int k = warp; k < p.j; k += kWarps) {
+      const double* col = p.Q + static_cast<int64_t>(k) * p.ldq;
+      const double2 q = full ? load_pair<false>(col, row, p.m) : load_pair<true>(col, row, p.m);
+      const double2 ct = sct[k];
+      ac.x = fma(q.x, ct.x, ac.x);
+      ac.y = fma(q.y, ct.x, ac.y);
+      at.x = fma(q.x, ct.y, at.x);
+      at.y = fma(q.y, ct.y, at.y);
+    }
+    part[warp][0][lane] = ac;
+    part[warp][1][lane] = at;
+    __syncthreads();
+    if (warp == 0) {
+      double2 sc = make_double2(0.0, 0.0), stt = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) {
+        sc.x += part[w][0][lane].x;
+        sc.y += part[w][0][lane].y;
+        stt.x += part[w][1][lane].x;
+        stt.y += part[w][1][lane].y;
+      }
+      const double2 w = full ? load_pair_rw<false>(p.w, row, p.m) : load_pair_rw<true>(p.w, row, p.m);
+      const double2 a = full ? load_pair<false>(p.aw, row, p.m) : load_pair<true>(p.aw, row, p.m);
+      double2 qn, wn;
+      qn.x = (w.x - sc.x) / alpha;
+      qn.y = (w.y - sc.y) / alpha;
+      const double ax = p.divide ? a.x / alpha : a.x;
+      const double ay = p.divide ? a.y / alpha : a.y;
+      wn.x = ax - fma(qn.x, tj, stt.x);
+      wn.y = ay - fma(qn.y, tj, stt.y);
+      if (full) {
+        store_pair<false>(qout, row, p.m, qn);
+        store_pair<false>(p.w_out, row, p.m, wn);
+      } else {
+        store_pair<true>(qout, row, p.m, qn);
+        store_pair<true>(p.w_out, row, p.m, wn);
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // TMA-staged K2: a producer warp streams 4-column x 1024-row tiles of Q and
 // the chunk's w / aw rows into shared memory with cp.async.bulk (mbarrier
 // completion, 4-stage ring + double-buffered vector slot); 8 consumer warps
@@ -405,6 +475,14 @@ template <int NC>
 int launch_update(const UpdParams& p, const double* host_coef, cudaStream_t st) {
   CoefPack<NC> pk;
   if (NC > 0) std::memcpy(pk.v, host_coef, sizeof(double) * (2 * p.j + 1));
+  if (p.m <= kUpdSmallRows && p.j > 0 && update_tma()) {
+    const size_t smem = sizeof(double2) * static_cast<size_t>((p.j + kCols - 1) / kCols * kCols + 1);
+    int rc = set_smem(reinterpret_cast<const void*>(dcgs2_update_small_kernel<NC>), smem);
+    if (rc) return rc;
+    const int grid = grid_for(p.m, 64, 4);
+    dcgs2_update_small_kernel<NC><<<grid, kThreads, smem, st>>>(p, pk);
+    return check_launch("dcgs2_update_small_kernel");
+  }
   const int jp = (p.j + kCols - 1) / kCols * kCols;
   const size_t tsmem = 256 + sizeof(double2) * (jp + 1) +
                        sizeof(double) * (static_cast<size_t>(kUStages) * kCols * kUR + 4 * kUR);

@@ -273,6 +273,7 @@ def halo_plan(rank, windows):
 class DenseOperator(LinearOperator):
     """Small dense operator (problems.py:68-85), single rank."""
 
+
     def __init__(self, a, comm=None):
         a = np.asarray(a, dtype=np.float64)
         if a.ndim != 2 or a.shape[0] != a.shape[1]:
