@@ -272,10 +272,14 @@ class PeerLink:
 
     def symmetric_vector(self, n):
         """A zeroed device vector in symmetric memory plus every rank's
-        pointer to its copy."""
+        pointer to its copy.  Collective; ranks may ask for different
+        lengths (uneven row blocks): every copy gets the largest."""
+        import torch.distributed as dist
         import torch.distributed._symmetric_memory as symm_mem
 
-        t = symm_mem.empty(max(n, 2), dtype=torch.float64, device=device())
+        nmax = torch.tensor([max(n, 2)], dtype=torch.int64, device=device())
+        dist.all_reduce(nmax, op=dist.ReduceOp.MAX, group=self.comm.group)
+        t = symm_mem.empty(int(nmax.item()), dtype=torch.float64, device=device())
         t.zero_()
         hdl = symm_mem.rendezvous(t, self._group_name)
         return t, [int(p) for p in hdl.buffer_ptrs], hdl

@@ -13,14 +13,17 @@ from conftest import ROOT
 pytestmark = pytest.mark.gpu
 
 
-def test_row_sharded_parity_nccl(cuda):
+@pytest.mark.parametrize("want", [4, 3])
+def test_row_sharded_parity_nccl(cuda, want):
+    """4 ranks (or all there are), and 3 ranks: uneven row blocks."""
     import torch
 
-    n = min(torch.cuda.device_count(), 4)
-    if n < 2:
-        pytest.skip("needs >= 2 GPUs")
+    have = torch.cuda.device_count()
+    n = min(have, want)
+    if n < 2 or (want == 3 and have < 3):
+        pytest.skip("needs >= 2 GPUs (3 for the uneven split)")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
-           "--master-addr=127.0.0.1", "--master-port=29517",
+           "--master-addr=127.0.0.1", f"--master-port={29517 + want}",
            os.path.join(ROOT, "scripts", "dist_check.py")]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
