@@ -98,6 +98,22 @@ def main():
         dev = float(np.max(dh)) if g.iterations == r["iterations"] else float("inf")
         res["gmres_hist_maxdiff"] = dev
         ok &= g.iterations == r["iterations"] and dev <= 1e-8
+    # Krylov-Schur on the row-sharded operator: every locked value must be an
+    # exact eigenvalue (manteuffel_eigenvalues) with the right multiplicity,
+    # the lock history identical on all ranks, Ritz vectors sharded
+    spec = kls.ManteuffelSpec(k=8)
+    op = kls.CsrOperator(kls.manteuffel_build(spec))
+    table = kls.manteuffel_eigenvalues(spec)
+    ks = kls.krylov_schur_run(op, kls.KrylovSchurConfig(max_basis=30, tol=1e-7, scheme="dcgs2",
+                                                        max_restarts=8), seed=11, exact=table)
+    hist = [None] * world
+    dist.all_gather_object(hist, ks.lock_history)
+    rep = kls.match_eigenvalues(ks.values.real, table, 1e-7)
+    res["ks_locked"] = ks.invariant_dim
+    res["ks_matched"] = rep.n_matched
+    ok &= (all(h == hist[0] for h in hist) and ks.invariant_dim > 0
+           and rep.n_matched == len(ks.values) and not ks.over_multiplicity
+           and ks.vectors.shape[0] == op.m_local)
     res["ok"] = bool(ok)
     flag = torch.tensor([1.0 if ok or rank != 0 else 0.0], device="cuda")
     dist.all_reduce(flag, op=dist.ReduceOp.MIN)
