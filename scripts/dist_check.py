@@ -98,6 +98,17 @@ def main():
         dev = float(np.max(dh)) if g.iterations == r["iterations"] else float("inf")
         res["gmres_hist_maxdiff"] = dev
         ok &= g.iterations == r["iterations"] and dev <= 1e-8
+    # DCGS2 / CGS2 QR of a row-sharded tall-skinny matrix (config 5's kernel)
+    A = np.random.Generator(np.random.PCG64(21)).standard_normal((50_021, 24))
+    for scheme in ("dcgs2", "cgs2"):
+        led = kls.SyncLedger()
+        Qd, R = kls.qr_factorize(A, scheme, ledger=led)
+        loo = kls.loss_of_orthogonality(Qd)
+        if rank == 0:
+            _, Rr, cnt = getattr(oracle, f"{scheme}_qr")(A)
+            err = float(np.max(np.abs(R - Rr)) / np.max(np.abs(Rr)))
+            res[f"qr_{scheme}_relerr"] = err
+            ok &= err <= 1e-10 and loo <= 1e-13 and led.reductions == cnt.reductions
     # Krylov-Schur on the row-sharded operator: every locked value must be an
     # exact eigenvalue (manteuffel_eigenvalues) with the right multiplicity,
     # the lock history identical on all ranks, Ritz vectors sharded
