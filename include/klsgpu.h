@@ -213,6 +213,16 @@ int kls_gram_dcgs2_step(const double* Q, int64_t ldq, int64_t m, int32_t j, cons
                         const double* aw, double* out, double* coef, double* gout, int32_t qr,
                         void* ws, size_t ws_bytes, void* stream);
 
+/* Host half of a DCGS2 Arnoldi step (arnoldi.py:367-420) in C++: guards,
+ * Pythagorean alpha, Stephen's-trick t_piv, Hessenberg column j-1 and the
+ * correction K, reproducing numpy's arithmetic bit for bit when ddot / dgemv
+ * are numpy's own cblas_ddot / cblas_dgemv (ILP64).  h: C-order Hessenberg
+ * buffer with row stride ldh.  Returns 0 (t_full, k_next: j+1 values;
+ * res = [alpha, vscale]), 1 happy breakdown, 2 Pythagorean breakdown. */
+int kls_dcgs2_host_step(const double* g, int32_t j, int64_t m, double wscale,
+                        const double* k_prev, double* h, int64_t ldh, double* t_full,
+                        double* k_next, double* res, void* ddot, void* dgemv);
+
 /* kls_gram_dcgs2 fused with the step's global reduction: the kernel's last
  * CTA performs the one-shot peer exchange itself and writes the rank-ordered
  * global sum of the 2j+3 scalars to out — compute and collective in one

@@ -39,6 +39,8 @@ SIGNATURES = {
                                                 i32, c_dp, sz, c_dp, i32, i32, i32,
                                                 ctypes.c_uint64, c_dp,
                                                 c_dp]),
+    "kls_dcgs2_host_step": (ctypes.c_int, [c_dp, i32, i64, f64, c_dp, c_dp, i64, c_dp, c_dp, c_dp,
+                                           c_dp, c_dp]),
     "kls_gram_dcgs2": (ctypes.c_int, [c_dp, i64, i64, i32, c_dp, c_dp, c_dp, c_dp, sz, c_dp]),
     "kls_dcgs2_update": (ctypes.c_int, [c_dp, i64, i64, i32, c_dp, c_dp, c_dp, f64, i32, c_dp]),
     "kls_dcgs2_scalars": (ctypes.c_int, [c_dp, i32, i32, c_dp, c_dp, c_dp]),
@@ -81,7 +83,7 @@ _NO_LAUNCH = frozenset({"kls_version", "kls_last_error", "kls_device_sm_count", 
                         "kls_host_device_ptr", "kls_workspace_bytes", "kls_peer_buffer_bytes",
                         "kls_lap7_nnz", "kls_mant5_nnz", "kls_ipc_handle_bytes",
                         "kls_peer_buffer_alloc", "kls_peer_buffer_open", "kls_peer_buffer_close",
-                        "kls_peer_buffer_free"})
+                        "kls_peer_buffer_free", "kls_dcgs2_host_step"})
 
 _lock = threading.Lock()
 _lib = None

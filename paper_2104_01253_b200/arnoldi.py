@@ -19,6 +19,7 @@ import os
 import numpy as np
 import torch
 
+from . import _lib
 from . import ledger as _ledger
 from ._engine import Engine
 from .errors import BreakdownError, DimensionError, UnknownSchemeError
@@ -34,7 +35,94 @@ def _unsupported(scheme):
         f"unknown scheme {scheme!r} (the B200 backend provides {', '.join(ARNOLDI_SCHEMES)})")
 
 
+_HOST_BLAS = None  # (cblas_ddot, cblas_dgemv) of numpy's OpenBLAS, or False
+
+
+def _host_blas():
+    """numpy's own OpenBLAS entry points (ILP64 scipy-openblas), so the C++
+    host step (kls_dcgs2_host_step) reproduces numpy's dot / matmul bit for
+    bit; False (numpy path) when this numpy carries another BLAS or the C++
+    step fails its self-check against the numpy step."""
+    global _HOST_BLAS
+    if _HOST_BLAS is None:
+        _HOST_BLAS = False
+        try:
+            import ctypes
+            import glob
+
+            libs = glob.glob(os.path.join(os.path.dirname(np.__file__), os.pardir, "numpy.libs",
+                                          "libscipy_openblas64_*.so"))
+            if len(libs) == 1:
+                blas = ctypes.CDLL(libs[0])
+                fns = (ctypes.cast(blas.scipy_cblas_ddot64_, ctypes.c_void_p).value,
+                       ctypes.cast(blas.scipy_cblas_dgemv64_, ctypes.c_void_p).value)
+                if _host_step_selfcheck(fns):
+                    _HOST_BLAS = fns
+        except (OSError, AttributeError):
+            _HOST_BLAS = False
+    return _HOST_BLAS
+
+
+def _host_step_c(g, j, m, wscale, k_prev, h, blas):
+    t_full = np.empty(j + 1)
+    k_next = np.empty(j + 1)
+    res = np.empty(2)
+    kp = np.ascontiguousarray(k_prev, dtype=np.float64) if j > 0 else None
+    st = _lib.load().kls_dcgs2_host_step(
+        g.ctypes.data, j, m, float(wscale), kp.ctypes.data if kp is not None else None,
+        h.ctypes.data, h.shape[1], t_full.ctypes.data, k_next.ctypes.data, res.ctypes.data,
+        blas[0], blas[1])
+    return st, t_full, k_next, res
+
+
+def _host_step_selfcheck(blas):
+    """The C++ step against the numpy step on seeded inputs: bitwise."""
+    rng = np.random.default_rng(5)
+    for j in (0, 1, 2, 7, 33, 100):
+        cap = j + 3
+        g = np.ascontiguousarray(rng.standard_normal(2 * j + 3))
+        g[j] = float(g[:j] @ g[:j]) + 4.0
+        g[2 * j + 2] = abs(g[2 * j + 2])
+        k_prev = rng.standard_normal(j)
+        h1 = rng.standard_normal((cap, cap - 1))
+        h2 = h1.copy()
+        ref = _host_step_numpy(g, j, 1000, 0.5, k_prev, h1, SyncLedger())
+        st, t_full, k_next, res = _host_step_c(g, j, 1000, 0.5, k_prev, h2, blas)
+        if st != 0 or ref is None:
+            return False
+        if not (np.array_equal(h1, h2) and np.array_equal(ref[1], t_full)
+                and np.array_equal(ref[4], k_next) and ref[2] == res[0] and ref[3] == res[1]):
+            return False
+    return True
+
+
 def dcgs2_host_step(g, j, m, wscale, k_prev, h, ledger):
+    """Host half of a DCGS2 step (arnoldi.py:367-420); see _host_step_numpy.
+    Runs in C++ (kls_dcgs2_host_step) with numpy's own BLAS when available —
+    identical bits, a fraction of the Python overhead."""
+    blas = _host_blas()
+    if not blas or h.dtype != np.float64 or not h.flags.c_contiguous:
+        return _host_step_numpy(g, j, m, wscale, k_prev, h, ledger)
+    g = np.ascontiguousarray(g, dtype=np.float64)
+    st, t_full, k_next, res = _host_step_c(g, j, m, wscale, k_prev, h, blas)
+    if st == 1:
+        return None
+    if st == 2:
+        ledger.add_flops(2 * j)  # the c.c of the failed norm, as the numpy step
+        raise BreakdownError(f"cancellation in the delayed norm of basis column {j}",
+                             kind="pythagorean", column=j)
+    if st != 0:
+        raise RuntimeError("kls_dcgs2_host_step: bad arguments")
+    ledger.add_flops(2 * j)
+    ledger.record(_ledger.MV_TIMES_MAT_ADD_MV, flops=2 * m * j)  # u = w - Q c
+    ledger.add_flops(2 * j)
+    ledger.add_flops(2 * (j + 1) * j)
+    ledger.add_flops(m)
+    ledger.record(_ledger.MV_TIMES_MAT_ADD_MV, flops=2 * m * (j + 1))  # w' = aw/alpha - V t
+    return g[:j].copy(), t_full, float(res[0]), float(res[1]), k_next
+
+
+def _host_step_numpy(g, j, m, wscale, k_prev, h, ledger):
     """Host half of a DCGS2 Arnoldi step (arnoldi.py:367-420), from the
     reduced vector g = [c, beta, s, s_piv, ||aw||^2] of kls_gram_dcgs2.
 
