@@ -324,6 +324,25 @@ class Engine:
                   self.ws, self.wsb, self.st)
         return self._finish(3)
 
+    def resid_norms_queue(self, b, ax, x, out):
+        """resid_norms into the device tensor `out` (3 doubles, summed over
+        ranks) without waiting: for diagnostics read back later in bulk."""
+        trace.note("resid_norms", 24 * self.ml)
+        if self.world == 1:
+            _lib.call("kls_resid_norms", b.data_ptr(), ax.data_ptr(), x.data_ptr(), self.ml,
+                      out.data_ptr(), self.ws, self.wsb, self.st)
+            return
+        if self.peer is not None:
+            self.stage.ensure(3)
+            src = self.stage.dev_out.data_ptr()
+            _lib.call("kls_resid_norms", b.data_ptr(), ax.data_ptr(), x.data_ptr(), self.ml, src,
+                      self.ws, self.wsb, self.st)
+            self.peer.allreduce(src, 3, out.data_ptr(), self.st)
+            return
+        _lib.call("kls_resid_norms", b.data_ptr(), ax.data_ptr(), x.data_ptr(), self.ml,
+                  out.data_ptr(), self.ws, self.wsb, self.st)
+        self.comm.allreduce_(out)
+
     def divide_into(self, dst, src, alpha):
         trace.note("scale", 16 * self.ml)
         _lib.call("kls_scale", src.data_ptr(), dst.data_ptr(), self.ml, float(alpha), 0, self.st)
