@@ -179,6 +179,48 @@ int64_t kls_mant5_nnz(int64_t k, int64_t row_lo, int64_t row_hi);
 int kls_build_mant5_csr(int64_t k, int64_t row_lo, int64_t nrows, int64_t col_base, double diff,
                         double conv, int64_t* rowptr, int32_t* col, double* val, void* stream);
 
+/* ---- one-GPU step plan ------------------------------------------------------
+ * The DCGS2 lookahead's per-step launches in one host call
+ * (paper_2104_01253_b200/arnoldi.py _step_ahead): update of step j (w ->
+ * w_out, column j of Q; coefficients from the previous scalar step in cdev),
+ * the operator (x_out = w_out's operand address -> aw_out), and, when gram
+ * != 0, the fused Gram + scalar step of step j+1 into gdev / cdev /
+ * gout[slot], then event[slot] is recorded. */
+enum { KLS_OP_ELL = 1, KLS_OP_CSR = 2, KLS_OP_STENCIL7 = 3, KLS_OP_DENSE = 4 };
+typedef struct {
+  int32_t kind;   /* KLS_OP_* */
+  int32_t width;  /* ELL: entries per row */
+  int64_t m;      /* rows */
+  int64_t n0;     /* ELL: ld; stencil: nx; dense: lda */
+  int64_t n1;     /* stencil: ny */
+  int64_t n2;     /* stencil: nz */
+  const void* p0; /* ELL: ecol; CSR: rowptr; dense: a */
+  const void* p1; /* ELL: eval; CSR: col */
+  const void* p2; /* ELL: elen; CSR: val */
+} KlsOpDesc;
+typedef struct {
+  double* Q;
+  int64_t ldq;
+  int64_t m;
+  double* gdev;
+  double* cdev;
+  double* gout[2];
+  void* ws;
+  size_t ws_bytes;
+  void* stream;
+  void* event[2];
+  int32_t divide; /* 1: Arnoldi form, 0: QR form */
+  int32_t qr;     /* scalar step in QR form */
+  KlsOpDesc op;
+} KlsStepPlan;
+int kls_dcgs2_queue_step(const KlsStepPlan* plan, int32_t j, const double* w, double* w_out,
+                         const double* x_out, const double* aw, double* aw_out, int32_t slot,
+                         int32_t gram);
+int kls_event_create(void** ev);
+int kls_event_destroy(void* ev);
+int kls_event_record(void* ev, void* stream);
+int kls_event_sync(void* ev);
+
 /* ---- cross-GPU exchange over NVLink peer memory ---------------------------
  * Symmetric buffers (same layout on every rank, mapped into every peer) of
  * kls_peer_buffer_bytes(cap) bytes; bufs[r] is rank r's buffer as seen from

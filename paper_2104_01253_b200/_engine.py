@@ -61,8 +61,14 @@ class Engine:
         self.slot_dev = [self.res_dev + 8 * nres * (1 + s) for s in (0, 1)]
         self.gdev = torch.empty(nres, dtype=torch.float64, device=dev)
         self.cdev = torch.empty(nres, dtype=torch.float64, device=dev)
-        self.slot_ev = [torch.cuda.Event(), torch.cuda.Event()]
-        self.tstream = torch.cuda.current_stream()  # the stream self.st names
+        # completion events of the two lookahead slots (CUDA events owned by
+        # the library, so kls_dcgs2_queue_step can record them too)
+        self.slot_ev = []
+        for _ in range(2):
+            ev = ctypes.c_void_p()
+            _lib.call("kls_event_create", ctypes.byref(ev))
+            self.slot_ev.append(ev.value)
+        self._plan = None  # kls_dcgs2_queue_step plan (one GPU), False when n/a
         self.ws, self.wsb = runtime.workspace_for(self.st, capacity + 1)
         # N > 1: the per-step reduction goes over NVLink peer memory when
         # available (csrc/comm.cu), else through NCCL
@@ -190,11 +196,11 @@ class Engine:
                 self.comm.allreduce_(self.gdev[:count])
             _lib.call("kls_dcgs2_scalars", self.gdev.data_ptr(), j, qflag, self.cdev.data_ptr(),
                       self.slot_dev[slot], self.st)
-        self.slot_ev[slot].record(self.tstream)
+        _lib.call("kls_event_record", self.slot_ev[slot], self.st)
 
     def wait_slot(self, slot, count):
         """Block until the queued Gram of `slot` has landed; its 2j+3 values."""
-        self.slot_ev[slot].synchronize()
+        _lib.call("kls_event_sync", self.slot_ev[slot])
         if self.peer is not None:
             self.peer.check()
         runtime.XFER["d2h"] += 8 * count
@@ -351,6 +357,43 @@ class Engine:
     def apply(self, x, y):
         """Uncounted operator application (the caller bumps op.napply)."""
         self.op.apply_into(x, y, self.st)
+
+    def __del__(self):
+        try:
+            for ev in getattr(self, "slot_ev", ()):
+                _lib.call("kls_event_destroy", ev)
+        except Exception:  # interpreter shutdown: the driver reclaims them
+            pass
+
+    # -- one-GPU step plan (kls_dcgs2_queue_step) ---------------------------------
+    def step_plan(self, qr=False):
+        """The launch plan of the lookahead step — update, operator, Gram +
+        scalar step, slot event — as one host call, or None (several ranks,
+        an operator without a plain-pointer description, or a tracer that
+        times each kernel)."""
+        if trace._active is not None:
+            return None
+        if self._plan is None:
+            self._plan = False
+            desc = self.op.op_desc() if self.world == 1 else None
+            if desc is not None:
+                p = _lib.KlsStepPlan()
+                p.Q, p.ldq, p.m = self.qptr, self.ld, self.ml
+                p.gdev, p.cdev = self.gdev.data_ptr(), self.cdev.data_ptr()
+                p.gout[0], p.gout[1] = self.slot_dev
+                p.ws, p.ws_bytes, p.stream = self.ws, self.wsb, self.st
+                p.event[0], p.event[1] = self.slot_ev
+                p.divide, p.qr = (0, 1) if qr else (1, 0)
+                p.op = desc
+                self._plan = p
+        return self._plan or None
+
+    def queue_step(self, plan, j, w, w_out, aw, aw_out, slot, gram):
+        """Step j of the lookahead through the plan: w -> w_out (and column j),
+        A w_out -> aw_out, then (gram) Gram_{j+1} into `slot`."""
+        _lib.call("kls_dcgs2_queue_step", ctypes.byref(plan), j, w.data_ptr(), w_out.local.data_ptr(),
+                  w_out.ext_ptr, aw.data_ptr(), aw_out.data_ptr(), slot, 1 if gram else 0)
+        _lib.count_launches(2 if gram else 1)
 
     def check_capacity(self, n):
         if n > self.capacity:

@@ -375,13 +375,16 @@ class _DelayedArnoldi(_BaseArnoldi):
         slot = self._slot
         # speculation: this step's update and operator (into the spare
         # buffers), then the next Gram
-        e.update_ahead(j, w.local, w2.local, aw, divide=True)
+        nxt = 1 - slot if j + 2 < self.capacity else None
         self.op.napply += 1
-        e.apply(w2, aw2)
-        nxt = None
-        if j + 2 < self.capacity:
-            nxt = 1 - slot
-            e.gram_ahead(j + 1, w2.local, aw2, nxt)
+        plan = e.step_plan()
+        if plan is not None:  # one host call for the three launches
+            e.queue_step(plan, j, w.local, w2, aw, aw2, nxt or 0, nxt is not None)
+        else:
+            e.update_ahead(j, w.local, w2.local, aw, divide=True)
+            e.apply(w2, aw2)
+            if nxt is not None:
+                e.gram_ahead(j + 1, w2.local, aw2, nxt)
         g = e.wait_slot(slot, 2 * j + 3)
         self._rec(_ledger.MV_TRANS_MV, 2 * m * (j + 1) * 2)
         try:

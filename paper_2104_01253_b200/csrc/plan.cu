@@ -1,0 +1,70 @@
+// Per-step launch plan of the one-GPU DCGS2 lookahead (arnoldi.py's
+// _step_ahead): one host call queues the fused update of step j, the
+// operator on its output and the Gram pass (+ scalar step) of step j + 1,
+// and records the step's completion event — instead of three Python-level
+// launches and a torch event.  At latency-bound sizes (config 1, GMRES and
+// Krylov-Schur tails) that is the difference between a host-bound and a
+// GPU-bound step.  Composes the public entry points, so the kernels and
+// their results are exactly those of the launch-by-launch path.
+#include "klsgpu.h"
+#include "common.cuh"
+
+using namespace kls;
+
+static int apply_op(const KlsOpDesc* op, const double* x, double* y, void* stream) {
+  switch (op->kind) {
+    case KLS_OP_ELL:
+      return kls_ell_spmv(static_cast<const int32_t*>(op->p0), static_cast<const double*>(op->p1),
+                          static_cast<const uint8_t*>(op->p2), op->width, op->m, op->n0, x, y,
+                          stream);
+    case KLS_OP_CSR:
+      return kls_csr_spmv(static_cast<const int64_t*>(op->p0), static_cast<const int32_t*>(op->p1),
+                          static_cast<const double*>(op->p2), op->m, x, y, stream);
+    case KLS_OP_STENCIL7:
+      return kls_stencil7(x, nullptr, nullptr, y, op->n0, op->n1, op->n2, stream);
+    case KLS_OP_DENSE:
+      return kls_dense_gemv(static_cast<const double*>(op->p0), op->n0, op->m, x, y, stream);
+    default:
+      return fail(KLS_EINVAL, "step plan: unknown operator kind %d", op->kind);
+  }
+}
+
+KLS_API int kls_event_create(void** ev) {
+  cudaEvent_t e;
+  const cudaError_t rc = cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  if (rc != cudaSuccess) return fail(KLS_ECUDA, "event create: %s", cudaGetErrorString(rc));
+  *ev = e;
+  return KLS_OK;
+}
+
+KLS_API int kls_event_destroy(void* ev) {
+  const cudaError_t rc = cudaEventDestroy(static_cast<cudaEvent_t>(ev));
+  return rc == cudaSuccess ? KLS_OK : fail(KLS_ECUDA, "event destroy: %s", cudaGetErrorString(rc));
+}
+
+KLS_API int kls_event_record(void* ev, void* stream) {
+  const cudaError_t rc = cudaEventRecord(static_cast<cudaEvent_t>(ev), static_cast<cudaStream_t>(stream));
+  return rc == cudaSuccess ? KLS_OK : fail(KLS_ECUDA, "event record: %s", cudaGetErrorString(rc));
+}
+
+KLS_API int kls_event_sync(void* ev) {
+  const cudaError_t rc = cudaEventSynchronize(static_cast<cudaEvent_t>(ev));
+  return rc == cudaSuccess ? KLS_OK : fail(KLS_ECUDA, "event sync: %s", cudaGetErrorString(rc));
+}
+
+KLS_API int kls_dcgs2_queue_step(const KlsStepPlan* p, int32_t j, const double* w, double* w_out,
+                                 const double* x_out, const double* aw, double* aw_out,
+                                 int32_t slot, int32_t gram) {
+  if (p == nullptr || slot < 0 || slot > 1) return fail(KLS_EINVAL, "queue_step: bad plan or slot");
+  int rc = kls_dcgs2_update_dev(p->Q, p->ldq, p->m, j, w, w_out, aw, p->cdev, p->divide, p->stream);
+  if (rc) return rc;
+  rc = apply_op(&p->op, x_out, aw_out, p->stream);
+  if (rc) return rc;
+  if (gram) {
+    rc = kls_gram_dcgs2_step(p->Q, p->ldq, p->m, j + 1, w_out, aw_out, p->gdev, p->cdev,
+                             p->gout[slot], p->qr, p->ws, p->ws_bytes, p->stream);
+    if (rc) return rc;
+    rc = kls_event_record(p->event[slot], p->stream);
+  }
+  return rc;
+}

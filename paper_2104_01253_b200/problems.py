@@ -164,6 +164,11 @@ class LinearOperator:
     def _launch(self, x, y, st):
         raise NotImplementedError
 
+    def op_desc(self):
+        """The one-rank apply as plain pointers (include/klsgpu.h KlsOpDesc)
+        for the C++ step plan, or None when the operator is not plain."""
+        return None
+
     # -- norms / dense ------------------------------------------------------
     def to_dense(self, max_order=4000):
         if self.n > max_order:
@@ -287,6 +292,9 @@ class DenseOperator(LinearOperator):
     def _launch(self, x, y, st):
         _lib.call("kls_dense_gemv", self._dev.data_ptr(), self.n, self.n, x.local.data_ptr(),
                   y.data_ptr(), st)
+
+    def op_desc(self):
+        return _lib.KlsOpDesc(kind=_lib.OP_DENSE, m=self.n, n0=self.n, p0=self._dev.data_ptr())
 
     def to_dense(self, max_order=None):
         return self.a.copy()
@@ -521,6 +529,16 @@ class CsrOperator(LinearOperator):
         _lib.call("kls_csr_spmv", self._rowptr_p, self._col_p, self._val_p, self.m_local,
                   x.ext_ptr, y.data_ptr(), st)
 
+    def op_desc(self):
+        if self.comm.world != 1 or self.m_local == 0:
+            return None
+        if self._ell is not None:
+            ecol, evals, elen, width, ld = self._ell
+            return _lib.KlsOpDesc(kind=_lib.OP_ELL, width=width, m=self.m_local, n0=ld,
+                                  p0=ecol.data_ptr(), p1=evals.data_ptr(), p2=elen.data_ptr())
+        return _lib.KlsOpDesc(kind=_lib.OP_CSR, m=self.m_local, p0=self._rowptr_p,
+                              p1=self._col_p, p2=self._val_p)
+
     def to_dense(self, max_order=4000):
         if self.n > max_order:
             raise MemoryError(f"dense assembly of order {self.n} refused (limit {max_order})")
@@ -745,6 +763,13 @@ class StencilLaplace3D(LinearOperator):
         hi = x.hi.data_ptr() if x.hi is not None else None
         _lib.call("kls_stencil7", x.local.data_ptr(), lo, hi, y.data_ptr(),
                   self.x_hi - self.x_lo, ny, nz, st)
+
+    def op_desc(self):
+        if self.comm.world != 1 or self.m_local == 0:
+            return None
+        _, ny, nz = self.dims
+        return _lib.KlsOpDesc(kind=_lib.OP_STENCIL7, m=self.m_local, n0=self.x_hi - self.x_lo,
+                              n1=ny, n2=nz)
 
     def _launch_peer(self, x, y, st):
         """Signal 'my vector is written' to the x-neighbours, then run the

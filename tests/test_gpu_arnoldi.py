@@ -387,3 +387,26 @@ def test_device_function_operator(cuda, scheme):
     assert op.napply == (16 if scheme == "dcgs2" else 15)  # delayed: steps + 1
     with pytest.raises(K.DimensionError):
         K.DeviceFunctionOperator(n, lambda x: x[:-1]).apply(start)
+
+
+@pytest.mark.parametrize("which", ["csr", "stencil", "dense"])
+def test_step_plan_bitwise(cuda, which, monkeypatch):
+    """kls_dcgs2_queue_step (one host call per lookahead step) gives bitwise
+    the expansion of the three separate launches."""
+    K = kls()
+    from paper_2104_01253_b200 import _engine
+
+    if which == "csr":
+        op = mant(30)
+    elif which == "stencil":
+        op = K.laplace3d(9, 8, 7)
+    else:
+        op = K.DenseOperator(np.random.default_rng(4).standard_normal((300, 300)))
+    start = np.random.Generator(np.random.PCG64(11)).standard_normal(op.n)
+    V1, H1 = K.arnoldi_expand(op, start, "dcgs2", steps=40)
+    V1 = V1.clone()
+    n1 = op.napply
+    monkeypatch.setattr(_engine.Engine, "step_plan", lambda self, qr=False: None)
+    V2, H2 = K.arnoldi_expand(op, start, "dcgs2", steps=40)
+    assert torch.equal(V1, V2) and np.array_equal(H1, H2)
+    assert op.napply == 2 * n1
