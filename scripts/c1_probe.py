@@ -1,3 +1,7 @@
+"""Config-1-sized DCGS2 expansions (m = 1e4, 50 steps) for an ncu launch list:
+
+    ncu --metrics gpu__time_duration.sum --csv python scripts/c1_probe.py
+"""
 import os, sys, time
 import numpy as np, torch
 sys.path.insert(0, '/root/repo')

@@ -1,3 +1,7 @@
+"""cProfile of Krylov-Schur at config-4 size: where a restart spends its time.
+
+    python scripts/ks_probe.py [k=3163] [restarts=400]
+"""
 import cProfile, io, json, os, pstats, sys, time
 import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))

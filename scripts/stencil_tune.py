@@ -1,3 +1,6 @@
+"""Time the matrix-free stencil apply at config-3 size (m = 1.3e8); sweep the
+x-chunk with KLS_STENCIL_XCHUNK and the variant with KLS_STENCIL=reg|smem.
+"""
 import os, sys, json, torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2104_01253_b200 import laplace3d
