@@ -295,6 +295,18 @@ int kls_stencil7_peer(const double* x, const double* x_lo, const double* x_hi, d
                       int64_t nx, int64_t ny, int64_t nz, void* mybuf, int32_t rank,
                       uint64_t epoch, int* err, void* stream);
 
+/* kls_ell_spmv with the row block's halo columns read straight from the
+ * neighbouring ranks' vectors over NVLink (the CSR operator's halo exchange,
+ * problems.py:127-136 across ranks, fused into the apply): x_lo = the lower
+ * neighbour's last nlo rows (peer-mapped), x_hi = the upper neighbour's first
+ * rows (peer-mapped), NULL when absent.  Rows [b_lo, nrows - b_hi) touch only
+ * owned columns and run first without waiting; the boundary rows wait for
+ * this rank's halo flags from lo_rank / hi_rank (in mybuf) to reach epoch. */
+int kls_ell_spmv_peer(const int32_t* ecol, const double* eval, const uint8_t* elen, int32_t width,
+                      int64_t nrows, int64_t ld, const double* x, const double* x_lo, int64_t nlo,
+                      const double* x_hi, double* y, int64_t b_lo, int64_t b_hi, void* mybuf,
+                      int32_t lo_rank, int32_t hi_rank, uint64_t epoch, int* err, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

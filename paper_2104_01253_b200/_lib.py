@@ -46,6 +46,9 @@ SIGNATURES = {
     "kls_event_destroy": (ctypes.c_int, [c_dp]),
     "kls_event_record": (ctypes.c_int, [c_dp, c_dp]),
     "kls_event_sync": (ctypes.c_int, [c_dp]),
+    "kls_ell_spmv_peer": (ctypes.c_int, [c_dp, c_dp, c_dp, i32, i64, i64, c_dp, c_dp, i64, c_dp,
+                                         c_dp, i64, i64, c_dp, i32, i32, ctypes.c_uint64, c_dp,
+                                         c_dp]),
     "kls_gram_dcgs2": (ctypes.c_int, [c_dp, i64, i64, i32, c_dp, c_dp, c_dp, c_dp, sz, c_dp]),
     "kls_dcgs2_update": (ctypes.c_int, [c_dp, i64, i64, i32, c_dp, c_dp, c_dp, f64, i32, c_dp]),
     "kls_dcgs2_scalars": (ctypes.c_int, [c_dp, i32, i32, c_dp, c_dp, c_dp]),

@@ -13,6 +13,7 @@
 // the reference's order (x-1, x+1, y-1, y+1, z-1, z+1).  For a row-sharded
 // grid the neighbouring x-planes of other ranks come in through x_lo / x_hi.
 #include "stencil.cuh"
+#include "peer.cuh"
 
 #include <cstdlib>
 
@@ -222,11 +223,54 @@ __device__ __forceinline__ void ell_fetch(EllRow<W>& r, const int32_t* ecol, con
   }
 }
 
-template <int W>
+// x accessors of the pipelined ELL product: the rank's window as one array,
+// or (peer) as three — column c of [lo halo | own rows | hi halo] lives at
+// lo[c], own[c - nlo] or hi[c - nlo - nown], the halo parts being the
+// neighbouring ranks' vectors read over NVLink.
+struct XPlain {
+  const double* x;
+  __device__ __forceinline__ double operator()(int64_t c) const { return __ldg(x + c); }
+};
+struct XWindow {
+  const double* lo;
+  const double* own;
+  const double* hi;
+  int64_t nlo;
+  int64_t nown;
+  __device__ __forceinline__ double operator()(int64_t c) const {
+    if (c < nlo) return __ldg(lo + c);
+    c -= nlo;
+    if (c < nown) return __ldg(own + c);
+    return __ldg(hi + (c - nown));
+  }
+};
+
+// Peer variant: a CTA first waits until the neighbours' "vector written"
+// flags (this rank's halo flags) reach epoch.
+struct PeerWait {
+  const uint64_t* flag_lo;
+  const uint64_t* flag_hi;
+  uint64_t epoch;
+  int* err;
+};
+
+template <int W, typename XA>
 __global__ void __launch_bounds__(kThreads, kEllBlocks) ell_spmv_pipe_kernel(
     const int32_t* __restrict__ ecol, const double* __restrict__ eval,
-    const uint8_t* __restrict__ elen, int64_t nrows, int64_t ld, const double* __restrict__ x,
-    double* __restrict__ y) {
+    const uint8_t* __restrict__ elen, int64_t nrows, int64_t ld, XA x,
+    double* __restrict__ y, PeerWait pw) {
+  if (pw.flag_lo != nullptr || pw.flag_hi != nullptr) {
+    __shared__ int s_ok;
+    if (threadIdx.x == 0) {
+      bool ok = true;
+      if (pw.flag_lo != nullptr) ok = ok && peer::wait_flag(pw.flag_lo, pw.epoch);
+      if (pw.flag_hi != nullptr) ok = ok && peer::wait_flag(pw.flag_hi, pw.epoch);
+      s_ok = ok;
+      if (!ok) *pw.err = 1;
+    }
+    __syncthreads();
+    if (!s_ok) return;
+  }
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= nrows) return;
@@ -239,7 +283,7 @@ __global__ void __launch_bounds__(kThreads, kEllBlocks) ell_spmv_pipe_kernel(
     if (nx < nrows) ell_fetch<W>(nxt, ecol, eval, elen, ld, nx);
     double p[W];
 #pragma unroll
-    for (int k = 0; k < W; ++k) p[k] = k < cur.n ? __dmul_rn(cur.v[k], __ldg(x + cur.c[k])) : 0.0;
+    for (int k = 0; k < W; ++k) p[k] = k < cur.n ? __dmul_rn(cur.v[k], x(cur.c[k])) : 0.0;
     double acc = 0.0;
     if (cur.n > 0) {
       double r = -0.0;
@@ -253,6 +297,26 @@ __global__ void __launch_bounds__(kThreads, kEllBlocks) ell_spmv_pipe_kernel(
     cur = nxt;
     i = nx;
   }
+}
+
+int grid_1d(int64_t n, int per_sm) {
+  const int64_t blocks = ceil_div(n, kThreads);
+  int g = static_cast<int>(std::min<int64_t>(blocks, (int64_t)per_sm * sm_count()));
+  return g < 1 ? 1 : g;
+}
+
+template <typename XA>
+int launch_ell_pipe(const int32_t* ecol, const double* eval, const uint8_t* elen, int32_t width,
+                    int64_t nrows, int64_t ld, XA x, double* y, PeerWait pw, cudaStream_t st) {
+  // one wave of resident CTAs; each thread walks its rows with a one-row lookahead
+  const int grid = grid_1d(nrows, kEllBlocks);
+  if (width <= 4)
+    ell_spmv_pipe_kernel<4, XA><<<grid, kThreads, 0, st>>>(ecol, eval, elen, nrows, ld, x, y, pw);
+  else if (width <= 6)
+    ell_spmv_pipe_kernel<6, XA><<<grid, kThreads, 0, st>>>(ecol, eval, elen, nrows, ld, x, y, pw);
+  else
+    ell_spmv_pipe_kernel<8, XA><<<grid, kThreads, 0, st>>>(ecol, eval, elen, nrows, ld, x, y, pw);
+  return check_launch("ell_spmv_pipe_kernel");
 }
 
 __global__ void __launch_bounds__(kTileZ * kTileY) stencil7_kernel(
@@ -301,11 +365,6 @@ __global__ void __launch_bounds__(kThreads) dense_gemv_kernel(const double* __re
   }
 }
 
-int grid_1d(int64_t n, int per_sm) {
-  const int64_t blocks = ceil_div(n, kThreads);
-  int g = static_cast<int>(std::min<int64_t>(blocks, (int64_t)per_sm * sm_count()));
-  return g < 1 ? 1 : g;
-}
 
 }  // namespace
 
@@ -405,13 +464,48 @@ KLS_API int kls_ell_spmv(const int32_t* ecol, const double* eval, const uint8_t*
       ell_spmv_kernel<8><<<grid, kThreads, 0, st>>>(ecol, eval, elen, nrows, ld, x, y);
     return check_launch("ell_spmv_kernel");
   }
-  // one wave of resident CTAs; each thread walks its rows with a one-row lookahead
-  const int grid = grid_1d(nrows, kEllBlocks);
-  if (width <= 4)
-    ell_spmv_pipe_kernel<4><<<grid, kThreads, 0, st>>>(ecol, eval, elen, nrows, ld, x, y);
-  else if (width <= 6)
-    ell_spmv_pipe_kernel<6><<<grid, kThreads, 0, st>>>(ecol, eval, elen, nrows, ld, x, y);
-  else
-    ell_spmv_pipe_kernel<8><<<grid, kThreads, 0, st>>>(ecol, eval, elen, nrows, ld, x, y);
-  return check_launch("ell_spmv_pipe_kernel");
+  return launch_ell_pipe(ecol, eval, elen, width, nrows, ld, XPlain{x}, y,
+                         PeerWait{nullptr, nullptr, 0, nullptr}, st);
+}
+
+// kls_ell_spmv with the halo columns read from the neighbours' vectors over
+// NVLink: x_lo = lower neighbour's rows [own_lo - nlo, own_lo) (peer-mapped),
+// x_hi = upper neighbour's first rows (peer-mapped), either NULL when absent.
+// Rows [b_lo, nrows - b_hi) touch only owned columns: they run first, with
+// no wait and one plain gather per entry, overlapping the neighbours'
+// progress; the b_lo leading and b_hi trailing rows then wait for this
+// rank's halo flags from lo_rank / hi_rank (in mybuf) to reach epoch and
+// read through the three-part window.  *err is set when a neighbour does not
+// arrive within 20 s.  Same products and order: bit-identical to kls_ell_spmv.
+KLS_API int kls_ell_spmv_peer(const int32_t* ecol, const double* eval, const uint8_t* elen,
+                              int32_t width, int64_t nrows, int64_t ld, const double* x,
+                              const double* x_lo, int64_t nlo, const double* x_hi, double* y,
+                              int64_t b_lo, int64_t b_hi, void* mybuf, int32_t lo_rank,
+                              int32_t hi_rank, uint64_t epoch, int* err, void* stream) {
+  if (ecol == nullptr || eval == nullptr || elen == nullptr || x == nullptr || y == nullptr ||
+      nrows < 0 || ld < nrows || width < 1 || width > 8 || mybuf == nullptr || err == nullptr ||
+      (nlo > 0 && x_lo == nullptr) || nlo < 0 || lo_rank >= peer::kMaxPeers ||
+      hi_rank >= peer::kMaxPeers || b_lo < 0 || b_hi < 0 || b_lo + b_hi > nrows)
+    return fail(KLS_EINVAL, "ell_spmv_peer: bad arguments");
+  if (nrows == 0) return KLS_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const uint64_t* flags = reinterpret_cast<const uint64_t*>(mybuf) + peer::kMaxPeers;
+  const uint64_t* flo = (x_lo != nullptr && lo_rank >= 0) ? flags + lo_rank : nullptr;
+  const uint64_t* fhi = (x_hi != nullptr && hi_rank >= 0) ? flags + hi_rank : nullptr;
+  const PeerWait none{nullptr, nullptr, 0, nullptr};
+  const int64_t mid = nrows - b_lo - b_hi;
+  int rc = KLS_OK;
+  if (mid > 0)  // window column c of an interior row is own row c - nlo
+    rc = launch_ell_pipe(ecol + b_lo, eval + b_lo, elen + b_lo, width, mid, ld, XPlain{x - nlo},
+                         y + b_lo, none, st);
+  const XWindow xw{x_lo, x, x_hi, nlo, nrows};
+  if (rc == KLS_OK && b_lo > 0)
+    rc = launch_ell_pipe(ecol, eval, elen, width, b_lo, ld, xw, y, PeerWait{flo, fhi, epoch, err},
+                         st);
+  if (rc == KLS_OK && b_hi > 0) {
+    const int64_t r0 = nrows - b_hi;
+    rc = launch_ell_pipe(ecol + r0, eval + r0, elen + r0, width, b_hi, ld, xw, y + r0,
+                         PeerWait{flo, fhi, epoch, err}, st);
+  }
+  return rc;
 }

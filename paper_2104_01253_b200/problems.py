@@ -458,6 +458,7 @@ class CsrOperator(LinearOperator):
                           ld, ecol.data_ptr(), evals.data_ptr(), elen.data_ptr(),
                           runtime.stream_handle())
                 self._ell = (ecol, evals, elen, width, ld)
+        self._peer = False
         if self.comm.world > 1:
             self._plan = self._halo_plan()
 
@@ -485,22 +486,63 @@ class CsrOperator(LinearOperator):
     def _needs_halo(self):
         return self.halo_lo > 0 or self.halo_hi > 0
 
-    def new_vector(self):
+    def _plain_vector(self):
         return HaloVector(self.m_local, self.halo_lo, self.halo_hi, contiguous=True)
 
+    def new_vector(self):
+        """Halo-capable vector.  With an NVLink peer link and halos that come
+        from the adjacent ranks only, the vector lives in symmetric memory and
+        the apply reads the neighbours' rows directly (kls_ell_spmv_peer);
+        otherwise the halo window arrives by NCCL send/recv."""
+        if not self._peer:
+            return self._plain_vector()
+        pool = self.__dict__.setdefault("_peer_pool", [])
+        for v in pool:
+            if not v.leased:
+                v.leased = True
+                return v
+        v = PeerVector(self._link, self.m_local)
+        v.leased = True
+        pool.append(v)
+        return v
+
+    def apply_into(self, x, y, st=None):
+        if not isinstance(x, (HaloVector, PeerVector)) and self._needs_halo():
+            # scratch copies take the NCCL path (see StencilLaplace3D)
+            if self._scratch is None:
+                self._scratch = self._plain_vector()
+            self._scratch.local.copy_(x)
+            x = self._scratch
+        super().apply_into(x, y, st)
+
     def _halo_plan(self):
-        """Exchange plan from every rank's [need_lo, own_lo, own_hi, need_hi)."""
+        """Exchange plan from every rank's [need_lo, own_lo, own_hi, need_hi),
+        and whether every rank can read its halo from its adjacent ranks'
+        vectors over NVLink (decided collectively: all ranks take one path)."""
         c = self.comm
+        link = runtime.peer_link(c)
         mine = torch.tensor([self.row_lo - self.halo_lo, self.row_lo, self.row_hi,
-                             self.row_hi + self.halo_hi], dtype=torch.int64, device=runtime.device())
+                             self.row_hi + self.halo_hi,
+                             1 if (link is not None and self._ell is not None) else 0],
+                            dtype=torch.int64, device=runtime.device())
         allw = [torch.empty_like(mine) for _ in range(c.world)]
         import torch.distributed as dist
 
         dist.all_gather(allw, mine, group=c.group)
-        return halo_plan(c.rank, [tuple(int(v) for v in w.cpu().tolist()) for w in allw])
+        wins = [tuple(int(v) for v in w.cpu().tolist()) for w in allw]
+        ok = all(w[4] for w in wins)
+        for r, (nlo, lo, hi, nhi, _) in enumerate(wins):
+            if nlo < lo and (r == 0 or nlo < wins[r - 1][1]):
+                ok = False  # lower halo reaches past the adjacent rank
+            if nhi > hi and (r == c.world - 1 or nhi > wins[r + 1][2]):
+                ok = False
+        self._peer = ok
+        self._link = link if ok else None
+        self._wins = wins
+        return halo_plan(c.rank, [w[:4] for w in wins])
 
     def _exchange(self, x):
-        if self._plan is None:
+        if self._plan is None or isinstance(x, PeerVector):
             return
         import torch.distributed as dist
 
@@ -521,6 +563,8 @@ class CsrOperator(LinearOperator):
         return 16 * self.m_local + 12 * int(self._col.numel()) + 8 * (self.m_local + 1)
 
     def _launch(self, x, y, st):
+        if isinstance(x, PeerVector):
+            return self._launch_peer(x, y, st)
         if self._ell is not None:
             ecol, evals, elen, width, ld = self._ell
             _lib.call("kls_ell_spmv", ecol.data_ptr(), evals.data_ptr(), elen.data_ptr(), width,
@@ -528,6 +572,49 @@ class CsrOperator(LinearOperator):
             return
         _lib.call("kls_csr_spmv", self._rowptr_p, self._col_p, self._val_p, self.m_local,
                   x.ext_ptr, y.data_ptr(), st)
+
+    def _launch_peer(self, x, y, st):
+        """Signal 'my vector is written' to the adjacent ranks, then the ELL
+        product reading their rows of the halo window over NVLink."""
+        link, r, world = self._link, self.comm.rank, self.comm.world
+        mask = (1 << (r - 1) if r > 0 else 0) | (1 << (r + 1) if r + 1 < world else 0)
+        x_lo = x_hi = None
+        if self.halo_lo > 0:
+            lo_prev, hi_prev = self._wins[r - 1][1], self._wins[r - 1][2]
+            x_lo = x.peer_ptrs[r - 1] + 8 * (hi_prev - lo_prev - self.halo_lo)
+        if self.halo_hi > 0:
+            x_hi = x.peer_ptrs[r + 1]
+        link.halo_epoch += 1
+        rec = trace._active
+        if rec is not None and rec.events:
+            with rec.span("halo"):
+                _lib.call("kls_peer_signal", link.ptrs, r, world, mask, link.halo_epoch, st)
+        else:
+            _lib.call("kls_peer_signal", link.ptrs, r, world, mask, link.halo_epoch, st)
+        ecol, evals, elen, width, ld = self._ell
+        b_lo, b_hi = self._halo_rows()
+        _lib.call("kls_ell_spmv_peer", ecol.data_ptr(), evals.data_ptr(), elen.data_ptr(), width,
+                  self.m_local, ld, x.local.data_ptr(), x_lo, self.halo_lo, x_hi, y.data_ptr(),
+                  b_lo, b_hi, link.mybuf, r - 1 if r > 0 else -1, r + 1 if r + 1 < world else -1,
+                  link.halo_epoch, link.err_dev, st)
+
+    def _halo_rows(self):
+        """(b_lo, b_hi): the leading rows up to the last one with a lower-halo
+        column, and the trailing rows from the first one with an upper-halo
+        column (window coordinates); the rows between read owned columns only."""
+        if getattr(self, "_brows", None) is None:
+            col, rp = self._col, self._rowptr
+            m, nlo = self.m_local, self.halo_lo
+            rows = torch.repeat_interleave(torch.arange(m, device=col.device),
+                                           (rp[1:] - rp[:-1]))
+            lo_rows = rows[col[: rows.numel()] < nlo]
+            hi_rows = rows[col[: rows.numel()] >= nlo + m]
+            b_lo = int(lo_rows.max().item()) + 1 if lo_rows.numel() else 0
+            b_hi = m - int(hi_rows.min().item()) if hi_rows.numel() else 0
+            if b_lo + b_hi > m:  # overlapping boundary bands: all rows wait
+                b_lo, b_hi = m, 0
+            self._brows = (b_lo, b_hi)
+        return self._brows
 
     def op_desc(self):
         if self.comm.world != 1 or self.m_local == 0:
