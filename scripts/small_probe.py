@@ -17,7 +17,7 @@ def bench(fn, reps=200):
     e1.record(); torch.cuda.synchronize()
     return e0.elapsed_time(e1) * 1e3 / reps
 
-for m in (10_000, 100_000, 1_000_000):
+for m in [int(float(v)) for v in os.environ.get("SIZES", "1e4,1e5,1e6").split(",")]:
     for j in (10, 50, 100):
         ld = runtime.pad_rows(m)
         Q = torch.randn((j + 1, ld), dtype=torch.float64, device="cuda") / np.sqrt(m)
