@@ -28,6 +28,30 @@ constexpr int kWarps = kThreads / 32;
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// Launch `kernel` as the programmatic dependent of the preceding kernel on
+// the stream (it may start while that one finishes; it pdl_wait()s before
+// touching the predecessor's results).  KLS_PDL=0 launches plainly.
+bool pdl_enabled();
+
+template <typename K, typename... Args>
+int launch_dependent(K kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                     const char* name, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, args...);
+  if (e != cudaSuccess) return fail(KLS_ECUDA, "%s launch: %s", name, cudaGetErrorString(e));
+  return check_launch(name);
+}
+
+
 }  // namespace kls
 
 // --------------------------------------------------------------------------
@@ -69,6 +93,14 @@ __device__ __forceinline__ void store_pair(double* col, int64_t r, int64_t m, do
     col[r] = v.x;
   }
 }
+
+// Programmatic dependent launch (sm_90+): a kernel launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization may start while its
+// predecessor finishes; it must pdl_wait() before touching what the
+// predecessor writes.  The predecessor pdl_trigger()s once its main work is
+// done.  Both are no-ops outside a PDL pair.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll

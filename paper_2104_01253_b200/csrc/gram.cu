@@ -27,6 +27,7 @@ using namespace kls::gram;
 
 template <int NX, int RP>
 __global__ void __launch_bounds__(kThreads, 2) gram_kernel(GramParams p) {
+  pdl_wait();  // x vectors / basis from the preceding kernels
   extern __shared__ double sacc[];  // [kWarps][ng * kG * NX]
   constexpr int V = kG * NX;
   constexpr int64_t WROWS = 64 * RP;
@@ -111,6 +112,7 @@ __device__ __forceinline__ void gram_small_block(const GramParams& p, int64_t ro
 
 template <int NX>
 __global__ void __launch_bounds__(kThreads, 2) gram_small_kernel(GramParams p) {
+  pdl_wait();
   extern __shared__ double sacc[];  // [kWarps][ng * kG * NX]
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -170,8 +172,8 @@ int launch_gram_small(GramParams p, size_t ws_bytes, cudaStream_t st) {
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return fail(KLS_ECUDA, "gram_small: smem attr: %s", cudaGetErrorString(e));
   }
-  gram_small_kernel<NX><<<grid, kThreads, smem, st>>>(p);
-  return check_launch("gram_small_kernel");
+  return launch_dependent(gram_small_kernel<NX>, dim3(grid), dim3(kThreads), smem, st,
+                          "gram_small_kernel", p);
 }
 
 template <int NX>
@@ -195,8 +197,8 @@ int launch_gram(GramParams p, size_t ws_bytes, cudaStream_t st) {
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return fail(KLS_ECUDA, "gram: smem attr: %s", cudaGetErrorString(e));
   }
-  gram_kernel<NX, kRP><<<grid, kThreads, smem, st>>>(p);
-  return check_launch("gram_kernel");
+  return launch_dependent(gram_kernel<NX, kRP>, dim3(grid), dim3(kThreads), smem, st,
+                          "gram_kernel", p);
 }
 
 }  // namespace

@@ -114,6 +114,9 @@ __device__ __forceinline__ void gram_epilogue(const GramParams& p, const double*
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const bool consumer = warp < kWarps;
+  // the streaming is done: a dependent update (PDL) may start staging its
+  // Q tiles while the partial sums and the scalar step finish here
+  pdl_trigger();
   // CTA reduction of the per-thread extras
 #pragma unroll
   for (int t = 0; t < NX; ++t) {

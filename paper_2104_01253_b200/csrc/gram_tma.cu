@@ -27,6 +27,7 @@ constexpr int kPanelTma = 256;    // basis columns per launch (per-warp accumula
 
 template <int NX>
 __global__ void __launch_bounds__(kTmaThreads, 1) gram_tma_kernel(GramParams p) {
+  pdl_wait();  // x vectors / basis from the preceding kernels
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr int V = kG * NX;
   const int nxb = NX + ((p.bext != nullptr && p.bext != p.x0) ? 1 : 0);  // staged rhs columns
@@ -195,8 +196,8 @@ int launch_gram_tma(GramParams p, size_t ws_bytes, cudaStream_t st) {
   cudaError_t e = cudaFuncSetAttribute(gram_tma_kernel<NX>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return fail(KLS_ECUDA, "gram_tma: smem attr: %s", cudaGetErrorString(e));
-  gram_tma_kernel<NX><<<grid, kTmaThreads, smem, st>>>(p);
-  return check_launch("gram_tma_kernel");
+  return launch_dependent(gram_tma_kernel<NX>, dim3(grid), dim3(kTmaThreads), smem, st,
+                          "gram_tma_kernel", p);
 }
 
 template int launch_gram_tma<1>(GramParams, size_t, cudaStream_t);

@@ -1,6 +1,8 @@
 // Error reporting and device queries behind the C-ABI.
 #include "common.cuh"
 
+#include <cstdlib>
+
 #include <cstdarg>
 #include <cstdio>
 #include <mutex>
@@ -59,3 +61,13 @@ KLS_API int kls_host_device_ptr(void* host, void** dev) {
   if (e != cudaSuccess) return kls::fail(KLS_ECUDA, "host_device_ptr: %s", cudaGetErrorString(e));
   return KLS_OK;
 }
+
+namespace kls {
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("KLS_PDL");
+    return !(e != nullptr && e[0] == '0');
+  }();
+  return on;
+}
+}  // namespace kls

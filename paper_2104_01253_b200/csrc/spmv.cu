@@ -259,6 +259,7 @@ __global__ void __launch_bounds__(kThreads, kEllBlocks) ell_spmv_pipe_kernel(
     const int32_t* __restrict__ ecol, const double* __restrict__ eval,
     const uint8_t* __restrict__ elen, int64_t nrows, int64_t ld, XA x,
     double* __restrict__ y, PeerWait pw) {
+  pdl_wait();  // x from the preceding update
   if (pw.flag_lo != nullptr || pw.flag_hi != nullptr) {
     __shared__ int s_ok;
     if (threadIdx.x == 0) {
@@ -297,6 +298,7 @@ __global__ void __launch_bounds__(kThreads, kEllBlocks) ell_spmv_pipe_kernel(
     cur = nxt;
     i = nx;
   }
+  pdl_trigger();
 }
 
 int grid_1d(int64_t n, int per_sm) {
@@ -310,13 +312,15 @@ int launch_ell_pipe(const int32_t* ecol, const double* eval, const uint8_t* elen
                     int64_t nrows, int64_t ld, XA x, double* y, PeerWait pw, cudaStream_t st) {
   // one wave of resident CTAs; each thread walks its rows with a one-row lookahead
   const int grid = grid_1d(nrows, kEllBlocks);
+  const char* name = "ell_spmv_pipe_kernel";
   if (width <= 4)
-    ell_spmv_pipe_kernel<4, XA><<<grid, kThreads, 0, st>>>(ecol, eval, elen, nrows, ld, x, y, pw);
-  else if (width <= 6)
-    ell_spmv_pipe_kernel<6, XA><<<grid, kThreads, 0, st>>>(ecol, eval, elen, nrows, ld, x, y, pw);
-  else
-    ell_spmv_pipe_kernel<8, XA><<<grid, kThreads, 0, st>>>(ecol, eval, elen, nrows, ld, x, y, pw);
-  return check_launch("ell_spmv_pipe_kernel");
+    return launch_dependent(ell_spmv_pipe_kernel<4, XA>, dim3(grid), dim3(kThreads), 0, st, name,
+                            ecol, eval, elen, nrows, ld, x, y, pw);
+  if (width <= 6)
+    return launch_dependent(ell_spmv_pipe_kernel<6, XA>, dim3(grid), dim3(kThreads), 0, st, name,
+                            ecol, eval, elen, nrows, ld, x, y, pw);
+  return launch_dependent(ell_spmv_pipe_kernel<8, XA>, dim3(grid), dim3(kThreads), 0, st, name,
+                          ecol, eval, elen, nrows, ld, x, y, pw);
 }
 
 __global__ void __launch_bounds__(kTileZ * kTileY) stencil7_kernel(
@@ -331,10 +335,12 @@ __global__ void __launch_bounds__(32 * kSTY) stencil7_smem_kernel(
     const double* __restrict__ x, const double* __restrict__ x_lo, const double* __restrict__ x_hi,
     double* __restrict__ y, int64_t nx, int32_t ny, int32_t nz, int32_t xchunk) {
   __shared__ double tile[kSTY + 2][kSTZ + 2];
+  pdl_wait();  // x from the preceding update
   const int64_t xa = static_cast<int64_t>(blockIdx.z) * xchunk;
   const int64_t xb = xa + xchunk < nx ? xa + xchunk : nx;
   if (xa >= xb) return;  // uniform per CTA: no thread reaches a barrier
   stencil7_tile_march(x, x_lo, x_hi, y, nx, ny, nz, xa, xb, tile);
+  pdl_trigger();
 }
 
 // stencil variant: 1 = shared-memory tiles (default), 0 = register march
@@ -403,10 +409,10 @@ KLS_API int kls_stencil7(const double* x, const double* x_lo, const double* x_hi
     const int64_t xc = std::min<int64_t>(env_chunk > 0 ? env_chunk : 32, nx);
     if (!stencil7_grid(nx, ny, nz, xc, grid, kSTZ, kSTY))
       return fail(KLS_EINVAL, "stencil7: grid too large");
-    stencil7_smem_kernel<<<grid, dim3(32, kSTY), 0, static_cast<cudaStream_t>(stream)>>>(
-        x, x_lo, x_hi, y, nx, static_cast<int32_t>(ny), static_cast<int32_t>(nz),
-        static_cast<int32_t>(xc));
-    return check_launch("stencil7_smem_kernel");
+    return launch_dependent(stencil7_smem_kernel, grid, dim3(32, kSTY), 0,
+                            static_cast<cudaStream_t>(stream), "stencil7_smem_kernel", x, x_lo,
+                            x_hi, y, nx, static_cast<int32_t>(ny), static_cast<int32_t>(nz),
+                            static_cast<int32_t>(xc));
   }
   const int64_t xchunk = std::min<int64_t>(env_chunk > 0 ? env_chunk : 16, nx);
   if (!stencil7_grid(nx, ny, nz, xchunk, grid)) return fail(KLS_EINVAL, "stencil7: grid too large");

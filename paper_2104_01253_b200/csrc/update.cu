@@ -104,6 +104,7 @@ template <int RP, int NC>
 __global__ void __launch_bounds__(kThreads, kUpdBlocksPerSm)
     dcgs2_update_kernel(UpdParams p, const __grid_constant__ CoefPack<NC> pk) {
   extern __shared__ double2 sct[];  // (c_k, t_k), padded to a multiple of kCols
+  pdl_wait();  // coefficients from the preceding Gram kernel
   const double* coef = NC > 0 ? pk.v : p.coef;
   const int jpad = (p.j + kCols - 1) / kCols * kCols;
   for (int k = threadIdx.x; k < jpad; k += kThreads)
@@ -124,6 +125,7 @@ __global__ void __launch_bounds__(kThreads, kUpdBlocksPerSm)
     else
       upd_chunk<RP, true>(p, sct, tj, alpha, wbase, lane);
   }
+  pdl_trigger();
 }
 
 // Small-m K2 (m_local <= kUpdSmallRows): one 64-row block per CTA, the 8
@@ -138,6 +140,7 @@ __global__ void __launch_bounds__(kThreads) dcgs2_update_small_kernel(
     UpdParams p, const __grid_constant__ CoefPack<NC> pk) {
   extern __shared__ double2 sct[];  // (c_k, t_k), padded to a multiple of kCols
   __shared__ double2 part[kWarps][2][32];
+  pdl_wait();  // coefficients from the preceding Gram kernel
   const double* coef = NC > 0 ? pk.v : p.coef;
   const int jpad = (p.j + kCols - 1) / kCols * kCols;
   for (int k = threadIdx.x; k < jpad; k += kThreads)
@@ -194,6 +197,7 @@ __global__ void __launch_bounds__(kThreads) dcgs2_update_small_kernel(
     }
     __syncthreads();
   }
+  pdl_trigger();
 }
 
 // TMA-staged K2: a producer warp streams 4-column x 1024-row tiles of Q and
@@ -221,10 +225,6 @@ __global__ void __launch_bounds__(kUThreads, 1)
   double* xbuf = qring + static_cast<size_t>(kUStages) * kCols * kUR;
 
   const double* coef = NC > 0 ? pk.v : p.coef;
-  for (int k = threadIdx.x; k < jpad; k += blockDim.x)
-    sct[k] = k < p.j ? make_double2(coef[k], coef[p.j + k]) : make_double2(0.0, 0.0);
-  const double tj = coef[2 * p.j];
-  const double alpha = p.alpha_dev != nullptr ? *p.alpha_dev : p.alpha;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int ng = (p.j + kCols - 1) / kCols;
@@ -268,6 +268,14 @@ __global__ void __launch_bounds__(kUThreads, 1)
     }
     return;
   }
+  // consumers: the coefficients come from the preceding Gram kernel (PDL);
+  // the producer above streams Q, w and aw meanwhile (none of which it writes)
+  pdl_wait();
+  for (int k = threadIdx.x; k < jpad; k += kWarps * 32)
+    sct[k] = k < p.j ? make_double2(coef[k], coef[p.j + k]) : make_double2(0.0, 0.0);
+  const double tj = coef[2 * p.j];
+  const double alpha = p.alpha_dev != nullptr ? *p.alpha_dev : p.alpha;
+  asm volatile("bar.sync 1, %0;" ::"n"(kWarps * 32) : "memory");
   constexpr int RP = 2;
   const int64_t wrow = warp * (64 * RP);
   double* qout = p.Q + static_cast<int64_t>(p.j) * p.ldq;
@@ -336,6 +344,7 @@ __global__ void __launch_bounds__(kUThreads, 1)
   }
   if (nfull * kUR < p.m && (nfull % gridDim.x) == blockIdx.x)
     upd_chunk<RP, true>(p, sct, tj, alpha, nfull * kUR + wrow, lane);
+  pdl_trigger();
 }
 
 // ---------------------------------------------------------------------------
@@ -480,8 +489,8 @@ int launch_update(const UpdParams& p, const double* host_coef, cudaStream_t st) 
     int rc = set_smem(reinterpret_cast<const void*>(dcgs2_update_small_kernel<NC>), smem);
     if (rc) return rc;
     const int grid = grid_for(p.m, 64, 4);
-    dcgs2_update_small_kernel<NC><<<grid, kThreads, smem, st>>>(p, pk);
-    return check_launch("dcgs2_update_small_kernel");
+    return launch_dependent(dcgs2_update_small_kernel<NC>, dim3(grid), dim3(kThreads), smem, st,
+                            "dcgs2_update_small_kernel", p, pk);
   }
   const int jp = (p.j + kCols - 1) / kCols * kCols;
   const size_t tsmem = 256 + sizeof(double2) * (jp + 1) +
@@ -491,15 +500,15 @@ int launch_update(const UpdParams& p, const double* host_coef, cudaStream_t st) 
     int rc = set_smem(reinterpret_cast<const void*>(dcgs2_update_tma_kernel<NC>), tsmem);
     if (rc) return rc;
     const int grid = static_cast<int>(std::min<int64_t>((p.m + kUR - 1) / kUR, sm_count()));
-    dcgs2_update_tma_kernel<NC><<<grid, kUThreads, tsmem, st>>>(p, pk);
-    return check_launch("dcgs2_update_tma_kernel");
+    return launch_dependent(dcgs2_update_tma_kernel<NC>, dim3(grid), dim3(kUThreads), tsmem, st,
+                            "dcgs2_update_tma_kernel", p, pk);
   }
   const size_t smem = sizeof(double2) * static_cast<size_t>((p.j + kCols - 1) / kCols * kCols + 1);
   int rc = set_smem(reinterpret_cast<const void*>(dcgs2_update_kernel<kUpdRP, NC>), smem);
   if (rc) return rc;
   const int grid = grid_for(p.m, 64 * kUpdRP * kWarps, kUpdBlocksPerSm);
-  dcgs2_update_kernel<kUpdRP, NC><<<grid, kThreads, smem, st>>>(p, pk);
-  return check_launch("dcgs2_update_kernel");
+  return launch_dependent(dcgs2_update_kernel<kUpdRP, NC>, dim3(grid), dim3(kThreads), smem, st,
+                          "dcgs2_update_kernel", p, pk);
 }
 
 int update_common(double* Q, int64_t ldq, int64_t m, int32_t j, double* w, const double* aw,
