@@ -216,6 +216,26 @@ typedef struct {
 int kls_dcgs2_queue_step(const KlsStepPlan* plan, int32_t j, const double* w, double* w_out,
                          const double* x_out, const double* aw, double* aw_out, int32_t slot,
                          int32_t gram);
+typedef struct {
+  const KlsStepPlan* plan;
+  double* w[2];          /* local rows of the two pending-vector buffers */
+  const double* wx[2];   /* their operand addresses for the operator */
+  double* aw[2];         /* their images */
+  const double* gslot[2];/* host views of the mapped result slots (plan->gout) */
+  double* h;             /* C-order Hessenberg buffer, row stride ldh */
+  int64_t ldh;
+  double* k;             /* K: in for step j0, out after the last step (capacity) */
+  double* scratch;       /* 2 * capacity doubles */
+  void* ddot;            /* cblas_ddot / cblas_dgemv for kls_dcgs2_host_step */
+  void* dgemv;
+  int64_t m;             /* global rows (guards) */
+  int32_t capacity;
+} KlsRunState;
+/* Up to nsteps DCGS2 lookahead steps in one call (one GPU): per step
+ * kls_dcgs2_queue_step, a wait on the step's scalars and
+ * kls_dcgs2_host_step; stops at a breakdown.  See plan.cu for io. */
+int kls_dcgs2_run(const KlsRunState* s, int32_t j0, int32_t nsteps, int32_t cur, int32_t slot,
+                  double* io);
 int kls_event_create(void** ev);
 int kls_event_destroy(void* ev);
 int kls_event_record(void* ev, void* stream);

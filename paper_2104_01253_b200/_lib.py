@@ -49,6 +49,7 @@ SIGNATURES = {
     "kls_ell_spmv_peer": (ctypes.c_int, [c_dp, c_dp, c_dp, i32, i64, i64, c_dp, c_dp, i64, c_dp,
                                          c_dp, i64, i64, c_dp, i32, i32, ctypes.c_uint64, c_dp,
                                          c_dp]),
+    "kls_dcgs2_run": (ctypes.c_int, [c_dp, i32, i32, i32, i32, c_dp]),
     "kls_gram_dcgs2": (ctypes.c_int, [c_dp, i64, i64, i32, c_dp, c_dp, c_dp, c_dp, sz, c_dp]),
     "kls_dcgs2_update": (ctypes.c_int, [c_dp, i64, i64, i32, c_dp, c_dp, c_dp, f64, i32, c_dp]),
     "kls_dcgs2_scalars": (ctypes.c_int, [c_dp, i32, i32, c_dp, c_dp, c_dp]),
@@ -108,6 +109,15 @@ class KlsStepPlan(ctypes.Structure):
     _fields_ = [("Q", c_dp), ("ldq", i64), ("m", i64), ("gdev", c_dp), ("cdev", c_dp),
                 ("gout", c_dp * 2), ("ws", c_dp), ("ws_bytes", sz), ("stream", c_dp),
                 ("event", c_dp * 2), ("divide", i32), ("qr", i32), ("op", KlsOpDesc)]
+
+
+class KlsRunState(ctypes.Structure):
+    """include/klsgpu.h KlsRunState (kls_dcgs2_run)."""
+
+    _fields_ = [("plan", ctypes.POINTER(KlsStepPlan)), ("w", c_dp * 2), ("wx", c_dp * 2),
+                ("aw", c_dp * 2), ("gslot", c_dp * 2), ("h", c_dp), ("ldh", i64), ("k", c_dp),
+                ("scratch", c_dp), ("ddot", c_dp), ("dgemv", c_dp), ("m", i64),
+                ("capacity", i32)]
 
 
 OP_ELL, OP_CSR, OP_STENCIL7, OP_DENSE = 1, 2, 3, 4

@@ -14,6 +14,7 @@ Other reference schemes are outside the hot path and
 raise UnknownSchemeError.
 """
 
+import ctypes
 import os
 
 import numpy as np
@@ -412,6 +413,102 @@ class _DelayedArnoldi(_BaseArnoldi):
             self._slot = nxt
         return True
 
+    def run_steps(self, nsteps):
+        """Up to `nsteps` steps; the same results, ledger and exceptions as
+        calling step() that often.  On one GPU with the step plan and the C++
+        host step available the whole lookahead loop runs in one library call
+        (kls_dcgs2_run); otherwise it is the step() loop."""
+        done = 0
+        while done < nsteps and not self.happy:
+            if self.size >= self.capacity:
+                raise DimensionError("expansion capacity exhausted")
+            n = self._run_native(min(nsteps - done, self.capacity - self.size))
+            if n is None:  # not eligible: one regular step
+                if not self.step():
+                    break
+                n = 1
+            done += n
+            if n == 0:
+                break
+        return done
+
+    def _run_native(self, nsteps):
+        e = self.eng
+        blas = _host_blas()
+        if (not self._lookahead or not self._pending or nsteps < 2 or not blas
+                or e.world != 1 or not self._h.flags.c_contiguous):
+            return None
+        plan = e.step_plan()
+        if plan is None:
+            return None
+        j0 = self.nbasis
+        w, aw, w2, aw2 = self._w, self._aw, self._w2, self._aw2
+        if self._ahead is None:
+            e.gram_ahead(j0, w.local, aw, self._slot)
+        cap = self.capacity
+        if getattr(self, "_run", None) is None:
+            st = _lib.KlsRunState()
+            st.plan = ctypes.pointer(plan)
+            st.h, st.ldh = self._h.ctypes.data, self._h.shape[1]
+            self._kbuf = np.zeros(cap)
+            self._scratch = np.zeros(2 * cap)
+            st.k, st.scratch = self._kbuf.ctypes.data, self._scratch.ctypes.data
+            st.ddot, st.dgemv = blas
+            st.m, st.capacity = self.m, cap
+            st.gslot[0], st.gslot[1] = e.slot_np[0].ctypes.data, e.slot_np[1].ctypes.data
+            self._run = st
+        st = self._run
+        st.w[0], st.w[1] = w.local.data_ptr(), w2.local.data_ptr()
+        st.wx[0], st.wx[1] = w.ext_ptr, w2.ext_ptr
+        st.aw[0], st.aw[1] = aw.data_ptr(), aw2.data_ptr()
+        if j0 > 0:
+            self._kbuf[:j0] = self._k
+        io = np.zeros(7)
+        io[0] = self._wscale
+        _lib.call("kls_dcgs2_run", ctypes.byref(st), j0, nsteps, 0, self._slot, io.ctypes.data)
+        done, status, jstop = int(io[2]), int(io[3]), int(io[4])
+        queued = done + (1 if status else 0)
+        _lib.count_launches(3 * queued)  # update, operator, Gram (+ scalar step)
+        m = self.m
+        led = self.ledger
+        js = np.arange(j0, j0 + done, dtype=np.int64)
+        # the ledger of the completed steps (_step_ahead + dcgs2_host_step)
+        led.record_many(_ledger.MV_TRANS_MV, done, int(np.sum(4 * m * (js + 1))))
+        led.record_many(_ledger.MV_TIMES_MAT_ADD_MV, 2 * done,
+                        int(np.sum(2 * m * js) + np.sum(2 * m * (js + 1))))
+        led.add_flops(int(np.sum(4 * js + 2 * (js + 1) * js) + m * done))
+        self.op.napply += done
+        if done:
+            self.nbasis += done
+            jl = j0 + done - 1
+            if jl > 0:
+                self.hcols = jl
+            if self.start_norm is None:
+                self.start_norm = float(io[1])
+            self._wscale = float(io[0])
+            self._k = self._kbuf[: jl + 1].copy()
+            if done % 2:
+                self._w, self._w2 = w2, w
+                self._aw, self._aw2 = aw2, aw
+            nxt = int(io[5])
+            self._ahead = nxt if nxt >= 0 else None
+            if nxt >= 0:
+                self._slot = nxt
+        if status:
+            # the breakdown step: its Gram reduction counted, its speculative
+            # apply discarded (as _step_ahead)
+            led.record(_ledger.MV_TRANS_MV, flops=4 * m * (jstop + 1))
+            self._ahead = None
+            if status == 2:
+                led.add_flops(2 * jstop)
+                raise BreakdownError(f"cancellation in the delayed norm of basis column {jstop}",
+                                     kind="pythagorean", column=jstop)
+            if jstop > 0:
+                self.hcols = jstop
+            self._pending = False
+            self._mark_happy()
+        return done
+
     def _release_w(self):
         for v in (self._w, self._w2):
             rel = getattr(v, "release", None)
@@ -566,7 +663,11 @@ def resume_arnoldi(op, basis, hbar, scheme, capacity, ledger=None, **options):
 def arnoldi_expand(op, start, scheme, steps, ledger=None, **options):
     """Fixed-order expansion; returns (V, Hbar) (arnoldi.py:603-609)."""
     exp = arnoldi(op, start, scheme, capacity=steps + 1, ledger=ledger, **options)
-    while exp.order < steps:
-        if not exp.step():
-            break
+    if hasattr(exp, "run_steps"):
+        while exp.order < steps and not exp.happy:
+            exp.run_steps(steps - exp.order)
+    else:
+        while exp.order < steps:
+            if not exp.step():
+                break
     return exp.finalize()

@@ -68,3 +68,52 @@ KLS_API int kls_dcgs2_queue_step(const KlsStepPlan* p, int32_t j, const double* 
   }
   return rc;
 }
+
+// The lookahead loop itself (arnoldi.py:349-423 per step, _step_ahead's
+// order): per step one queue_step, one wait on the step's scalars, the C++
+// host step; stops after nsteps, at a breakdown, or when the next Gram would
+// not fit the basis.  io: [0] wscale (in/out), [1] alpha of the first
+// completed step, [2] steps completed, [3] status (0 / 1 happy / 2
+// Pythagorean), [4] j of the stopping step, [5] slot of the queued next Gram
+// (-1: none), [6] buffer index of the pending vector.
+KLS_API int kls_dcgs2_run(const KlsRunState* s, int32_t j0, int32_t nsteps, int32_t cur,
+                          int32_t slot, double* io) {
+  if (s == nullptr || io == nullptr || cur < 0 || cur > 1 || slot < 0 || slot > 1)
+    return fail(KLS_EINVAL, "dcgs2_run: bad arguments");
+  double wscale = io[0];
+  double* t_full = s->scratch;
+  double* k_next = s->scratch + s->capacity;
+  double res[2];
+  int32_t done = 0, status = 0, jstop = j0;
+  for (int32_t t = 0; t < nsteps; ++t) {
+    const int32_t j = j0 + t;
+    const int32_t nxt = j + 2 < s->capacity ? 1 - slot : -1;
+    int rc = kls_dcgs2_queue_step(s->plan, j, s->w[cur], s->w[1 - cur], s->wx[1 - cur],
+                                  s->aw[cur], s->aw[1 - cur], nxt >= 0 ? nxt : 0, nxt >= 0);
+    if (rc) return rc;
+    rc = kls_event_sync(s->plan->event[slot]);
+    if (rc) return rc;
+    const int st = kls_dcgs2_host_step(s->gslot[slot], j, s->m, wscale, s->k, s->h, s->ldh,
+                                       t_full, k_next, res, s->ddot, s->dgemv);
+    if (st < 0) return fail(KLS_EINVAL, "dcgs2_run: host step arguments");
+    jstop = j;
+    if (st != 0) {
+      status = st;
+      break;
+    }
+    if (done == 0) io[1] = res[0];
+    for (int32_t i = 0; i <= j; ++i) s->k[i] = k_next[i];
+    wscale = res[1];
+    ++done;
+    cur = 1 - cur;
+    slot = nxt;
+    if (nxt < 0) break;  // no Gram queued for j + 1: the caller finishes
+  }
+  io[0] = wscale;
+  io[2] = done;
+  io[3] = status;
+  io[4] = jstop;
+  io[5] = slot;
+  io[6] = cur;
+  return KLS_OK;
+}

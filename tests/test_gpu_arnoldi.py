@@ -410,3 +410,37 @@ def test_step_plan_bitwise(cuda, which, monkeypatch):
     V2, H2 = K.arnoldi_expand(op, start, "dcgs2", steps=40)
     assert torch.equal(V1, V2) and np.array_equal(H1, H2)
     assert op.napply == 2 * n1
+
+
+@pytest.mark.parametrize("which", ["csr", "stencil", "dense_happy"])
+def test_native_run_matches_step_loop(cuda, which):
+    """run_steps (the whole lookahead loop in kls_dcgs2_run) against the
+    Python step() loop: identical H, V, ledger, napply and breakdown state."""
+    K = kls()
+    if which == "csr":
+        op, steps = mant(30), 60
+    elif which == "stencil":
+        op, steps = K.laplace3d(9, 8, 7), 60
+    else:  # invariant subspace of dimension 5: a happy breakdown mid-run
+        d = np.diag(np.repeat([1.0, 2.0, 3.0, 4.0, 5.0], 40))
+        op, steps = K.DenseOperator(d), 30
+    start = np.random.Generator(np.random.PCG64(17)).standard_normal(op.n)
+    out = []
+    for native in (False, True):
+        led = K.SyncLedger()
+        op.napply = 0
+        exp = K.arnoldi(op, start, "dcgs2", capacity=steps + 1, ledger=led)
+        if native:
+            while exp.order < steps and not exp.happy:
+                exp.run_steps(steps - exp.order)
+        else:
+            while exp.order < steps and exp.step():
+                pass
+        V, H = exp.finalize()
+        out.append((V.clone(), H, led.reductions, led.flops, dict(led.kernel_counts), op.napply,
+                    exp.happy, exp.hcols, exp.start_norm))
+    a, b = out
+    assert torch.equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    assert a[2:] == b[2:]
+    if which == "dense_happy":
+        assert b[6] and b[1].shape[1] == 5
