@@ -285,6 +285,40 @@ int kls_dcgs2_host_step(const double* g, int32_t j, int64_t m, double wscale,
                         const double* k_prev, double* h, int64_t ldh, double* t_full,
                         double* k_next, double* res, void* ddot, void* dgemv);
 
+/* Host real-Schur services for Krylov-Schur restarts (schur.py:84-410) in
+ * C++, bit for bit with the reference's numpy arithmetic when the table
+ * holds numpy's own ILP64 OpenBLAS entry points (cblas_ddot, cblas_dgemv,
+ * cblas_dgemm, dgesv_, dgeqrf_, dorgqr_).  Matrices are C-order n x n. */
+typedef struct KlsHostBlas {
+  void* ddot;
+  void* dgemv;
+  void* dgemm;
+  void* dgesv;
+  void* dgeqrf;
+  void* dorgqr;
+  void* zgemv;     /* cblas_zgemv, cblas_zdotu_sub (eigenvectors) */
+  void* zdotu_sub;
+} KlsHostBlas;
+/* hessenberg_reduce (schur.py:84-114): H in place, U out.  0 / -1. */
+int kls_hessenberg_reduce(double* h, double* u, int64_t n, const KlsHostBlas* blas);
+/* Francis double-shift sweeps + the final 2x2 split pass of
+ * hessenberg_real_schur (schur.py:176-290) on T, accumulating into Z.
+ * 0 ok, 1 sweep limit exceeded (IterationLimitError), -1 bad arguments. */
+int kls_schur_sweeps(double* t, double* z, int64_t n, int64_t max_sweeps,
+                     const KlsHostBlas* blas);
+/* schur_eigenvectors (schur.py:446-487) for the picked blocks: vals
+ * (npick complex, interleaved), vecs (npick rows of zrows complex: Z y). */
+int kls_schur_eigenvectors(const double* t, const double* z, int64_t n, int64_t zrows,
+                           const int64_t* picks, int64_t npick, double* vals, double* vecs,
+                           const KlsHostBlas* blas);
+/* swap_adjacent_blocks (schur.py:305-340): 1 swapped, 0 refused. */
+int kls_schur_swap(double* t, double* z, int64_t n, int64_t i, int32_t p, int32_t q,
+                   const KlsHostBlas* blas);
+/* move_blocks_front (schur.py:378-410): returns the size moved; -1 when nsel
+ * differs from the block count (DimensionError), -2 on other errors. */
+int64_t kls_schur_move_front(double* t, double* z, int64_t n, const uint8_t* selected,
+                             int64_t nsel, const KlsHostBlas* blas);
+
 /* kls_gram_dcgs2 fused with the step's global reduction: the kernel's last
  * CTA performs the one-shot peer exchange itself and writes the rank-ordered
  * global sum of the 2j+3 scalars to out — compute and collective in one

@@ -50,6 +50,11 @@ SIGNATURES = {
                                          c_dp, i64, i64, c_dp, i32, i32, ctypes.c_uint64, c_dp,
                                          c_dp]),
     "kls_dcgs2_run": (ctypes.c_int, [c_dp, i32, i32, i32, i32, c_dp]),
+    "kls_hessenberg_reduce": (ctypes.c_int, [c_dp, c_dp, i64, c_dp]),
+    "kls_schur_sweeps": (ctypes.c_int, [c_dp, c_dp, i64, i64, c_dp]),
+    "kls_schur_swap": (ctypes.c_int, [c_dp, c_dp, i64, i64, i32, i32, c_dp]),
+    "kls_schur_move_front": (i64, [c_dp, c_dp, i64, c_dp, i64, c_dp]),
+    "kls_schur_eigenvectors": (ctypes.c_int, [c_dp, c_dp, i64, i64, c_dp, i64, c_dp, c_dp, c_dp]),
     "kls_gram_dcgs2": (ctypes.c_int, [c_dp, i64, i64, i32, c_dp, c_dp, c_dp, c_dp, sz, c_dp]),
     "kls_dcgs2_update": (ctypes.c_int, [c_dp, i64, i64, i32, c_dp, c_dp, c_dp, f64, i32, c_dp]),
     "kls_dcgs2_scalars": (ctypes.c_int, [c_dp, i32, i32, c_dp, c_dp, c_dp]),
@@ -93,7 +98,9 @@ _NO_LAUNCH = frozenset({"kls_version", "kls_last_error", "kls_device_sm_count", 
                         "kls_lap7_nnz", "kls_mant5_nnz", "kls_ipc_handle_bytes",
                         "kls_peer_buffer_alloc", "kls_peer_buffer_open", "kls_peer_buffer_close",
                         "kls_peer_buffer_free", "kls_dcgs2_host_step", "kls_event_create",
-                        "kls_event_destroy", "kls_event_record", "kls_event_sync"})
+                        "kls_event_destroy", "kls_event_record", "kls_event_sync",
+                        "kls_hessenberg_reduce", "kls_schur_sweeps", "kls_schur_swap",
+                        "kls_schur_move_front", "kls_schur_eigenvectors"})
 
 
 class KlsOpDesc(ctypes.Structure):
@@ -101,6 +108,13 @@ class KlsOpDesc(ctypes.Structure):
 
     _fields_ = [("kind", i32), ("width", i32), ("m", i64), ("n0", i64), ("n1", i64), ("n2", i64),
                 ("p0", c_dp), ("p1", c_dp), ("p2", c_dp)]
+
+
+class KlsHostBlas(ctypes.Structure):
+    """include/klsgpu.h KlsHostBlas: numpy's own BLAS / LAPACK entry points."""
+
+    _fields_ = [("ddot", c_dp), ("dgemv", c_dp), ("dgemm", c_dp), ("dgesv", c_dp),
+                ("dgeqrf", c_dp), ("dorgqr", c_dp), ("zgemv", c_dp), ("zdotu_sub", c_dp)]
 
 
 class KlsStepPlan(ctypes.Structure):
