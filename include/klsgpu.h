@@ -164,6 +164,11 @@ int kls_resid_norms(const double* b, const double* ax, const double* x, int64_t 
  * the Krylov-Schur basis rotation v_mat[:, nlock:k] @ Z (eig.py:237). */
 int kls_tsgemm_inplace(double* V, int64_t ldv, int64_t m, int32_t k, const double* Z,
                        void* stream);
+/* V(:, 0:p) <- V(:, 0:k) Z(:, 0:p) in place, Z k x p column-major on the
+ * device (eig.py:237 keeps the first p columns of V Z).  Register-blocked;
+ * V 16-byte aligned, even ldv. */
+int kls_tsgemm_inplace_cols(double* V, int64_t ldv, int64_t m, int32_t k, int32_t p,
+                            const double* Z, void* stream);
 
 /* ---- device-side operator construction -------------------
  * CSR of a row block [row_lo, row_lo + nrows) built directly in HBM, entry

@@ -78,6 +78,7 @@ SIGNATURES = {
     "kls_sub": (ctypes.c_int, [c_dp, c_dp, c_dp, i64, c_dp]),
     "kls_resid_norms": (ctypes.c_int, [c_dp, c_dp, c_dp, i64, c_dp, c_dp, sz, c_dp]),
     "kls_tsgemm_inplace": (ctypes.c_int, [c_dp, i64, i64, i32, c_dp, c_dp]),
+    "kls_tsgemm_inplace_cols": (ctypes.c_int, [c_dp, i64, i64, i32, i32, c_dp, c_dp]),
     "kls_peer_buffer_bytes": (sz, [i32]),
     "kls_lap7_nnz": (i64, [i64, i64, i64, i64, i64]),
     "kls_build_lap7_csr": (ctypes.c_int, [i64, i64, i64, i64, i64, i64, c_dp, c_dp, c_dp, c_dp]),

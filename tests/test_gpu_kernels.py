@@ -261,6 +261,29 @@ def test_tsgemm_inplace(cuda, rng):
     assert np.allclose(vb[:k, :m].cpu().numpy().T, V @ Z, rtol=1e-12, atol=1e-12)
 
 
+@pytest.mark.parametrize("m,k,p", [(1, 1, 1), (127, 5, 3), (130, 60, 30), (10007, 37, 37),
+                                   (100_003, 60, 33), (4099, 70, 65), (777, 100, 100)])
+def test_tsgemm_inplace_cols(cuda, rng, m, k, p):
+    """Krylov-Schur rotation V(:, :p) <- V(:, :k) Z(:, :p): ragged row tiles,
+    column passes beyond 32, columns p..k-1 untouched; bitwise equal to the
+    sequential fma order over k (the square kernel's order)."""
+    lib, rt = _lib()
+    V = rng.standard_normal((m, k + 1))
+    Z = rng.standard_normal((k, p))
+    vb, ld = _colmajor(V)
+    zd = torch.from_numpy(np.ascontiguousarray(Z.T).ravel()).cuda()  # k x p column-major
+    lib.call("kls_tsgemm_inplace_cols", vb.data_ptr(), ld, m, k, p, zd.data_ptr(),
+             rt.stream_handle())
+    got = vb[: k + 1, :m].cpu().numpy().T
+    ref = V[:, :k] @ Z
+    assert np.allclose(got[:, :p], ref, rtol=1e-12, atol=1e-12 * np.sqrt(k))
+    assert np.array_equal(got[:, p:], V[:, p:])  # untouched columns (and the guard column k)
+    vb2, _ = _colmajor(V)
+    z2 = torch.from_numpy(np.ascontiguousarray(np.pad(Z, ((0, 0), (0, k - p))).T).ravel()).cuda()
+    lib.call("kls_tsgemm_inplace", vb2.data_ptr(), ld, m, k, z2.data_ptr(), rt.stream_handle())
+    assert torch.equal(vb2[:p, :m], vb[:p, :m])  # same fma order as the square entry point
+
+
 def test_resid_norms_and_scale(cuda, rng):
     lib, rt = _lib()
     n = 12345
