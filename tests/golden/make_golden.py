@@ -283,11 +283,40 @@ def mtx_corpus(kls):
         json.dump(corpus, f, indent=1, sort_keys=True)
 
 
+def gmres_config2(kls):
+    """BASELINE config 2 at full size: GMRES(50) with DCGS2 on the 1000 x 1000
+    convection-diffusion operator (ManteuffelSpec(k=1000, beta=0.5), m = 1e6),
+    b = A 1 / ||A 1|| (cli.py:255-257), rtol 1e-6.  ~12 min of reference CPU
+    time; stores the iteration count, the residual history and the
+    cumulative reduction history (small) for the iteration-parity test."""
+    import time
+
+    op = kls.CsrOperator(kls.manteuffel_build(kls.ManteuffelSpec(k=1000, beta=0.5)))
+    one = op.apply(np.ones(op.n))
+    b = one / np.linalg.norm(one)
+    led = kls.SyncLedger()
+    t0 = time.perf_counter()
+    res = kls.gmres_solve(op, b, kls.GmresConfig(max_iters=10000, restart=50, rtol=1e-6,
+                                                 scheme="dcgs2"), ledger=led)
+    out = {"iterations": res.iterations, "converged": res.converged,
+           "residual_history": res.residual_history,
+           "backward_errors": res.backward_errors,
+           "reduction_history": res.reduction_history,
+           "reductions": led.reductions, "cpu_s": time.perf_counter() - t0,
+           "x_sample": res.x[::997]}
+    np.savez_compressed(os.path.join(OUT, "gmres_config2.npz"), **out)
+
+
 if __name__ == "__main__":
     if sys.argv[1:] == ["--only", "mtx"]:
         sys.path.insert(0, REF)
         import kls
 
         mtx_corpus(kls)
+    elif sys.argv[1:] == ["--only", "gmres_config2"]:
+        sys.path.insert(0, REF)
+        import kls
+
+        gmres_config2(kls)
     else:
         main()

@@ -69,3 +69,29 @@ def test_backward_error_exact_solution(cuda):
     x = np.random.Generator(np.random.PCG64(2)).standard_normal(op.n)
     b = op.apply(x).cpu().numpy()
     assert K.backward_error(op, x, b) <= 1e-15
+
+
+def test_gmres_config2_full_size_iteration_parity(cuda):
+    """BASELINE config 2 at full size (m = 1e6 convection-diffusion,
+    GMRES(50), DCGS2, rtol 1e-6): the same iteration count to convergence as
+    the reference's CPU run (tests/golden/make_golden.py --only
+    gmres_config2), residual histories within the reference's paired-curve
+    tolerance, identical cumulative reduction counts."""
+    K = kls()
+    try:
+        g = golden("gmres_config2.npz")
+    except FileNotFoundError:
+        pytest.skip("gmres_config2.npz not generated")
+    op = K.CsrOperator(K.manteuffel_build(K.ManteuffelSpec(k=1000, beta=0.5)))
+    one = op.apply(np.ones(op.n)).cpu().numpy()
+    b = one / np.linalg.norm(one)
+    led = K.SyncLedger()
+    res = K.gmres_solve(op, b, K.GmresConfig(max_iters=10000, restart=50, rtol=1e-6,
+                                             scheme="dcgs2"), ledger=led)
+    assert res.converged == bool(g["converged"])
+    assert res.iterations == int(g["iterations"])
+    ref = g["residual_history"]
+    assert res.residual_history.shape == ref.shape
+    assert np.max(np.abs(res.residual_history - ref)) <= 1e-8
+    assert np.array_equal(res.reduction_history, g["reduction_history"])
+    assert led.reductions == int(g["reductions"])

@@ -284,11 +284,15 @@ def test_tsgemm_inplace_cols(cuda, rng, m, k, p):
     assert torch.equal(vb2[:p, :m], vb[:p, :m])  # same fma order as the square entry point
 
 
-def test_resid_norms_and_scale(cuda, rng):
+@pytest.mark.parametrize("n,off", [(1, 0), (2, 0), (3, 1), (12345, 0), (12345, 1), (1_000_001, 0)])
+def test_resid_norms_and_scale(cuda, rng, n, off):
+    """128-bit path (aligned operands, odd tail) and the scalar path (an
+    operand at an odd element offset)."""
     lib, rt = _lib()
-    n = 12345
     b, ax, x = (rng.standard_normal(n) for _ in range(3))
     bd, axd, xd = (torch.from_numpy(v).cuda() for v in (b, ax, x))
+    if off:
+        axd = torch.cat([torch.zeros(off, dtype=torch.float64, device="cuda"), axd])[off:]
     out = torch.zeros(3, dtype=torch.float64, device="cuda")
     ws, wsb = rt.workspace(4)
     lib.call("kls_resid_norms", bd.data_ptr(), axd.data_ptr(), xd.data_ptr(), n, out.data_ptr(),
