@@ -135,6 +135,119 @@ __global__ void __launch_bounds__(kThreads, 2) gram_small_kernel(GramParams p) {
   gram_epilogue<NX>(p, sacc, stride, ex, xn);
 }
 
+// Latency-bound K1 for the smallest m (config 1, the GMRES / Krylov-Schur
+// tails on one GPU): one CTA per output row — CTA c forms row c of
+// [Q, bext]^T [x0 (, x1)] (or the x_last . x_last slot) over all m rows — so
+// no CTA ever waits on another's partial sums: each output is one CTA's
+// fixed-order tree (4 strided row-pair accumulators per thread, warp
+// butterflies, warps in index order).  The last CTA to finish (ticket) runs
+// the fused DCGS2 scalar step on the staged result.  At m = 1e4 the chunked
+// small kernel spent most of its time in the cross-CTA partial sum.
+constexpr int kColThreads = 512;
+constexpr int64_t kColRows = 1 << 14;  // at or below this m (one GPU) gram_cols_kernel is used
+
+template <int NX>
+__global__ void __launch_bounds__(kColThreads) gram_cols_kernel(GramParams p) {
+  extern __shared__ double sg[];  // staged g (2k + 3) for the scalar step
+  __shared__ double sred[kColThreads / 32][NX];
+  __shared__ bool s_last;
+  pdl_wait();
+  const int c = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool has_b = p.bext != nullptr;
+  const bool norm_row = c >= p.k + (has_b ? 1 : 0);  // the x_last . x_last slot
+  const double* left = c < p.k ? p.Q + static_cast<int64_t>(c) * p.ldq
+                       : has_b && c == p.k ? p.bext
+                                           : (NX == 2 ? p.x1 : p.x0);
+  const double* xs[2] = {norm_row ? left : p.x0, norm_row ? left : p.x1};
+  constexpr int U = 4;
+  double acc[NX][U];
+#pragma unroll
+  for (int t = 0; t < NX; ++t)
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc[t][u] = 0.0;
+  const int nt = norm_row ? 1 : NX;
+  const int64_t npair = p.m / 2;
+  const double2* l2 = reinterpret_cast<const double2*>(left);
+  int64_t i = tid;
+  for (; i + (U - 1) * kColThreads < npair; i += U * kColThreads) {
+    double2 a[U], x[NX][U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) a[u] = l2[i + u * kColThreads];
+#pragma unroll
+    for (int t = 0; t < NX; ++t)
+      if (t < nt)
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          x[t][u] = reinterpret_cast<const double2*>(xs[t])[i + u * kColThreads];
+#pragma unroll
+    for (int t = 0; t < NX; ++t)
+      if (t < nt)
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          acc[t][u] = fma(a[u].x, x[t][u].x, acc[t][u]);
+          acc[t][u] = fma(a[u].y, x[t][u].y, acc[t][u]);
+        }
+  }
+  for (; i < npair; i += kColThreads) {
+    const double2 a = l2[i];
+#pragma unroll
+    for (int t = 0; t < NX; ++t)
+      if (t < nt) {
+        const double2 x = reinterpret_cast<const double2*>(xs[t])[i];
+        acc[t][0] = fma(a.x, x.x, acc[t][0]);
+        acc[t][0] = fma(a.y, x.y, acc[t][0]);
+      }
+  }
+  if ((p.m & 1) && tid == 0) {
+#pragma unroll
+    for (int t = 0; t < NX; ++t)
+      if (t < nt) acc[t][0] = fma(left[p.m - 1], xs[t][p.m - 1], acc[t][0]);
+  }
+#pragma unroll
+  for (int t = 0; t < NX; ++t) {
+    const double v = warp_sum((acc[t][0] + acc[t][1]) + (acc[t][2] + acc[t][3]));
+    if (lane == 0) sred[warp][t] = v;
+  }
+  __syncthreads();
+  if (tid < nt) {
+    double v = 0.0;
+#pragma unroll
+    for (int w = 0; w < kColThreads / 32; ++w) v += sred[w][tid];
+    const int64_t dst = norm_row ? static_cast<int64_t>(NX) * p.out_ld
+                        : c < p.k ? static_cast<int64_t>(tid) * p.out_ld + p.col0 + c
+                                  : static_cast<int64_t>(tid) * p.out_ld + p.bext_row;
+    p.out[dst] = v;
+  }
+  pdl_trigger();
+  if (p.coef == nullptr) return;
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) s_last = atomicAdd(p.ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const int ng = 2 * p.bext_row + 3;
+  for (int k = tid; k < ng; k += kColThreads) sg[k] = __ldcg(p.out + k);
+  __syncthreads();
+  dcgs2_scalars_block(sg, p.bext_row, p.qr, p.coef, p.gout);
+  if (tid == 0) *p.ticket = 0u;
+}
+
+template <int NX>
+int launch_gram_cols(GramParams p, cudaStream_t st) {
+  const int grid = p.k + (p.bext != nullptr ? 1 : 0) + (p.xnorm ? 1 : 0);
+  if (grid == 0) return KLS_OK;  // nothing to reduce (and no scalar step: it needs bext)
+  const size_t smem = p.coef != nullptr ? sizeof(double) * (2 * static_cast<size_t>(p.bext_row) + 3) : 0;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(gram_cols_kernel<NX>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return fail(KLS_ECUDA, "gram_cols: smem attr: %s", cudaGetErrorString(e));
+  }
+  return launch_dependent(gram_cols_kernel<NX>, dim3(grid), dim3(kColThreads), smem, st,
+                          "gram_cols_kernel", p);
+}
+
 constexpr int64_t kSmallRows = 1 << 15;  // at or below this the small-m K1 is used (scripts/small_probe.py)
 constexpr int kRP = 4;                   // row pairs per lane per chunk
 constexpr int kPanel = 1024;             // max Q columns per launch
@@ -178,6 +291,9 @@ int launch_gram_small(GramParams p, size_t ws_bytes, cudaStream_t st) {
 
 template <int NX>
 int launch_gram(GramParams p, size_t ws_bytes, cudaStream_t st) {
+  if (p.m <= kColRows && p.m >= 2 && p.peers.world <= 1 && gram_variant() == 1 &&
+      (p.coef == nullptr || p.bext_row * 2 + 3 <= 2 * kPanel + 3))
+    return launch_gram_cols<NX>(p, st);
   if (p.m <= kSmallRows && p.k > 0 && p.k <= kPanel && gram_variant() != 2)
     return launch_gram_small<NX>(p, ws_bytes, st);
   if (gram_variant() != 0 && tma_eligible(p)) return launch_gram_tma<NX>(p, ws_bytes, st);
