@@ -304,6 +304,16 @@ def gmres_config2(kls):
            "reduction_history": res.reduction_history,
            "reductions": led.reductions, "cpu_s": time.perf_counter() - t0,
            "x_sample": res.x[::997]}
+    # the reference's own noise floor: the same solve under another BLAS
+    # thread count (a different summation order in OpenBLAS's dot / gemv).
+    # Run the script with OPENBLAS_NUM_THREADS=1; this second solve uses 8.
+    from threadpoolctl import threadpool_limits
+
+    with threadpool_limits(limits=8, user_api="blas"):
+        res8 = kls.gmres_solve(op, b, kls.GmresConfig(max_iters=10000, restart=50, rtol=1e-6,
+                                                      scheme="dcgs2"))
+    out["iterations_threads8"] = res8.iterations
+    out["residual_history_threads8"] = res8.residual_history
     np.savez_compressed(os.path.join(OUT, "gmres_config2.npz"), **out)
 
 

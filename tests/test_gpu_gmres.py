@@ -73,10 +73,15 @@ def test_backward_error_exact_solution(cuda):
 
 def test_gmres_config2_full_size_iteration_parity(cuda):
     """BASELINE config 2 at full size (m = 1e6 convection-diffusion,
-    GMRES(50), DCGS2, rtol 1e-6): the same iteration count to convergence as
-    the reference's CPU run (tests/golden/make_golden.py --only
-    gmres_config2), residual histories within the reference's paired-curve
-    tolerance, identical cumulative reduction counts."""
+    GMRES(50), DCGS2, rtol 1e-6, 57 restart cycles): the same iteration
+    count to convergence as the reference's CPU run (tests/golden/
+    make_golden.py --only gmres_config2) and identical cumulative reduction
+    counts.  Residual histories: through the slow phase (cycles < 42) the
+    curves agree to ~1e-14; once convergence accelerates the restarted
+    iteration amplifies rounding and the reference itself moves by up to
+    1.1e-7 (1.7e-3 relative) under a BLAS thread-count change, so each
+    cycle must stay within 1e-8 or 3x the reference's own spread in that
+    cycle, whichever is larger."""
     K = kls()
     try:
         g = golden("gmres_config2.npz")
@@ -92,6 +97,12 @@ def test_gmres_config2_full_size_iteration_parity(cuda):
     assert res.iterations == int(g["iterations"])
     ref = g["residual_history"]
     assert res.residual_history.shape == ref.shape
-    assert np.max(np.abs(res.residual_history - ref)) <= 1e-8
+    assert int(g["iterations_threads8"]) == int(g["iterations"])
+    spread = np.abs(g["residual_history_threads8"] - ref)
+    dev = np.abs(res.residual_history - ref)
+    for c0 in range(0, ref.size, 50):
+        cyc = slice(c0, c0 + 50)
+        assert dev[cyc].max() <= max(1e-8, 3.0 * spread[cyc].max()), c0 // 50
+    assert dev[: 42 * 50].max() <= 1e-12
     assert np.array_equal(res.reduction_history, g["reduction_history"])
     assert led.reductions == int(g["reductions"])
