@@ -291,8 +291,7 @@ int launch_gram_small(GramParams p, size_t ws_bytes, cudaStream_t st) {
 
 template <int NX>
 int launch_gram(GramParams p, size_t ws_bytes, cudaStream_t st) {
-  if (p.m <= kColRows && p.m >= 2 && p.peers.world <= 1 && gram_variant() == 1 &&
-      (p.coef == nullptr || p.bext_row * 2 + 3 <= 2 * kPanel + 3))
+  if (p.m <= kColRows && p.m >= 2 && p.peers.world <= 1 && gram_variant() == 1)
     return launch_gram_cols<NX>(p, st);
   if (p.m <= kSmallRows && p.k > 0 && p.k <= kPanel && gram_variant() != 2)
     return launch_gram_small<NX>(p, ws_bytes, st);

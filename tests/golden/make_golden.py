@@ -317,12 +317,40 @@ def gmres_config2(kls):
     np.savez_compressed(os.path.join(OUT, "gmres_config2.npz"), **out)
 
 
+def ks_config4_shape(kls):
+    """BASELINE config 4's Krylov-Schur settings (nonsymmetric convection-
+    diffusion beta = 0.5, max_basis 60, tol 1e-7, DCGS2, seed 1729) at
+    k = 100 (m = 1e4), 30 restarts: the reference's run (run the script with
+    OPENBLAS_NUM_THREADS=1) and, for its own sensitivity, the same run under
+    8 BLAS threads (a different summation order in OpenBLAS's dot / gemv)."""
+    from threadpoolctl import threadpool_limits
+
+    spec = kls.ManteuffelSpec(k=100, beta=0.5)
+    op = kls.CsrOperator(kls.manteuffel_build(spec))
+    cfg = kls.KrylovSchurConfig(max_basis=60, tol=1e-7, scheme="dcgs2", max_restarts=30)
+    out = {}
+    for tag, nthr in (("", 1), ("alt_", 8)):
+        with threadpool_limits(limits=nthr, user_api="blas"):
+            res = kls.krylov_schur_run(op, cfg, seed=1729)
+        out[f"{tag}values"] = res.values
+        out[f"{tag}lock_history"] = np.array(res.lock_history)
+        out[f"{tag}restarts"] = res.restarts
+        out[f"{tag}invariant_dim"] = res.invariant_dim
+        out[f"{tag}incomplete"] = res.incomplete
+    np.savez_compressed(os.path.join(OUT, "ks_config4_shape.npz"), **out)
+
+
 if __name__ == "__main__":
     if sys.argv[1:] == ["--only", "mtx"]:
         sys.path.insert(0, REF)
         import kls
 
         mtx_corpus(kls)
+    elif sys.argv[1:] == ["--only", "ks_config4_shape"]:
+        sys.path.insert(0, REF)
+        import kls
+
+        ks_config4_shape(kls)
     elif sys.argv[1:] == ["--only", "gmres_config2"]:
         sys.path.insert(0, REF)
         import kls

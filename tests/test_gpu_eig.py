@@ -3,6 +3,7 @@ identical lock histories and restart counts, Ritz values within 1e-9
 relative, locked pairs passing an explicit residual recompute."""
 
 import numpy as np
+import torch
 import pytest
 
 from conftest import golden
@@ -89,3 +90,33 @@ def test_diagonal_and_rotation_operators(cuda, rng):
     got = np.sort_complex(res.values)
     want = np.sort_complex(np.linalg.eigvals(a))
     assert np.max(np.abs(got - want)) <= 1e-8
+
+
+def test_krylov_schur_config4_settings_vs_reference(cuda):
+    """BASELINE config 4's settings (beta = 0.5 convection-diffusion,
+    max_basis 60, tol 1e-7, DCGS2, seed 1729) at m = 1e4, 30 restarts,
+    against the reference's own run: identical lock history, restart count
+    and invariant dimension (stable under the reference's BLAS thread-count
+    change, golden alt_*), and every locked value within 1e-9 relative or 10x
+    the reference's own drift for that value (up to
+    2.4e-7 for the last-locked pair of this pseudospectral problem)."""
+    K = kls()
+    g = golden("ks_config4_shape.npz")
+    assert np.array_equal(g["lock_history"], g["alt_lock_history"])
+    op = K.CsrOperator(K.manteuffel_build(K.ManteuffelSpec(k=100, beta=0.5)))
+    cfg = K.KrylovSchurConfig(max_basis=60, tol=1e-7, scheme="dcgs2", max_restarts=30)
+    res = K.krylov_schur_run(op, cfg, seed=1729)
+    assert list(res.lock_history) == list(g["lock_history"])
+    assert res.restarts == int(g["restarts"])
+    assert res.invariant_dim == int(g["invariant_dim"])
+    assert res.incomplete == bool(g["incomplete"])
+    ref, alt = g["values"], g["alt_values"]
+    assert res.values.shape == ref.shape
+    rel = np.abs(res.values - ref) / np.abs(ref)
+    drift = np.abs(alt - ref) / np.abs(ref)
+    assert np.all(rel <= np.maximum(1e-9, 10.0 * drift))
+    # locked at the reference's criterion (Ritz estimate below tol); an
+    # explicit ||A z - lam z|| is not a meaningful bound here: the locked
+    # values are pseudospectral (eigenvalue condition numbers ~1e10,
+    # PAPER.md:809-823), so their eigenvectors are ill-determined
+    assert np.all(np.asarray(res.residuals) < cfg.tol)
