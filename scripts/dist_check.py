@@ -4,8 +4,9 @@
 
 Row-sharded DCGS2 / CGS2 Arnoldi on the matrix-free stencil and on a CSR
 operator, plus restarted GMRES, compared on rank 0 with the CPU oracle run
-single-process on the same global input.  Prints one JSON line; exit 1 on a
-parity failure.
+single-process on the same global input, and config 3's expansion shape
+against the reference's own run (tests/golden/arnoldi_config3_shape.npz).
+Prints one JSON line; exit 1 on a parity failure.
 """
 
 import json
@@ -16,7 +17,8 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
 
 
 def main():
@@ -49,6 +51,21 @@ def main():
             res[f"stencil_{scheme}_loo"] = loo
             res[f"stencil_{scheme}_reductions"] = [led.reductions, cnt.reductions]
             ok &= err <= 1e-10 and led.reductions == cnt.reductions and loo <= 1e-12
+    # config 3's expansion shape against the reference's own run (golden)
+    g = np.load(os.path.join(ROOT, "tests", "golden", "arnoldi_config3_shape.npz"))
+    start3 = np.random.Generator(np.random.PCG64(1729)).standard_normal(62 * 64 * 64)
+    for scheme in ("dcgs2", "cgs2"):
+        op = kls.laplace3d(62, 64, 64)
+        led = kls.SyncLedger()
+        V, H = kls.arnoldi_expand(op, start3, scheme, steps=100, ledger=led)
+        loo = kls.loss_of_orthogonality(V)
+        ref = g[f"{scheme}_H"]
+        err = float(np.max(np.abs(H - ref)) / np.max(np.abs(ref)))
+        if rank == 0:
+            res[f"config3_shape_{scheme}_relerr"] = err
+            res[f"config3_shape_{scheme}_loo"] = loo
+        ok &= (err <= 1e-10 and led.reductions == int(g[f"{scheme}_reductions"]) and
+               loo <= 10 * max(float(g[f"{scheme}_loo"]), 1e-15))
     # CSR (Manteuffel k=60)
     k = 60
     csr = kls.manteuffel_build(kls.ManteuffelSpec(k=k))

@@ -340,12 +340,48 @@ def ks_config4_shape(kls):
     np.savez_compressed(os.path.join(OUT, "ks_config4_shape.npz"), **out)
 
 
+def arnoldi_config3_shape(kls):
+    """BASELINE config 3's expansion (3-D Poisson 7-point, x slowest, n = 100,
+    start PCG64(1729)) on one GPU's share of the 8-GPU split scaled down:
+    laplace3d(62, 64, 64), m = 253,952.  DCGS2 and CGS2; H, loss of
+    orthogonality, ledger counts, a row sample of V; plus the DCGS2 H under
+    8 BLAS threads (the reference's own summation-order spread)."""
+    from threadpoolctl import threadpool_limits
+
+    op = kls.laplace3d(62, 64, 64)
+    m = op.shape[0]
+    start = np.random.Generator(np.random.PCG64(1729)).standard_normal(m)
+    out = {}
+    for scheme, nthr, tag in (("dcgs2", 1, "dcgs2"), ("cgs2", 1, "cgs2"), ("dcgs2", 8, "dcgs2_t8")):
+        op.napply = 0
+        with threadpool_limits(limits=nthr, user_api="blas"):
+            led = kls.SyncLedger()
+            exp = kls.arnoldi(op, start, scheme, 101, ledger=led)
+            for _ in range(100):
+                exp.step()
+            V, H = exp.finalize()
+        out[f"{tag}_H"] = H
+        if nthr == 1:
+            G = V.T @ V
+            out[f"{tag}_loo"] = np.linalg.norm(np.eye(G.shape[0]) - G)
+            out[f"{tag}_Vrows"] = V[::4999]
+            for k, v in ledger_fields(led).items():
+                out[f"{tag}_{k}"] = v
+            out[f"{tag}_napply"] = op.napply
+    np.savez_compressed(os.path.join(OUT, "arnoldi_config3_shape.npz"), **out)
+
+
 if __name__ == "__main__":
     if sys.argv[1:] == ["--only", "mtx"]:
         sys.path.insert(0, REF)
         import kls
 
         mtx_corpus(kls)
+    elif sys.argv[1:] == ["--only", "arnoldi_config3_shape"]:
+        sys.path.insert(0, REF)
+        import kls
+
+        arnoldi_config3_shape(kls)
     elif sys.argv[1:] == ["--only", "ks_config4_shape"]:
         sys.path.insert(0, REF)
         import kls
