@@ -371,6 +371,41 @@ def arnoldi_config3_shape(kls):
     np.savez_compressed(os.path.join(OUT, "arnoldi_config3_shape.npz"), **out)
 
 
+def _config5_matrix(m, n, seed=2525, density=1e-3):
+    """Config 5's random-sparse tall-skinny shape: each column has
+    round(density * m) N(0, 1) entries at distinct random rows."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    A = np.zeros((m, n))
+    nnz = max(1, int(round(density * m)))
+    for c in range(n):
+        rows = rng.choice(m, size=nnz, replace=False)
+        A[rows, c] = rng.standard_normal(nnz)
+    return A
+
+
+def qr_config5_shape(kls):
+    """DCGS2 / CGS2 QR of config 5's matrix shape at m = 250,000, n = 100
+    (density 1e-3): R, loss of orthogonality, ledger counts and a row sample
+    of Q from the reference; the matrix is regenerated by the test from the
+    same seed (_config5_matrix, copied there)."""
+    from threadpoolctl import threadpool_limits
+
+    A = _config5_matrix(250_000, 100)
+    out = {}
+    for scheme, nthr, tag in (("dcgs2", 1, "dcgs2"), ("cgs2", 1, "cgs2"), ("dcgs2", 8, "dcgs2_t8")):
+        with threadpool_limits(limits=nthr, user_api="blas"):
+            led = kls.SyncLedger()
+            Q, R = kls.qr_factorize(A, scheme, ledger=led)
+        out[f"{tag}_R"] = R
+        if nthr == 1:
+            out[f"{tag}_loo"] = np.linalg.norm(np.eye(Q.shape[1]) - Q.T @ Q)
+            out[f"{tag}_Qrows"] = Q[::4999]
+            for k, v in ledger_fields(led).items():
+                out[f"{tag}_{k}"] = v
+    out["Asum"] = A.sum(axis=0)
+    np.savez_compressed(os.path.join(OUT, "qr_config5_shape.npz"), **out)
+
+
 if __name__ == "__main__":
     if sys.argv[1:] == ["--only", "mtx"]:
         sys.path.insert(0, REF)
@@ -382,6 +417,11 @@ if __name__ == "__main__":
         import kls
 
         arnoldi_config3_shape(kls)
+    elif sys.argv[1:] == ["--only", "qr_config5_shape"]:
+        sys.path.insert(0, REF)
+        import kls
+
+        qr_config5_shape(kls)
     elif sys.argv[1:] == ["--only", "ks_config4_shape"]:
         sys.path.insert(0, REF)
         import kls

@@ -246,6 +246,38 @@ def test_qr_matches_reference(cuda, scheme):
     assert_h_close(R, g[f"kappa_{scheme}_R"])
 
 
+def _config5_matrix(m, n, seed=2525, density=1e-3):
+    """tests/golden/make_golden.py _config5_matrix (same draws)."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    A = np.zeros((m, n))
+    nnz = max(1, int(round(density * m)))
+    for c in range(n):
+        rows = rng.choice(m, size=nnz, replace=False)
+        A[rows, c] = rng.standard_normal(nnz)
+    return A
+
+
+@pytest.mark.parametrize("scheme", ["dcgs2", "cgs2"])
+def test_qr_config5_shape_matches_reference(cuda, scheme):
+    """Config 5's random-sparse tall-skinny QR (density 1e-3) at m = 250,000,
+    n = 100, through the public qr_factorize with host input, against the
+    reference's own run: R within 1e-13 relative normwise (the reference
+    moves 2e-16 between 1 and 8 BLAS threads), Q rows, LOO, ledger."""
+    K = kls()
+    g = golden("qr_config5_shape.npz")
+    A = _config5_matrix(250_000, 100)
+    assert np.array_equal(A.sum(axis=0), g["Asum"])
+    led = K.SyncLedger()
+    Q, R = K.qr_factorize(A, scheme, ledger=led)
+    assert_h_close(R, g[f"{scheme}_R"], rtol=1e-13)
+    assert np.max(np.abs(host(Q)[::4999] - g[f"{scheme}_Qrows"])) <= 1e-12
+    assert K.loss_of_orthogonality(Q) <= 10 * max(float(g[f"{scheme}_loo"]), 1e-15)
+    assert led.reductions == g[f"{scheme}_reductions"]
+    assert led.flops == g[f"{scheme}_flops"]
+    assert led.kernel_counts["MvTransMv"] == g[f"{scheme}_mvtransmv"]
+    assert led.kernel_counts["MvTimesMatAddMv"] == g[f"{scheme}_mvtimes"]
+
+
 def test_qr_hand_worked_step(cuda):
     """tests/test_ortho.py:145-158 / SPEC.md:215: beta=26, c=1, alpha=5."""
     K = kls()
