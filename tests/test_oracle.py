@@ -117,3 +117,18 @@ def test_gmres(case, scheme):
     assert np.array_equal(res["backward_errors"], g[f"{p}_backward_errors"])
     assert np.array_equal(res["reduction_history"], g[f"{p}_reduction_history"])
     assert np.array_equal(res["x"], g[f"{p}_x"])
+
+
+@pytest.mark.parametrize("scheme", ["dcgs2", "cgs2"])
+def test_arnoldi_config3_shape(scheme):
+    """The oracle at config 3's expansion shape (laplace3d(62, 64, 64),
+    m = 253,952, n = 100) against the reference's own run: H within 1e-13
+    normwise (the BLAS thread count here may differ from the golden's)."""
+    g = golden("arnoldi_config3_shape.npz")
+    dims = (62, 64, 64)
+    start = np.random.Generator(np.random.PCG64(1729)).standard_normal(int(np.prod(dims)))
+    V, H, cnt = getattr(oracle, f"{scheme}_arnoldi")(
+        lambda x: oracle.stencil7_matvec(x, dims), start, 100)
+    ref = g[f"{scheme}_H"]
+    assert np.max(np.abs(H - ref)) <= 1e-13 * np.max(np.abs(ref))
+    assert cnt.reductions == g[f"{scheme}_reductions"]
