@@ -14,4 +14,18 @@ kls.gmres_solve(mop, rng.standard_normal(mop.n), kls.GmresConfig(max_iters=30, r
 kls.qr_factorize(rng.standard_normal((3001, 9)), "dcgs2")
 kls.krylov_schur_run(kls.CsrOperator(kls.manteuffel_build(kls.ManteuffelSpec(k=6))),
                      kls.KrylovSchurConfig(max_basis=12, scheme="dcgs2", max_restarts=3), seed=1)
+# Krylov-Schur rotation kernel: ragged row tile, two column passes
+import torch
+from paper_2104_01253_b200 import _lib, runtime
+m, k, p = 1001, 40, 35
+ld = runtime.pad_rows(m)
+V = torch.randn((k + 1, ld), dtype=torch.float64, device="cuda")
+Z = torch.randn(k * p, dtype=torch.float64, device="cuda")
+_lib.call("kls_tsgemm_inplace_cols", V.data_ptr(), ld, m, k, p, Z.data_ptr(), runtime.stream_handle())
+# host Schur services (C++) on a 40 x 40 problem
+from paper_2104_01253_b200 import schur
+f = schur.hessenberg_real_schur(schur.hessenberg_reduce(rng.standard_normal((40, 40)))[0])
+schur.move_blocks_front(f, [i % 3 == 0 for i in range(len(f.blocks()))])
+schur.schur_eigenvectors(f)
+torch.cuda.synchronize()
 print("sanitize run ok")
