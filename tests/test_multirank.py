@@ -1,6 +1,6 @@
 """The row-sharded (N > 1) host logic on CPU with the gloo backend, world
-size 2 and 3: row partition, the CSR halo exchange plan, the one allreduce
-per DCGS2 step, and the replicated host step math — driving numpy stand-ins
+size 2, 3 and 8 (the driver's largest run): row partition, the CSR halo
+exchange plan, the one allreduce per DCGS2 step, and the replicated host step math — driving numpy stand-ins
 for the device kernels (test scaffolding only) — reproduce the oracle's
 single-process Hessenberg matrix and reduction count."""
 
@@ -107,7 +107,7 @@ def _worker(rank, world, port, k, steps, out):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world", [2, 3, 8])
 def test_sharded_dcgs2_matches_oracle(world):
     k, steps = 12, 16
     mgr = mp.Manager()
@@ -135,7 +135,7 @@ def test_halo_plan_symmetry():
     from paper_2104_01253_b200.problems import halo_plan
 
     rng = np.random.default_rng(0)
-    for world in (2, 3, 5):
+    for world in (2, 3, 5, 8):
         bounds = np.sort(rng.choice(np.arange(1, 100), size=world - 1, replace=False))
         edges = [0, *bounds.tolist(), 100]
         wins = []
