@@ -61,9 +61,10 @@ def dims_of(s):
     return tuple(int(v) for v in s.split(","))
 
 
-def workload_name(dims, n, scheme):
+def workload_name(dims, n, scheme, operator="stencil"):
     m = dims[0] * dims[1] * dims[2]
-    return f"{scheme} Arnoldi-QR, laplace3d{dims} matrix-free 7-point, m={m}, n={n}"
+    form = "matrix-free 7-point" if operator == "stencil" else "7-point as CSR"
+    return f"{scheme} Arnoldi-QR, laplace3d{dims} {form}, m={m}, n={n}"
 
 
 # ---------------------------------------------------------------------------
@@ -129,7 +130,7 @@ def run_reference(args):
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic: PCG64(1729) standard-normal start vector",
-        "config": {"workload": workload_name(dims, args.n, args.scheme), "m": m, "n": args.n,
+        "config": {"workload": workload_name(dims, args.n, args.scheme, args.operator), "m": m, "n": args.n,
                    "sample_rows": ms, "sample_dims": list(sdims),
                    "extrapolation": "iters/s at the sample size x (sample rows / m)"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
@@ -388,7 +389,7 @@ def run_ours(args):
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic: PCG64(1729) standard-normal start vector, matrix-free 3-D Poisson",
-        "config": {"workload": workload_name(dims, args.n, args.scheme), "m": m, "n": args.n,
+        "config": {"workload": workload_name(dims, args.n, args.scheme, args.operator), "m": m, "n": args.n,
                    "scheme": args.scheme,
                    "operator": ("laplace3d 7-point, matrix-free" if args.operator == "stencil"
                                 else "laplace3d 7-point as device-assembled CSR (int32 cols)"),

@@ -212,16 +212,28 @@ struct EllRow {
   double v[W];
 };
 
+// The entry loads are predicated on the stored width (uniform, known up
+// front), not on the row's length: padding slots hold (0, 0.0), and
+// predicating on elen would make every row's loads wait for its elen byte
+// (one more dependent memory latency per row: 5.9 -> 6.6 TB/s at m = 1.3e8).
+// The row length still bounds the arithmetic (numpy's reduceat order).
+// W is the stored width itself for widths 4..8 (no predicates, no spills),
+// else the next instantiated size with slots >= width predicated off.
 template <int W>
 __device__ __forceinline__ void ell_fetch(EllRow<W>& r, const int32_t* ecol, const double* eval,
-                                          const uint8_t* elen, int64_t ld, int64_t i) {
+                                          const uint8_t* elen, int64_t ld, int64_t i, int width) {
   r.n = ld_na_u8(elen + i);
 #pragma unroll
   for (int k = 0; k < W; ++k) {
-    r.c[k] = k < r.n ? ld_na_s32(ecol + k * ld + i) : 0;
-    r.v[k] = k < r.n ? ld_na_f64(eval + k * ld + i) : 0.0;
+    r.c[k] = k < width ? ld_na_s32(ecol + k * ld + i) : 0;
+    r.v[k] = k < width ? ld_na_f64(eval + k * ld + i) : 0.0;
   }
 }
+
+// resident CTAs per SM of the pipelined kernel: two rows of W entries in
+// registers must fit the 64K-register file without spilling
+template <int W>
+constexpr int ell_blocks() { return W >= 7 ? 3 : kEllBlocks; }
 
 // x accessors of the pipelined ELL product: the rank's window as one array,
 // or (peer) as three — column c of [lo halo | own rows | hi halo] lives at
@@ -255,10 +267,10 @@ struct PeerWait {
 };
 
 template <int W, typename XA>
-__global__ void __launch_bounds__(kThreads, kEllBlocks) ell_spmv_pipe_kernel(
+__global__ void __launch_bounds__(kThreads, ell_blocks<W>()) ell_spmv_pipe_kernel(
     const int32_t* __restrict__ ecol, const double* __restrict__ eval,
     const uint8_t* __restrict__ elen, int64_t nrows, int64_t ld, XA x,
-    double* __restrict__ y, PeerWait pw) {
+    double* __restrict__ y, PeerWait pw, int width) {
   pdl_wait();  // x from the preceding update
   if (pw.flag_lo != nullptr || pw.flag_hi != nullptr) {
     __shared__ int s_ok;
@@ -276,12 +288,12 @@ __global__ void __launch_bounds__(kThreads, kEllBlocks) ell_spmv_pipe_kernel(
   int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= nrows) return;
   EllRow<W> cur;
-  ell_fetch<W>(cur, ecol, eval, elen, ld, i);
+  ell_fetch<W>(cur, ecol, eval, elen, ld, i, width);
   while (true) {
     const int64_t nx = i + stride;
     EllRow<W> nxt;
     nxt.n = 0;
-    if (nx < nrows) ell_fetch<W>(nxt, ecol, eval, elen, ld, nx);
+    if (nx < nrows) ell_fetch<W>(nxt, ecol, eval, elen, ld, nx, width);
     double p[W];
 #pragma unroll
     for (int k = 0; k < W; ++k) p[k] = k < cur.n ? __dmul_rn(cur.v[k], x(cur.c[k])) : 0.0;
@@ -307,20 +319,25 @@ int grid_1d(int64_t n, int per_sm) {
   return g < 1 ? 1 : g;
 }
 
+template <int W, typename XA>
+int launch_ell_w(const int32_t* ecol, const double* eval, const uint8_t* elen, int32_t width,
+                 int64_t nrows, int64_t ld, XA x, double* y, PeerWait pw, cudaStream_t st) {
+  // one wave of resident CTAs; each thread walks its rows with a one-row lookahead
+  const int grid = grid_1d(nrows, ell_blocks<W>());
+  return launch_dependent(ell_spmv_pipe_kernel<W, XA>, dim3(grid), dim3(kThreads), 0, st,
+                          "ell_spmv_pipe_kernel", ecol, eval, elen, nrows, ld, x, y, pw, width);
+}
+
 template <typename XA>
 int launch_ell_pipe(const int32_t* ecol, const double* eval, const uint8_t* elen, int32_t width,
                     int64_t nrows, int64_t ld, XA x, double* y, PeerWait pw, cudaStream_t st) {
-  // one wave of resident CTAs; each thread walks its rows with a one-row lookahead
-  const int grid = grid_1d(nrows, kEllBlocks);
-  const char* name = "ell_spmv_pipe_kernel";
-  if (width <= 4)
-    return launch_dependent(ell_spmv_pipe_kernel<4, XA>, dim3(grid), dim3(kThreads), 0, st, name,
-                            ecol, eval, elen, nrows, ld, x, y, pw);
-  if (width <= 6)
-    return launch_dependent(ell_spmv_pipe_kernel<6, XA>, dim3(grid), dim3(kThreads), 0, st, name,
-                            ecol, eval, elen, nrows, ld, x, y, pw);
-  return launch_dependent(ell_spmv_pipe_kernel<8, XA>, dim3(grid), dim3(kThreads), 0, st, name,
-                          ecol, eval, elen, nrows, ld, x, y, pw);
+  switch (width) {
+    case 5: return launch_ell_w<5>(ecol, eval, elen, width, nrows, ld, x, y, pw, st);
+    case 6: return launch_ell_w<6>(ecol, eval, elen, width, nrows, ld, x, y, pw, st);
+    case 7: return launch_ell_w<7>(ecol, eval, elen, width, nrows, ld, x, y, pw, st);
+    case 8: return launch_ell_w<8>(ecol, eval, elen, width, nrows, ld, x, y, pw, st);
+    default: return launch_ell_w<4>(ecol, eval, elen, width, nrows, ld, x, y, pw, st);  // 1..4
+  }
 }
 
 __global__ void __launch_bounds__(kTileZ * kTileY) stencil7_kernel(
