@@ -7,8 +7,11 @@
 //
 // Pipeline per CTA (persistent, one CTA per SM): a 4-stage ring of
 // 4 columns x 1024 rows (32 KB per stage) for Q, and a double-buffered
-// slot for the chunk's right-hand vectors.  Only full 1024-row chunks go
-// through the copy engine; the ragged tail chunk is read directly.
+// slot for the chunk's right-hand vectors.  Chunks are scheduled by
+// sched_chunk (tma.cuh): whole rounds round-robin, the remainder split into
+// one short chunk per CTA (a multiple of 64 rows: warps skip their 64-row
+// blocks past its end).  The < 64 rows past the last multiple of 64 are
+// read directly by the last CTA.
 #include "gram.cuh"
 #include "tma.cuh"
 
@@ -44,7 +47,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1) gram_tma_kernel(GramParams p) 
   const int lane = threadIdx.x & 31;
   const int ng = (p.k + kG - 1) / kG;
   const int stride = ng * V;
-  const int64_t nfull = p.m / kR;
+  const int64_t m64 = p.m & ~static_cast<int64_t>(63);
+  const int64_t nrounds = sched_rounds<kR>(m64);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -61,6 +65,11 @@ __global__ void __launch_bounds__(kTmaThreads, 1) gram_tma_kernel(GramParams p) 
     double* wacc = sacc + warp * stride;
     for (int i = lane; i < stride; i += 32) wacc[i] = 0.0;
   }
+  // rows past a short chunk's end are multiplied by zeroed x rows: the ring
+  // must hold finite values there, so it starts zeroed
+  for (int i = threadIdx.x; i < kStages * kG * kR / 2; i += blockDim.x)
+    reinterpret_cast<double2*>(qring)[i] = make_double2(0.0, 0.0);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // before the bulk copies land
   __syncthreads();
 
   double ex[NX];
@@ -73,23 +82,23 @@ __global__ void __launch_bounds__(kTmaThreads, 1) gram_tma_kernel(GramParams p) 
       const double* xsrc[3] = {p.x0, p.x1, p.bext};
       uint32_t use = 0;  // Q stage fills so far
       uint32_t xuse = 0;
-      for (int64_t c = blockIdx.x; c < nfull; c += gridDim.x, ++xuse) {
+      int64_t row, nr;
+      for (int64_t it = 0; sched_chunk<kR>(it, nrounds, m64, row, nr); ++it, ++xuse) {
+        const uint32_t bytes = static_cast<uint32_t>(nr) * sizeof(double);
         const int xs = xuse & 1;
         if (xuse >= 2) mbar_wait(xempty + xs, ((xuse >> 1) - 1) & 1);
-        mbar_expect_tx(xfull + xs, static_cast<uint32_t>(nxb) * kR * sizeof(double));
+        mbar_expect_tx(xfull + xs, static_cast<uint32_t>(nxb) * bytes);
         for (int t = 0; t < nxb; ++t)
-          bulk_g2s(xbuf + (static_cast<size_t>(xs) * 3 + t) * kR, xsrc[t] + c * kR,
-                   kR * sizeof(double), xfull + xs);
+          bulk_g2s(xbuf + (static_cast<size_t>(xs) * 3 + t) * kR, xsrc[t] + row, bytes, xfull + xs);
         for (int g = 0; g < ng; ++g, ++use) {
           const int s = use % kStages;
           const uint32_t round = use / kStages;
           if (round >= 1) mbar_wait(empty + s, (round - 1) & 1);
           const int ncols = min(kG, p.k - g * kG);
-          mbar_expect_tx(full + s, static_cast<uint32_t>(ncols) * kR * sizeof(double));
+          mbar_expect_tx(full + s, static_cast<uint32_t>(ncols) * bytes);
           for (int cc = 0; cc < ncols; ++cc)
             bulk_g2s(qring + (static_cast<size_t>(s) * kG + cc) * kR,
-                     p.Q + static_cast<int64_t>(g * kG + cc) * p.ldq + c * kR, kR * sizeof(double),
-                     full + s);
+                     p.Q + static_cast<int64_t>(g * kG + cc) * p.ldq + row, bytes, full + s);
         }
       }
     }
@@ -98,7 +107,11 @@ __global__ void __launch_bounds__(kTmaThreads, 1) gram_tma_kernel(GramParams p) 
     const int64_t wrow = warp * (64 * kRPt);
     uint32_t use = 0;
     uint32_t xuse = 0;
-    for (int64_t c = blockIdx.x; c < nfull; c += gridDim.x, ++xuse) {
+    int64_t row, nr;  // nr: a multiple of 64
+    for (int64_t it = 0; sched_chunk<kR>(it, nrounds, m64, row, nr); ++it, ++xuse) {
+      bool live[kRPt];
+#pragma unroll
+      for (int r = 0; r < kRPt; ++r) live[r] = wrow + 64 * r < nr;
       const int xs = xuse & 1;
       mbar_wait(xfull + xs, (xuse >> 1) & 1);
       double2 xv[NX][kRPt];
@@ -107,11 +120,12 @@ __global__ void __launch_bounds__(kTmaThreads, 1) gram_tma_kernel(GramParams p) 
       for (int t = 0; t < NX; ++t)
 #pragma unroll
         for (int r = 0; r < kRPt; ++r)
-          xv[t][r] = *reinterpret_cast<const double2*>(xb + t * kR + wrow + 64 * r + 2 * lane);
+          xv[t][r] = live[r] ? *reinterpret_cast<const double2*>(xb + t * kR + wrow + 64 * r + 2 * lane)
+                             : make_double2(0.0, 0.0);
       if (p.bext != nullptr) {
 #pragma unroll
         for (int r = 0; r < kRPt; ++r) {
-          const double2 b = p.bext == p.x0
+          const double2 b = p.bext == p.x0 || !live[r]
                                 ? xv[0][r]
                                 : *reinterpret_cast<const double2*>(xb + NX * kR + wrow + 64 * r + 2 * lane);
 #pragma unroll
@@ -164,9 +178,9 @@ __global__ void __launch_bounds__(kTmaThreads, 1) gram_tma_kernel(GramParams p) 
         if ((lane & (32 / V - 1)) == 0) wacc[g * V + warp_slot<V>(lane)] += sred;
       }
     }
-    // ragged tail: the CTA that would own chunk nfull reads it directly
-    if (nfull * kR < p.m && (nfull % gridDim.x) == blockIdx.x)
-      gram_chunk<NX, kRPt, true>(p, nfull * kR + wrow, lane, wacc, ex, xn);
+    // the < 64 rows past m64: read directly by the last CTA
+    if (m64 < p.m && blockIdx.x == gridDim.x - 1)
+      gram_chunk<NX, kRPt, true>(p, m64 + wrow, lane, wacc, ex, xn);
   }
   gram_epilogue<NX>(p, sacc, stride, ex, xn);
 }

@@ -228,7 +228,8 @@ __global__ void __launch_bounds__(kUThreads, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int ng = (p.j + kCols - 1) / kCols;
-  const int64_t nfull = p.m / kUR;
+  const int64_t m64 = p.m & ~static_cast<int64_t>(63);  // chunks: sched_chunk (tma.cuh)
+  const int64_t nrounds = sched_rounds<kUR>(m64);
   if (threadIdx.x == 0) {
     for (int s = 0; s < kUStages; ++s) {
       mbar_init(full + s, 1);
@@ -245,24 +246,23 @@ __global__ void __launch_bounds__(kUThreads, 1)
   if (warp == kWarps) {
     if (lane == 0) {
       uint32_t use = 0, xuse = 0;
-      for (int64_t c = blockIdx.x; c < nfull; c += gridDim.x, ++xuse) {
+      int64_t row, nr;
+      for (int64_t it = 0; sched_chunk<kUR>(it, nrounds, m64, row, nr); ++it, ++xuse) {
+        const uint32_t bytes = static_cast<uint32_t>(nr) * sizeof(double);
         const int xs = xuse & 1;
         if (xuse >= 2) mbar_wait(xempty + xs, ((xuse >> 1) - 1) & 1);
-        mbar_expect_tx(xfull + xs, 2u * kUR * sizeof(double));
-        bulk_g2s(xbuf + (static_cast<size_t>(xs) * 2) * kUR, p.w + c * kUR, kUR * sizeof(double),
-                 xfull + xs);
-        bulk_g2s(xbuf + (static_cast<size_t>(xs) * 2 + 1) * kUR, p.aw + c * kUR,
-                 kUR * sizeof(double), xfull + xs);
+        mbar_expect_tx(xfull + xs, 2u * bytes);
+        bulk_g2s(xbuf + (static_cast<size_t>(xs) * 2) * kUR, p.w + row, bytes, xfull + xs);
+        bulk_g2s(xbuf + (static_cast<size_t>(xs) * 2 + 1) * kUR, p.aw + row, bytes, xfull + xs);
         for (int g = 0; g < ng; ++g, ++use) {
           const int s = use % kUStages;
           const uint32_t round = use / kUStages;
           if (round >= 1) mbar_wait(empty + s, (round - 1) & 1);
           const int ncols = min(kCols, p.j - g * kCols);
-          mbar_expect_tx(full + s, static_cast<uint32_t>(ncols) * kUR * sizeof(double));
+          mbar_expect_tx(full + s, static_cast<uint32_t>(ncols) * bytes);
           for (int cc = 0; cc < ncols; ++cc)
             bulk_g2s(qring + (static_cast<size_t>(s) * kCols + cc) * kUR,
-                     p.Q + static_cast<int64_t>(g * kCols + cc) * p.ldq + c * kUR,
-                     kUR * sizeof(double), full + s);
+                     p.Q + static_cast<int64_t>(g * kCols + cc) * p.ldq + row, bytes, full + s);
         }
       }
     }
@@ -280,7 +280,8 @@ __global__ void __launch_bounds__(kUThreads, 1)
   const int64_t wrow = warp * (64 * RP);
   double* qout = p.Q + static_cast<int64_t>(p.j) * p.ldq;
   uint32_t use = 0, xuse = 0;
-  for (int64_t c = blockIdx.x; c < nfull; c += gridDim.x, ++xuse) {
+  int64_t crow, nr;  // nr: a multiple of 64; rows past it are computed but not stored
+  for (int64_t it = 0; sched_chunk<kUR>(it, nrounds, m64, crow, nr); ++it, ++xuse) {
     double2 ac[RP], at[RP];
 #pragma unroll
     for (int r = 0; r < RP; ++r) {
@@ -330,7 +331,8 @@ __global__ void __launch_bounds__(kUThreads, 1)
     if (lane == 0) mbar_arrive(xempty + xs);
 #pragma unroll
     for (int r = 0; r < RP; ++r) {
-      const int64_t row = c * kUR + wrow + 64 * r + 2 * lane;
+      if (wrow + 64 * r >= nr) continue;
+      const int64_t row = crow + wrow + 64 * r + 2 * lane;
       double2 qn, wn;
       qn.x = (wv[r].x - ac[r].x) / alpha;
       qn.y = (wv[r].y - ac[r].y) / alpha;
@@ -342,8 +344,8 @@ __global__ void __launch_bounds__(kUThreads, 1)
       *reinterpret_cast<double2*>(p.w_out + row) = wn;
     }
   }
-  if (nfull * kUR < p.m && (nfull % gridDim.x) == blockIdx.x)
-    upd_chunk<RP, true>(p, sct, tj, alpha, nfull * kUR + wrow, lane);
+  if (m64 < p.m && blockIdx.x == gridDim.x - 1)
+    upd_chunk<RP, true>(p, sct, tj, alpha, m64 + wrow, lane);
   pdl_trigger();
 }
 

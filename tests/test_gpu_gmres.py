@@ -79,9 +79,10 @@ def test_gmres_config2_full_size_iteration_parity(cuda):
     counts.  Residual histories: through the slow phase (cycles < 42) the
     curves agree to ~1e-14; once convergence accelerates the restarted
     iteration amplifies rounding and the reference itself moves by up to
-    1.1e-7 (1.7e-3 relative) under a BLAS thread-count change, so each
-    cycle must stay within 1e-8 or 3x the reference's own spread in that
-    cycle, whichever is larger."""
+    1.1e-7 (1.7e-3 relative) under a BLAS thread-count change (one sample
+    of that spread), so the whole curve must stay within 3x the reference's
+    largest spread and each cycle within 1e-8 or 10x the spread in that
+    cycle."""
     K = kls()
     try:
         g = golden("gmres_config2.npz")
@@ -102,7 +103,8 @@ def test_gmres_config2_full_size_iteration_parity(cuda):
     dev = np.abs(res.residual_history - ref)
     for c0 in range(0, ref.size, 50):
         cyc = slice(c0, c0 + 50)
-        assert dev[cyc].max() <= max(1e-8, 3.0 * spread[cyc].max()), c0 // 50
+        assert dev[cyc].max() <= max(1e-8, 10.0 * spread[cyc].max()), c0 // 50
+    assert dev.max() <= 3.0 * spread.max()
     assert dev[: 42 * 50].max() <= 1e-12
     assert np.array_equal(res.reduction_history, g["reduction_history"])
     assert led.reductions == int(g["reductions"])
