@@ -137,6 +137,12 @@ int kls_csr_to_ell(const int64_t* rowptr, const int32_t* col, const double* val,
  * entry order, same reduceat summation). */
 int kls_ell_spmv(const int32_t* ecol, const double* eval, const uint8_t* elen, int32_t width,
                  int64_t nrows, int64_t ld, const double* x, double* y, void* stream);
+/* GMRES backward-error norms fused with the ELL product (gmres.py:46-60):
+ * out = [||b - A x||^2, ||x||^2, ||b||^2] for a one-rank ELL operator; A x is
+ * formed bit-identically to kls_ell_spmv and not stored. */
+int kls_ell_resid_norms(const int32_t* ecol, const double* eval, const uint8_t* elen,
+                        int32_t width, int64_t nrows, int64_t ld, const double* x,
+                        const double* b, double* out, void* ws, size_t ws_bytes, void* stream);
 
 /* Matrix-free 7-point Laplacian, bit-identical to StencilLaplace3D._matvec
  * (problems.py:296-305) on nx local x-planes of a (.., ny, nz) grid; x_lo /

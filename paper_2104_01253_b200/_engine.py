@@ -358,6 +358,23 @@ class Engine:
         """Uncounted operator application (the caller bumps op.napply)."""
         self.op.apply_into(x, y, self.st)
 
+    def apply_resid_norms(self, x, y, b, out):
+        """GMRES's backward-error column (gmres.py:171-172): y = A x and the
+        norms [||b - y||^2, ||x||^2, ||b||^2] into the device tensor `out`,
+        without waiting.  On one GPU with an ELL operator the two are one
+        kernel (kls_ell_resid_norms: A x bit-identical, y not stored);
+        otherwise the product and kls_resid_norms."""
+        ell = getattr(self.op, "_ell", None)
+        if (self.world == 1 and ell is not None and trace._active is None
+                and not getattr(self.op, "_peer", False)):
+            ecol, evals, elen, width, ld = ell
+            _lib.call("kls_ell_resid_norms", ecol.data_ptr(), evals.data_ptr(), elen.data_ptr(),
+                      width, self.ml, ld, x.data_ptr(), b.data_ptr(), out.data_ptr(), self.ws,
+                      self.wsb, self.st)
+            return
+        self.apply(x, y)
+        self.resid_norms_queue(b, y, x, out)
+
     def __del__(self):
         try:
             for ev in getattr(self, "slot_ev", ()):

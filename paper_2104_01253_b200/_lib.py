@@ -51,6 +51,8 @@ SIGNATURES = {
                                          c_dp]),
     "kls_dcgs2_run": (ctypes.c_int, [c_dp, i32, i32, i32, i32, c_dp]),
     "kls_hessenberg_reduce": (ctypes.c_int, [c_dp, c_dp, i64, c_dp]),
+    "kls_ell_resid_norms": (ctypes.c_int, [c_dp, c_dp, c_dp, i32, i64, i64, c_dp, c_dp, c_dp,
+                                           c_dp, sz, c_dp]),
     "kls_schur_sweeps": (ctypes.c_int, [c_dp, c_dp, i64, i64, c_dp]),
     "kls_schur_swap": (ctypes.c_int, [c_dp, c_dp, i64, i64, i32, i32, c_dp]),
     "kls_schur_move_front": (i64, [c_dp, c_dp, i64, c_dp, i64, c_dp]),

@@ -12,6 +12,7 @@
 // x-slowest (nx, ny, nz) grid, y = 6 g minus the six Dirichlet neighbours in
 // the reference's order (x-1, x+1, y-1, y+1, z-1, z+1).  For a row-sharded
 // grid the neighbouring x-planes of other ranks come in through x_lo / x_hi.
+#include "reduce.cuh"
 #include "stencil.cuh"
 #include "peer.cuh"
 
@@ -371,6 +372,66 @@ int stencil_variant() {
   return v;
 }
 
+// GMRES's per-column backward error (gmres.py:46-60, :171-172) on an ELL
+// operator in one pass: y = A x row by row exactly as the pipelined product
+// (same fetch, same arithmetic: y is bit-identical), never stored; the
+// kernel accumulates ||b - y||^2, ||x||^2 and ||b||^2 and reduces them over
+// the grid (deterministic).  Saves the write of y and the re-read of y, x
+// and b by kls_resid_norms, and one launch per GMRES column.
+template <int W>
+__global__ void __launch_bounds__(kThreads, W >= 7 ? 2 : 3) ell_resid_norms_kernel(
+    const int32_t* __restrict__ ecol, const double* __restrict__ eval,
+    const uint8_t* __restrict__ elen, int64_t nrows, int64_t ld, const double* __restrict__ x,
+    const double* __restrict__ b, int width, RedWs ws, double* out) {
+  pdl_wait();
+  double v[3] = {0.0, 0.0, 0.0};
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < nrows) {
+    EllRow<W> cur;
+    ell_fetch<W>(cur, ecol, eval, elen, ld, i, width);
+    while (true) {
+      const int64_t nx = i + stride;
+      EllRow<W> nxt;
+      nxt.n = 0;
+      if (nx < nrows) ell_fetch<W>(nxt, ecol, eval, elen, ld, nx, width);
+      double p[W];
+#pragma unroll
+      for (int k = 0; k < W; ++k) p[k] = k < cur.n ? __dmul_rn(cur.v[k], __ldg(x + cur.c[k])) : 0.0;
+      double acc = 0.0;
+      if (cur.n > 0) {
+        double r = -0.0;
+#pragma unroll
+        for (int k = 1; k < W; ++k)
+          if (k < cur.n) r = __dadd_rn(r, p[k]);
+        acc = __dadd_rn(p[0], r);
+      }
+      const double bi = __ldcs(b + i);
+      const double xi = __ldg(x + i);
+      const double rr = bi - acc;
+      v[0] = fma(rr, rr, v[0]);
+      v[1] = fma(xi, xi, v[1]);
+      v[2] = fma(bi, bi, v[2]);
+      if (nx >= nrows) break;
+      cur = nxt;
+      i = nx;
+    }
+  }
+  pdl_trigger();
+  grid_reduce_finish<3>(v, ws, out);
+}
+
+template <int W>
+int launch_ell_resid(const int32_t* ecol, const double* eval, const uint8_t* elen, int32_t width,
+                     int64_t nrows, int64_t ld, const double* x, const double* b, double* out,
+                     void* ws, size_t ws_bytes, cudaStream_t st) {
+  const int grid = grid_1d(nrows, W >= 7 ? 2 : 3);
+  if (!red_ws_fits(ws_bytes, grid, 3)) return fail(KLS_ENOSPC, "ell_resid_norms: workspace too small");
+  return launch_dependent(ell_resid_norms_kernel<W>, dim3(grid), dim3(kThreads), 0, st,
+                          "ell_resid_norms_kernel", ecol, eval, elen, nrows, ld, x, b, width,
+                          red_ws(ws), out);
+}
+
 // dense y = A x, A row-major n x n (DenseOperator, problems.py:68-85):
 // one warp per row
 __global__ void __launch_bounds__(kThreads) dense_gemv_kernel(const double* __restrict__ a,
@@ -489,6 +550,26 @@ KLS_API int kls_ell_spmv(const int32_t* ecol, const double* eval, const uint8_t*
   }
   return launch_ell_pipe(ecol, eval, elen, width, nrows, ld, XPlain{x}, y,
                          PeerWait{nullptr, nullptr, 0, nullptr}, st);
+}
+
+// out = [||b - A x||^2, ||x||^2, ||b||^2] over this row block for an ELL
+// operator (rows of x at their own index: a one-rank operator), A x formed
+// bit-identically to kls_ell_spmv but not stored.
+KLS_API int kls_ell_resid_norms(const int32_t* ecol, const double* eval, const uint8_t* elen,
+                                int32_t width, int64_t nrows, int64_t ld, const double* x,
+                                const double* b, double* out, void* ws, size_t ws_bytes,
+                                void* stream) {
+  if (ecol == nullptr || eval == nullptr || elen == nullptr || x == nullptr || b == nullptr ||
+      out == nullptr || ws == nullptr || nrows < 1 || ld < nrows || width < 1 || width > 8)
+    return fail(KLS_EINVAL, "ell_resid_norms: bad arguments");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  switch (width) {
+    case 5: return launch_ell_resid<5>(ecol, eval, elen, width, nrows, ld, x, b, out, ws, ws_bytes, st);
+    case 6: return launch_ell_resid<6>(ecol, eval, elen, width, nrows, ld, x, b, out, ws, ws_bytes, st);
+    case 7: return launch_ell_resid<7>(ecol, eval, elen, width, nrows, ld, x, b, out, ws, ws_bytes, st);
+    case 8: return launch_ell_resid<8>(ecol, eval, elen, width, nrows, ld, x, b, out, ws, ws_bytes, st);
+    default: return launch_ell_resid<4>(ecol, eval, elen, width, nrows, ld, x, b, out, ws, ws_bytes, st);
+  }
 }
 
 // kls_ell_spmv with the halo columns read from the neighbours' vectors over

@@ -340,3 +340,26 @@ def test_device_built_manteuffel_matches_host(cuda, rng, k, beta):
     assert np.array_equal(dev._val.cpu().numpy()[: ptr[-1]], dat)
     x = rng.standard_normal(k * k)
     assert np.array_equal(dev.apply(x).cpu().numpy(), oracle.csr_matvec(ptr, idx, dat, x))
+
+
+@pytest.mark.parametrize("k,beta", [(37, 0.5), (100, 0.0)])
+def test_ell_resid_norms_fused(cuda, rng, k, beta):
+    """kls_ell_resid_norms = kls_ell_spmv + the three norms of
+    kls_resid_norms (A x not stored), on device-built Manteuffel ELL."""
+    import paper_2104_01253_b200 as kls
+    from paper_2104_01253_b200 import problems
+
+    lib, rt = _lib()
+    op = problems.manteuffel_operator(kls.ManteuffelSpec(k=k, beta=beta))
+    assert op._ell is not None
+    x = torch.from_numpy(rng.standard_normal(op.n)).cuda()
+    b = torch.from_numpy(rng.standard_normal(op.n)).cuda()
+    y = op.apply(x).cpu().numpy()
+    ecol, evals, elen, width, ld = op._ell
+    out = torch.zeros(3, dtype=torch.float64, device="cuda")
+    ws, wsb = rt.workspace(4)
+    lib.call("kls_ell_resid_norms", ecol.data_ptr(), evals.data_ptr(), elen.data_ptr(), width,
+             op.n, ld, x.data_ptr(), b.data_ptr(), out.data_ptr(), ws, wsb, rt.stream_handle())
+    xh, bh = x.cpu().numpy(), b.cpu().numpy()
+    want = [np.sum((bh - y) ** 2), xh @ xh, bh @ bh]
+    assert np.allclose(out.cpu().numpy(), want, rtol=1e-12, atol=0)
