@@ -8,7 +8,7 @@
 // Pipeline per CTA (persistent, one CTA per SM): a 4-stage ring of
 // 4 columns x 1024 rows (32 KB per stage) for Q, and a double-buffered
 // slot for the chunk's right-hand vectors.  Chunks are scheduled by
-// sched_chunk (tma.cuh): whole rounds round-robin, the remainder split into
+// ChunkWalk (tma.cuh): whole rounds round-robin, the remainder split into
 // one short chunk per CTA (a multiple of 64 rows: warps skip their 64-row
 // blocks past its end).  The < 64 rows past the last multiple of 64 are
 // read directly by the last CTA.
@@ -48,7 +48,6 @@ __global__ void __launch_bounds__(kTmaThreads, 1) gram_tma_kernel(GramParams p) 
   const int ng = (p.k + kG - 1) / kG;
   const int stride = ng * V;
   const int64_t m64 = p.m & ~static_cast<int64_t>(63);
-  const int64_t nrounds = sched_rounds<kR>(m64);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -83,7 +82,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) gram_tma_kernel(GramParams p) 
       uint32_t use = 0;  // Q stage fills so far
       uint32_t xuse = 0;
       int64_t row, nr;
-      for (int64_t it = 0; sched_chunk<kR>(it, nrounds, m64, row, nr); ++it, ++xuse) {
+      for (ChunkWalk<kR> cw(m64); cw.next(row, nr); ++xuse) {
         const uint32_t bytes = static_cast<uint32_t>(nr) * sizeof(double);
         const int xs = xuse & 1;
         if (xuse >= 2) mbar_wait(xempty + xs, ((xuse >> 1) - 1) & 1);
@@ -108,7 +107,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) gram_tma_kernel(GramParams p) 
     uint32_t use = 0;
     uint32_t xuse = 0;
     int64_t row, nr;  // nr: a multiple of 64
-    for (int64_t it = 0; sched_chunk<kR>(it, nrounds, m64, row, nr); ++it, ++xuse) {
+    for (ChunkWalk<kR> cw(m64); cw.next(row, nr); ++xuse) {
       bool live[kRPt];
 #pragma unroll
       for (int r = 0; r < kRPt; ++r) live[r] = wrow + 64 * r < nr;

@@ -49,39 +49,51 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // short chunk per CTA) rather than dealt as whole chunks to some CTAs while
 // the others idle: at m = 1e6 (977 chunks) K1 / K2 at j = 50 take 73 / 65 us
 // instead of 77 / 72.  At many rounds the split gains nothing, so it is not
-// used there (the schedule is then the plain round-robin one).  Returns
-// false past the CTA's last chunk; nr is a multiple of 64.
+// used there (the schedule is then the plain round-robin one).
 constexpr int64_t kBalanceRounds = 16;
 
-// q: sched_rounds<R>(m64), computed once per kernel (a 64-bit division)
+// The schedule as an incremental walk (per chunk: one add and one compare on
+// the producer's critical path): round-robin chunks [row, row + R) with row
+// stepping by grid * R up to rr_end, then at most one short balanced chunk.
 template <int R>
-__device__ __forceinline__ int64_t sched_rounds(int64_t m64) {
-  return m64 / R / gridDim.x;
-}
+struct ChunkWalk {
+  int64_t row, step, rr_end, tail_row, tail_nr;
 
-template <int R>
-__device__ __forceinline__ bool sched_chunk(int64_t it, int64_t q, int64_t m64, int64_t& row,
-                                            int64_t& nr) {
-  const int64_t grid = gridDim.x, b = blockIdx.x;
-  if (q >= kBalanceRounds) {
-    const int64_t c = it * grid + b;
-    row = c * R;
-    if (row >= m64) return false;
-    nr = m64 - row < R ? m64 - row : R;
-    return true;
+  __device__ __forceinline__ explicit ChunkWalk(int64_t m64) {
+    const int64_t grid = gridDim.x, b = blockIdx.x;
+    const int64_t q = m64 / R / grid;  // whole rounds
+    step = grid * R;
+    row = b * R;
+    if (q >= kBalanceRounds) {
+      rr_end = m64;  // plain round-robin; the last chunk may be short
+      tail_nr = 0;
+      tail_row = 0;
+    } else {
+      rr_end = q * step;
+      const int64_t per = ((m64 - rr_end) / 64 + grid - 1) / grid * 64;
+      tail_row = rr_end + b * per;
+      const int64_t left = m64 - tail_row;
+      tail_nr = left < per ? (left > 0 ? left : 0) : per;
+    }
   }
-  if (it < q) {
-    row = (it * grid + b) * R;
-    nr = R;
-    return true;
+
+  // next chunk: start row r and rows nr (a multiple of 64); false when done
+  __device__ __forceinline__ bool next(int64_t& r, int64_t& nr) {
+    if (row < rr_end) {
+      r = row;
+      nr = rr_end - row < R ? rr_end - row : R;
+      row += step;
+      return true;
+    }
+    if (tail_nr > 0) {
+      r = tail_row;
+      nr = tail_nr;
+      tail_nr = 0;
+      return true;
+    }
+    return false;
   }
-  if (it > q) return false;
-  const int64_t base = q * grid * R;
-  const int64_t per = ((m64 - base) / 64 + grid - 1) / grid * 64;
-  row = base + b * per;
-  nr = m64 - row < per ? m64 - row : per;
-  return nr > 0;
-}
+};
 
 }  // namespace tma
 }  // namespace kls

@@ -228,8 +228,7 @@ __global__ void __launch_bounds__(kUThreads, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int ng = (p.j + kCols - 1) / kCols;
-  const int64_t m64 = p.m & ~static_cast<int64_t>(63);  // chunks: sched_chunk (tma.cuh)
-  const int64_t nrounds = sched_rounds<kUR>(m64);
+  const int64_t m64 = p.m & ~static_cast<int64_t>(63);  // chunks: ChunkWalk (tma.cuh)
   if (threadIdx.x == 0) {
     for (int s = 0; s < kUStages; ++s) {
       mbar_init(full + s, 1);
@@ -247,7 +246,7 @@ __global__ void __launch_bounds__(kUThreads, 1)
     if (lane == 0) {
       uint32_t use = 0, xuse = 0;
       int64_t row, nr;
-      for (int64_t it = 0; sched_chunk<kUR>(it, nrounds, m64, row, nr); ++it, ++xuse) {
+      for (ChunkWalk<kUR> cw(m64); cw.next(row, nr); ++xuse) {
         const uint32_t bytes = static_cast<uint32_t>(nr) * sizeof(double);
         const int xs = xuse & 1;
         if (xuse >= 2) mbar_wait(xempty + xs, ((xuse >> 1) - 1) & 1);
@@ -281,7 +280,7 @@ __global__ void __launch_bounds__(kUThreads, 1)
   double* qout = p.Q + static_cast<int64_t>(p.j) * p.ldq;
   uint32_t use = 0, xuse = 0;
   int64_t crow, nr;  // nr: a multiple of 64; rows past it are computed but not stored
-  for (int64_t it = 0; sched_chunk<kUR>(it, nrounds, m64, crow, nr); ++it, ++xuse) {
+  for (ChunkWalk<kUR> cw(m64); cw.next(crow, nr); ++xuse) {
     double2 ac[RP], at[RP];
 #pragma unroll
     for (int r = 0; r < RP; ++r) {
