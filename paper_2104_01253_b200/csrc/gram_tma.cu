@@ -65,10 +65,13 @@ __global__ void __launch_bounds__(kTmaThreads, 1) gram_tma_kernel(GramParams p) 
     for (int i = lane; i < stride; i += 32) wacc[i] = 0.0;
   }
   // rows past a short chunk's end are multiplied by zeroed x rows: the ring
-  // must hold finite values there, so it starts zeroed
-  for (int i = threadIdx.x; i < kStages * kG * kR / 2; i += blockDim.x)
-    reinterpret_cast<double2*>(qring)[i] = make_double2(0.0, 0.0);
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // before the bulk copies land
+  // must hold finite values there, so it starts zeroed when short chunks
+  // can occur (balanced last round, or m64 not a multiple of the chunk)
+  if (m64 / kR / gridDim.x < kBalanceRounds || (m64 % kR) != 0) {
+    for (int i = threadIdx.x; i < kStages * kG * kR / 2; i += blockDim.x)
+      reinterpret_cast<double2*>(qring)[i] = make_double2(0.0, 0.0);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // before the bulk copies land
+  }
   __syncthreads();
 
   double ex[NX];
