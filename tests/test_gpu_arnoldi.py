@@ -97,8 +97,9 @@ def test_config1_poisson100(cuda, scheme):
     assert led.reductions == g[f"{scheme}_reductions"]
 
 
-@pytest.mark.parametrize("scheme", ["dcgs2", "cgs2"])
-def test_config3_shape_matches_reference(cuda, scheme):
+@pytest.mark.parametrize("scheme,operator", [("dcgs2", "stencil"), ("cgs2", "stencil"),
+                                             ("dcgs2", "csr")])
+def test_config3_shape_matches_reference(cuda, scheme, operator):
     """Config 3's expansion (3-D Poisson 7-point, x slowest, n = 100, start
     PCG64(1729)) at laplace3d(62, 64, 64), m = 253,952, against the
     reference's own run: H within 1e-10 relative normwise (the north star;
@@ -106,7 +107,8 @@ def test_config3_shape_matches_reference(cuda, scheme):
     of orthogonality of the same order, identical ledger and napply."""
     K = kls()
     g = golden("arnoldi_config3_shape.npz")
-    op = K.laplace3d(62, 64, 64)
+    # the matrix-free stencil or the device-assembled CSR (ELL) form
+    op = K.laplace3d(62, 64, 64) if operator == "stencil" else K.laplace3d_csr_operator(62, 64, 64)
     start = np.random.Generator(np.random.PCG64(1729)).standard_normal(op.n)
     led = K.SyncLedger()
     exp = K.arnoldi(op, start, scheme, 101, ledger=led)
