@@ -5,7 +5,8 @@
 Row-sharded DCGS2 / CGS2 Arnoldi on the matrix-free stencil and on a CSR
 operator, plus restarted GMRES, compared on rank 0 with the CPU oracle run
 single-process on the same global input, and config 3's expansion shape
-against the reference's own run (tests/golden/arnoldi_config3_shape.npz).
+and config 2 at full size against the reference's own runs
+(tests/golden/arnoldi_config3_shape.npz, gmres_config2.npz).
 Prints one JSON line; exit 1 on a parity failure.
 """
 
@@ -115,6 +116,25 @@ def main():
         dev = float(np.max(dh)) if g.iterations == r["iterations"] else float("inf")
         res["gmres_hist_maxdiff"] = dev
         ok &= g.iterations == r["iterations"] and dev <= 1e-8
+    # config 2 at full size (m = 1e6, GMRES(50), rtol 1e-6) row-sharded,
+    # against the reference's own run (tests/golden/gmres_config2.npz)
+    g2 = np.load(os.path.join(ROOT, "tests", "golden", "gmres_config2.npz"))
+    ptr2, idx2, dat2 = oracle.manteuffel_csr(1000, 0.5)
+    one2 = oracle.csr_matvec(ptr2, idx2, dat2, np.ones(1000 * 1000))
+    b2 = one2 / np.linalg.norm(one2)
+    op2 = kls.manteuffel_operator(kls.ManteuffelSpec(k=1000, beta=0.5))
+    led2 = kls.SyncLedger()
+    gm = kls.gmres_solve(op2, b2, kls.GmresConfig(max_iters=10000, restart=50, rtol=1e-6,
+                                                  scheme="dcgs2"), ledger=led2)
+    ref2 = g2["residual_history"]
+    spread2 = np.abs(g2["residual_history_threads8"] - ref2)
+    same_len = gm.residual_history.shape == ref2.shape
+    dev2 = float(np.max(np.abs(gm.residual_history - ref2))) if same_len else float("inf")
+    if rank == 0:
+        res["config2_iterations"] = [gm.iterations, int(g2["iterations"])]
+        res["config2_hist_maxdiff"] = dev2
+    ok &= (gm.iterations == int(g2["iterations"]) and led2.reductions == int(g2["reductions"])
+           and dev2 <= 3.0 * float(spread2.max()))
     # DCGS2 / CGS2 QR of a row-sharded tall-skinny matrix (config 5's kernel)
     A = np.random.Generator(np.random.PCG64(21)).standard_normal((50_021, 24))
     for scheme in ("dcgs2", "cgs2"):
