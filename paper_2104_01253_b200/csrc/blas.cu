@@ -132,12 +132,19 @@ __global__ void __launch_bounds__(kThreads) tsgemm_kernel(double* __restrict__ V
 // 2 loads per FMA (~13x slower at m = 1e7, k = 60).
 constexpr int kRotRows = 128;
 
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(src_bytes)
+               : "memory");
+}
+
 __global__ void __launch_bounds__(kThreads, 2)
     rotate_kernel(double* __restrict__ V, int64_t ldv, int64_t m, int32_t k, int32_t p,
-                  const double* __restrict__ Z, int32_t zp) {
+                  const double* __restrict__ Z, int32_t zp, int32_t dbuf) {
   extern __shared__ __align__(16) double smr[];
   double* zs = smr;                                   // [k][zp]
-  double* tile = smr + static_cast<size_t>(k) * zp;   // [k][kRotRows]
+  double* const tile0 = smr + static_cast<size_t>(k) * zp;  // [k][kRotRows], x2 when dbuf
+  double* const tile1 = tile0 + static_cast<size_t>(k) * kRotRows;
   for (int i = threadIdx.x; i < k * zp; i += kThreads) {
     const int r = i / zp, c = i % zp;
     zs[i] = c < p ? Z[static_cast<int64_t>(c) * k + r] : 0.0;
@@ -146,23 +153,34 @@ __global__ void __launch_bounds__(kThreads, 2)
   const int lane = threadIdx.x & 31;
   const int64_t ntiles = (m + kRotRows - 1) / kRotRows;
   const int npass = (p + 31) / 32;
-  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+  // tile t's k columns into buf with 16-byte cp.async (rows past m zero-filled)
+  auto load_tile = [&](int64_t t, double* buf) {
     const int64_t row0 = t * kRotRows;
-    const bool full = row0 + kRotRows <= m;
-    __syncthreads();  // previous tile's readers are done (and Z is staged)
     for (int i = threadIdx.x; i < k * (kRotRows / 2); i += kThreads) {
       const int c = i / (kRotRows / 2), r2 = 2 * (i % (kRotRows / 2));
-      const double* src = V + static_cast<int64_t>(c) * ldv + row0 + r2;
-      double2 v;
-      if (full) {
-        v = __ldcs(reinterpret_cast<const double2*>(src));
-      } else {
-        v.x = row0 + r2 < m ? src[0] : 0.0;
-        v.y = row0 + r2 + 1 < m ? src[1] : 0.0;
-      }
-      *reinterpret_cast<double2*>(tile + c * kRotRows + r2) = v;
+      const int64_t row = row0 + r2;
+      const double* col = V + static_cast<int64_t>(c) * ldv;
+      const int bytes = row + 2 <= m ? 16 : (row < m ? 8 : 0);
+      cp_async16(buf + c * kRotRows + r2, bytes ? col + row : col, bytes);
     }
-    __syncthreads();
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  int it = 0;
+  if (static_cast<int64_t>(blockIdx.x) < ntiles) load_tile(blockIdx.x, tile0);
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+    const int64_t row0 = t * kRotRows;
+    const bool full = row0 + kRotRows <= m;
+    double* tile = (dbuf && (it & 1)) ? tile1 : tile0;
+    const int64_t tn = t + gridDim.x;
+    if (dbuf && tn < ntiles) {
+      // the next tile streams in while this one is multiplied (in place is
+      // safe: the tiles are disjoint rows, each owned by one CTA)
+      load_tile(tn, (it & 1) ? tile0 : tile1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();  // the tile (and Z) are staged
     for (int pass = 0; pass < npass; ++pass) {
       const int cb = pass * 32 + 4 * warp;
       if (cb >= p) continue;
@@ -193,11 +211,14 @@ __global__ void __launch_bounds__(kThreads, 2)
           if (full || row0 + lane + 32 * r < m) dst[lane + 32 * r] = acc[r][c];
       }
     }
+    __syncthreads();  // this tile's readers are done before it is refilled
+    if (!dbuf && tn < ntiles) load_tile(tn, tile0);
   }
 }
 
-size_t rotate_smem(int k, int zp) {
-  return sizeof(double) * (static_cast<size_t>(k) * zp + static_cast<size_t>(k) * kRotRows);
+size_t rotate_smem(int k, int zp, int nbuf) {
+  return sizeof(double) *
+         (static_cast<size_t>(k) * zp + static_cast<size_t>(nbuf) * k * kRotRows);
 }
 
 }  // namespace
@@ -212,7 +233,8 @@ KLS_API int kls_tsgemm_inplace_cols(double* V, int64_t ldv, int64_t m, int32_t k
     return fail(KLS_EINVAL, "tsgemm_inplace_cols: bad arguments");
   if (m == 0 || k == 0 || p == 0) return KLS_OK;
   const int zp = ((p + 31) / 32) * 32;
-  const size_t smem = rotate_smem(k, zp);
+  const int dbuf = rotate_smem(k, zp, 2) <= 227 * 1024 ? 1 : 0;  // double-buffered tiles when they fit
+  const size_t smem = rotate_smem(k, zp, dbuf ? 2 : 1);
   if ((reinterpret_cast<uintptr_t>(V) & 15) != 0 || (ldv & 1) != 0 || smem > 227 * 1024)
     return fail(KLS_EINVAL, "tsgemm_inplace_cols: V must be 16-byte aligned with even ldv, k <= %d",
                 static_cast<int>((227 * 1024 / sizeof(double)) / (kRotRows + zp)));
@@ -223,7 +245,7 @@ KLS_API int kls_tsgemm_inplace_cols(double* V, int64_t ldv, int64_t m, int32_t k
   const int per_sm = smem <= 110 * 1024 ? 2 : 1;
   const int grid = static_cast<int>(std::min<int64_t>(ntiles, (int64_t)per_sm * sm_count()));
   rotate_kernel<<<grid, kThreads, smem, static_cast<cudaStream_t>(stream)>>>(V, ldv, m, k, p, Z,
-                                                                            zp);
+                                                                            zp, dbuf);
   return check_launch("rotate_kernel");
 }
 
@@ -268,7 +290,7 @@ KLS_API int kls_tsgemm_inplace(double* V, int64_t ldv, int64_t m, int32_t k, con
     return fail(KLS_EINVAL, "tsgemm_inplace: bad arguments");
   if (m == 0 || k == 0) return KLS_OK;
   if ((reinterpret_cast<uintptr_t>(V) & 15) == 0 && (ldv & 1) == 0 &&
-      rotate_smem(k, ((k + 31) / 32) * 32) <= 227 * 1024)
+      rotate_smem(k, ((k + 31) / 32) * 32, 1) <= 227 * 1024)
     return kls_tsgemm_inplace_cols(V, ldv, m, k, k, Z, stream);
   size_t smem = sizeof(double) * (size_t)k * kTileRows;
   int z_in_smem = 0;
