@@ -14,8 +14,9 @@
  * Layout: a basis block Q is column-major with leading dimension ldq (even;
  * the Python host pads it to a multiple of 32 doubles).  Vectors are fp64
  * arrays of m rows, 16-byte aligned.  Reductions are deterministic (fixed
- * summation order, no fp64 atomics); results are bitwise reproducible for a
- * fixed device.
+ * summation order, no fp64 atomics) AND independent of the number of ranks
+ * the rows are split over: they follow the fixed segment tree of KlsSegs
+ * below, so 1, 2, 3, 4, 6 or 8 GPUs give bitwise-identical results.
  *
  * Each declaration cites the reference interface it replaces
  * (/root/reference/pkg/src/kls/<file>:<line>).
@@ -49,8 +50,36 @@ int kls_host_device_ptr(void* host, void** dev);
 
 /* Bytes of reduction workspace that cover any call with <= kmax basis
  * columns on the current device.  Zero it once before first use; every
- * reducing kernel leaves its ticket at zero again. */
+ * reducing kernel leaves its tickets at zero again. */
 size_t kls_workspace_bytes(int64_t m, int32_t kmax);
+
+/* ---- rank-count-independent reductions -----------------------------------
+ * The global rows [0, m) are cut into 24 segments at multiples of `unit`
+ * rows (64 for CSR / dense / QR blocks, a stencil's x-plane — even); rank r
+ * of `world` (1 <= world <= 24) owns segments [r*24/world, (r+1)*24/world)
+ * and therefore rows kls_seg_rows(); its local m must equal that range.
+ * Every reduction sums segments over one fixed tree, so its result does not
+ * depend on world.  With world > 1 a reduction that is not fused with a
+ * peer exchange writes this rank's EXPORTED tree nodes instead of the
+ * result: out[e * xstride + o] for its e-th exported node (<= 8 nodes;
+ * xstride = the call's output count unless stated), which
+ * kls_peer_seg_combine or (after an all_gather) kls_seg_combine turn into
+ * the global values.  NULL KlsSegs = one rank holding all m rows, unit 64.
+ * The reference has one process and numpy sums (kernels.py:44-60); this is
+ * the layout its MPI_Allreduce becomes here. */
+typedef struct KlsSegs {
+  int64_t m;     /* global rows */
+  int64_t unit;  /* partition unit (rows, even) */
+  int32_t world; /* ranks */
+  int32_t rank;  /* this rank */
+} KlsSegs;
+/* This rank's global rows [lo, hi). */
+int kls_seg_rows(const KlsSegs* s, int64_t* lo, int64_t* hi);
+/* The tree nodes rank exports, left to right (ids[<= 8]); returns the count. */
+int kls_seg_exports(int32_t rank, int32_t world, int32_t* ids);
+/* blocks = [world][8][stride] gathered export blocks -> out[0:nout]. */
+int kls_seg_combine(const double* blocks, int32_t nout, int64_t stride, int32_t world, double* out,
+                    void* stream);
 
 /* Fused block inner products — kernels.mv_trans_mv (kernels.py:44-60):
  *   out = [Q(:, 0:k), bext]^T [x0 (, x1)]      column-major,
@@ -60,7 +89,7 @@ size_t kls_workspace_bytes(int64_t m, int32_t kmax);
  * basis block still reduces, kernels.py:5-9).  One pass over Q. */
 int kls_mv_trans_mv(const double* Q, int64_t ldq, int64_t m, int32_t k, const double* bext,
                     const double* x0, const double* x1, int32_t nx, int32_t xnorm, double* out,
-                    void* ws, size_t ws_bytes, void* stream);
+                    const KlsSegs* segs, void* ws, size_t ws_bytes, void* stream);
 
 /* The single fused reduction of a DCGS2 Arnoldi step — replaces
  *   g = mv_trans_mv(np.hstack([Q, w]), np.column_stack([w, aw]))
@@ -70,7 +99,8 @@ int kls_mv_trans_mv(const double* Q, int64_t ldq, int64_t m, int32_t k, const do
  *   out[2j+2]  = aw.aw
  * 2j+3 doubles: the payload of the one allreduce per step. */
 int kls_gram_dcgs2(const double* Q, int64_t ldq, int64_t m, int32_t j, const double* w,
-                   const double* aw, double* out, void* ws, size_t ws_bytes, void* stream);
+                   const double* aw, double* out, const KlsSegs* segs, void* ws, size_t ws_bytes,
+                   void* stream);
 
 /* Fused DCGS2 update — the two MvTimesMatAddMv of a step
  * (arnoldi.py:389-391 and 415-420; QR form ortho.py:371-375, 396-398):
@@ -105,12 +135,13 @@ int kls_dcgs2_update_dev(double* Q, int64_t ldq, int64_t m, int32_t j, const dou
  * the norm2 that follows a projection (ortho.py:153-154, arnoldi.py:433-434). */
 int kls_mv_times_mat_add_mv(double* Y, int64_t ldy, int64_t m, int32_t l, const double* B,
                             int64_t ldb, int32_t k, const double* S, double sign, double scale,
-                            double* nrm_out, void* ws, size_t ws_bytes, void* stream);
+                            double* nrm_out, const KlsSegs* segs, void* ws, size_t ws_bytes,
+                            void* stream);
 /* Same with S in HOST memory (k*l <= 2048), carried in the launch. */
 int kls_mv_times_mat_add_mv_host(double* Y, int64_t ldy, int64_t m, int32_t l, const double* B,
                                  int64_t ldb, int32_t k, const double* S_host, double sign,
-                                 double scale, double* nrm_out, void* ws, size_t ws_bytes,
-                                 void* stream);
+                                 double scale, double* nrm_out, const KlsSegs* segs, void* ws,
+                                 size_t ws_bytes, void* stream);
 
 /* CGS2 comparator, fused first update + second projection of
  * Cgs2State.push (reference ortho.py:148-151, i.e. MvTimesMatAddMv followed
@@ -119,8 +150,8 @@ int kls_mv_times_mat_add_mv_host(double* Y, int64_t ldy, int64_t m, int32_t l, c
  * are re-read from L2, so the pair costs one HBM pass over Q.  1 <= k <= 2048;
  * s is host memory (carried in the launch) when s_on_host != 0, else device. */
 int kls_project_gram(const double* Q, int64_t ldq, int64_t m, int32_t k, double* v,
-                     const double* s, int32_t s_on_host, int32_t xnorm, double* out, void* ws,
-                     size_t ws_bytes, void* stream);
+                     const double* s, int32_t s_on_host, int32_t xnorm, double* out,
+                     const KlsSegs* segs, void* ws, size_t ws_bytes, void* stream);
 
 /* y = A x for CSR rows (int64 row pointer, int32 columns, fp64 values),
  * bit-identical to CsrMatrix.matvec (problems.py:127-136): products, then
@@ -142,7 +173,8 @@ int kls_ell_spmv(const int32_t* ecol, const double* eval, const uint8_t* elen, i
  * formed bit-identically to kls_ell_spmv and not stored. */
 int kls_ell_resid_norms(const int32_t* ecol, const double* eval, const uint8_t* elen,
                         int32_t width, int64_t nrows, int64_t ld, const double* x,
-                        const double* b, double* out, void* ws, size_t ws_bytes, void* stream);
+                        const double* b, double* out, const KlsSegs* segs, void* ws,
+                        size_t ws_bytes, void* stream);
 
 /* Matrix-free 7-point Laplacian, bit-identical to StencilLaplace3D._matvec
  * (problems.py:296-305) on nx local x-planes of a (.., ny, nz) grid; x_lo /
@@ -164,7 +196,7 @@ int kls_sub(const double* a, const double* b, double* out, int64_t n, void* stre
 /* Backward-error norms in one pass (gmres.backward_error, gmres.py:46-60):
  * out = [||b - ax||^2, ||x||^2, ||b||^2] (device). */
 int kls_resid_norms(const double* b, const double* ax, const double* x, int64_t n, double* out,
-                    void* ws, size_t ws_bytes, void* stream);
+                    const KlsSegs* segs, void* ws, size_t ws_bytes, void* stream);
 
 /* V(:, 0:k) <- V(:, 0:k) Z in place, Z k x k column-major on the device —
  * the Krylov-Schur basis rotation v_mat[:, nlock:k] @ Z (eig.py:237). */
@@ -213,6 +245,7 @@ typedef struct {
   double* Q;
   int64_t ldq;
   int64_t m;
+  KlsSegs segs;   /* the rows' layout (world 1 here) */
   double* gdev;
   double* cdev;
   double* gout[2];
@@ -270,13 +303,16 @@ int kls_peer_buffer_open(const void* handle, void** peer_buf);
 int kls_peer_buffer_close(void* peer_buf);
 int kls_peer_buffer_free(void* buf);
 
-/* The DCGS2 step's single global reduction (ledger site
- * kernels.py:57-59) as a one-shot NVLink exchange: sum over ranks of nv
- * doubles at src, accumulated in rank order (bitwise identical on all ranks),
- * written to out (device or mapped host memory).  epoch: +1 per call, same on
- * all ranks. */
-int kls_peer_allreduce(const double* src, int32_t nv, double* out, void* const* bufs, int32_t rank,
-                       int32_t world, int32_t cap, uint64_t epoch, int* err, void* stream);
+/* A reduction's global combine (ledger site
+ * kernels.py:57-59) as a one-shot NVLink exchange: src holds this rank's
+ * exported node values of nv outputs ([e][nv], as a reduction with world > 1
+ * writes them); every rank publishes them, and all evaluate the fixed
+ * segment tree into out (device or mapped host memory) — bitwise identical
+ * on all ranks and to a one-rank run.  epoch: +1 per call, same on all
+ * ranks; 8 * nv <= cap. */
+int kls_peer_seg_combine(const double* src, int32_t nv, double* out, void* const* bufs,
+                         int32_t rank, int32_t world, int32_t cap, uint64_t epoch, int* err,
+                         void* stream);
 
 /* kls_gram_dcgs2 with the step's device scalar arithmetic (kls_dcgs2_scalars)
  * fused into the kernel's last CTA: out <- g (2j+3), coef <- [c, s/alpha
@@ -284,7 +320,7 @@ int kls_peer_allreduce(const double* src, int32_t nv, double* out, void* const* 
  * j <= 1024.  One launch per step for arnoldi.py:362-400 / ortho.py:378-399. */
 int kls_gram_dcgs2_step(const double* Q, int64_t ldq, int64_t m, int32_t j, const double* w,
                         const double* aw, double* out, double* coef, double* gout, int32_t qr,
-                        void* ws, size_t ws_bytes, void* stream);
+                        const KlsSegs* segs, void* ws, size_t ws_bytes, void* stream);
 
 /* Host half of a DCGS2 Arnoldi step (arnoldi.py:367-420) in C++: guards,
  * Pythagorean alpha, Stephen's-trick t_piv, Hessenberg column j-1 and the
@@ -330,22 +366,24 @@ int kls_schur_swap(double* t, double* z, int64_t n, int64_t i, int32_t p, int32_
 int64_t kls_schur_move_front(double* t, double* z, int64_t n, const uint8_t* selected,
                              int64_t nsel, const KlsHostBlas* blas);
 
-/* kls_gram_dcgs2 fused with the step's global reduction: the kernel's last
- * CTA performs the one-shot peer exchange itself and writes the rank-ordered
- * global sum of the 2j+3 scalars to out — compute and collective in one
- * launch (j <= 1024, 2j+3 <= cap). */
+/* kls_gram_dcgs2 fused with the step's global reduction: the finishing CTA
+ * publishes this rank's exported tree nodes over NVLink peer memory and
+ * evaluates the fixed segment tree — compute and collective in one launch
+ * (8 (2 min(j, 256) + 5) <= cap; j > 256 runs as ceil(j / 256) column
+ * panels that use epochs epoch, epoch + 1, ...); segs->world / rank must
+ * match bufs. */
 int kls_gram_dcgs2_peer(const double* Q, int64_t ldq, int64_t m, int32_t j, const double* w,
-                        const double* aw, double* out, void* ws, size_t ws_bytes,
-                        void* const* bufs, int32_t rank, int32_t world, int32_t cap,
-                        uint64_t epoch, int* err, void* stream);
+                        const double* aw, double* out, const KlsSegs* segs, void* ws,
+                        size_t ws_bytes, void* const* bufs, int32_t rank, int32_t world,
+                        int32_t cap, uint64_t epoch, int* err, void* stream);
 
 /* kls_gram_dcgs2_step fused with the peer allreduce: Gram pass, the step's
  * one global reduction and the scalar step in a single launch. */
 int kls_gram_dcgs2_peer_step(const double* Q, int64_t ldq, int64_t m, int32_t j,
                              const double* w, const double* aw, double* out, double* coef,
-                             double* gout, int32_t qr, void* ws, size_t ws_bytes,
-                             void* const* bufs, int32_t rank, int32_t world, int32_t cap,
-                             uint64_t epoch, int* err, void* stream);
+                             double* gout, int32_t qr, const KlsSegs* segs, void* ws,
+                             size_t ws_bytes, void* const* bufs, int32_t rank, int32_t world,
+                             int32_t cap, uint64_t epoch, int* err, void* stream);
 
 /* Raise this rank's halo flag (= epoch) in the buffers of the ranks set in
  * target_mask, ordered after all prior work on the stream. */

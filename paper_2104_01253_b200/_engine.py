@@ -22,6 +22,12 @@ from .errors import DimensionError
 _PACK = 2048  # coefficients that fit in a kernel launch (kls_*_host)
 
 
+def _panels(j):
+    """Column panels (of <= 256) a Gram launch with j basis columns runs as;
+    each fused peer exchange consumes one epoch."""
+    return max(1, -(-j // 256))
+
+
 def _mapped(host_ptr):
     """Device address of a page-locked host address (identical under UVA)."""
     dptr = ctypes.c_void_p()
@@ -70,6 +76,9 @@ class Engine:
             self.slot_ev.append(ev.value)
         self._plan = None  # kls_dcgs2_queue_step plan (one GPU), False when n/a
         self.ws, self.wsb = runtime.workspace_for(self.st, capacity + 1)
+        # the rows' reduction layout (rank-count-independent segment tree)
+        self.segs = op.segs
+        self.segp = op.segs.ptr
         # N > 1: the per-step reduction goes over NVLink peer memory when
         # available (csrc/comm.cu), else through NCCL
         self.peer = runtime.peer_link(self.comm) if self.world > 1 else None
@@ -88,64 +97,76 @@ class Engine:
 
     # -- reductions -----------------------------------------------------------
     def _out(self, count):
-        """Where a reducing kernel writes `count` results."""
+        """Where a reducing kernel writes `count` results (world > 1: this
+        rank's exported tree nodes, up to 8 x count)."""
         if self.world == 1:
             if count > self.res_np.size:
                 raise DimensionError("result buffer too small")
             return self.res_dev
-        self.stage.ensure(count)
+        self.stage.ensure(runtime.SEG_MAX_EXPORT * count)
         return self.stage.dev_out.data_ptr()
 
-    def _finish(self, count):
-        if self.world == 1:
-            _lib.call("kls_stream_sync", self.st)
-            runtime.XFER["d2h"] += 8 * count
-            return self.res_np[:count].copy()
+    def _combine_into(self, count, dst_ptr, dst=None):
+        """world > 1: combine the exported nodes in stage.dev_out over the
+        ranks into dst_ptr (peer exchange) or dst (NCCL path, a tensor)."""
         rec = trace._active
         if self.peer is not None:
             if count > self.res_np.size:
                 raise DimensionError("result buffer too small")
             if rec is not None and rec.events:
                 with rec.span("allreduce"):
-                    self.peer.allreduce(self.stage.dev_out.data_ptr(), count, self.res_dev, self.st)
+                    self.peer.seg_combine(self.stage.dev_out.data_ptr(), count, dst_ptr, self.st)
             else:
-                self.peer.allreduce(self.stage.dev_out.data_ptr(), count, self.res_dev, self.st)
+                self.peer.seg_combine(self.stage.dev_out.data_ptr(), count, dst_ptr, self.st)
+            return None
+        if rec is not None and rec.events:
+            with rec.span("allreduce"):
+                out = self.comm.combine_(self.stage.dev_out, count)
+        else:
+            out = self.comm.combine_(self.stage.dev_out, count)
+        if dst is not None:
+            dst[:count].copy_(out)
+        return out
+
+    def _finish(self, count):
+        if self.world == 1:
+            _lib.call("kls_stream_sync", self.st)
+            runtime.XFER["d2h"] += 8 * count
+            return self.res_np[:count].copy()
+        if self.peer is not None:
+            self._combine_into(count, self.res_dev)
             _lib.call("kls_stream_sync", self.st)
             self.peer.check()
             runtime.XFER["d2h"] += 8 * count
             return self.res_np[:count].copy()
-        out = self.stage.dev_out[:count]
-        if rec is not None and rec.events:
-            with rec.span("allreduce"):
-                self.comm.allreduce_(out)
-        else:
-            self.comm.allreduce_(out)
+        out = self._combine_into(count, None)
+        self.stage.dev_out[:count].copy_(out)
         return self.stage.fetch(count)
 
     def gram_dcgs2(self, j, w, aw):
         """[Q(:,0:j), w]^T [w, aw] and aw.aw over all ranks: 2j+3 values."""
-        if self.peer is not None and j <= 1024 and 2 * j + 3 <= self.res_np.size:
+        if self.peer is not None and 2 * j + 3 <= self.res_np.size:
             return self._gram_dcgs2_fused(j, w, aw)
         out = self._out(2 * j + 3)
         rec = trace._active
         if rec is None:
             _lib.call("kls_gram_dcgs2", self.qptr, self.ld, self.ml, j, w.data_ptr(),
-                      aw.data_ptr(), out, self.ws, self.wsb, self.st)
+                      aw.data_ptr(), out, self.segp, self.ws, self.wsb, self.st)
         else:
             rec.note("gram", 8 * self.ml * (j + 2))
             with rec.span("gram"):
                 _lib.call("kls_gram_dcgs2", self.qptr, self.ld, self.ml, j, w.data_ptr(),
-                          aw.data_ptr(), out, self.ws, self.wsb, self.st)
+                          aw.data_ptr(), out, self.segp, self.ws, self.wsb, self.st)
         return self._finish(2 * j + 3)
 
     def _gram_dcgs2_fused(self, j, w, aw):
         """N > 1: Gram + one-shot NVLink allreduce in one kernel; the global
         sum lands in the mapped result buffer."""
         link = self.peer
-        link.ar_epoch += 1
+        first = link.take_epochs(_panels(j))
         args = ("kls_gram_dcgs2_peer", self.qptr, self.ld, self.ml, j, w.data_ptr(), aw.data_ptr(),
-                self.res_dev, self.ws, self.wsb, link.ptrs, link.rank, link.world, link.CAP,
-                link.ar_epoch, link.err_dev, self.st)
+                self.res_dev, self.segp, self.ws, self.wsb, link.ptrs, link.rank, link.world,
+                link.CAP, first, link.err_dev, self.st)
         rec = trace._active
         if rec is None:
             _lib.call(*args)
@@ -168,32 +189,33 @@ class Engine:
         rec = trace._active
         if rec is not None:
             rec.note("gram", 8 * self.ml * (j + 2))
-        fused = j <= 1024  # scalar step fused into the Gram kernel's last CTA
+        fused = True  # scalar step fused into the Gram kernel's finishing CTA
         qflag = 1 if qr else 0
-        if self.peer is not None and j <= 1024 and count <= self.peer.CAP:
+        if self.peer is not None:
             link = self.peer
-            link.ar_epoch += 1
+            first = link.take_epochs(_panels(j))
             link.comm.allreduce_calls += 1
             args = ("kls_gram_dcgs2_peer_step", self.qptr, self.ld, self.ml, j, w.data_ptr(),
                     aw.data_ptr(), self.gdev.data_ptr(), self.cdev.data_ptr(), self.slot_dev[slot],
-                    qflag, self.ws, self.wsb, link.ptrs, link.rank, link.world, link.CAP,
-                    link.ar_epoch, link.err_dev, self.st)
-        elif self.world == 1 and fused:
+                    qflag, self.segp, self.ws, self.wsb, link.ptrs, link.rank, link.world,
+                    link.CAP, first, link.err_dev, self.st)
+        elif self.world == 1:
             args = ("kls_gram_dcgs2_step", self.qptr, self.ld, self.ml, j, w.data_ptr(),
                     aw.data_ptr(), self.gdev.data_ptr(), self.cdev.data_ptr(), self.slot_dev[slot],
-                    qflag, self.ws, self.wsb, self.st)
+                    qflag, self.segp, self.ws, self.wsb, self.st)
         else:
             fused = False
+            dst = self.gdev.data_ptr() if self.world == 1 else self._out(count)
             args = ("kls_gram_dcgs2", self.qptr, self.ld, self.ml, j, w.data_ptr(), aw.data_ptr(),
-                    self.gdev.data_ptr(), self.ws, self.wsb, self.st)
+                    dst, self.segp, self.ws, self.wsb, self.st)
         if rec is not None and rec.events:
             with rec.span("gram"):
                 _lib.call(*args)
         else:
             _lib.call(*args)
         if not fused:
-            if self.world > 1 and self.peer is None:
-                self.comm.allreduce_(self.gdev[:count])
+            if self.world > 1:
+                self._combine_into(count, self.gdev.data_ptr(), self.gdev)
             _lib.call("kls_dcgs2_scalars", self.gdev.data_ptr(), j, qflag, self.cdev.data_ptr(),
                       self.slot_dev[slot], self.st)
         _lib.call("kls_event_record", self.slot_ev[slot], self.st)
@@ -228,7 +250,8 @@ class Engine:
             return np.zeros(0)
         out = self._out(n)
         args = ("kls_mv_trans_mv", self.qptr if k else None, self.ld, self.ml, k, None,
-                x.data_ptr(), None, 1, 1 if xnorm else 0, out, self.ws, self.wsb, self.st)
+                x.data_ptr(), None, 1, 1 if xnorm else 0, out, self.segp, self.ws, self.wsb,
+                self.st)
         rec = trace._active
         if rec is None:
             _lib.call(*args)
@@ -269,11 +292,12 @@ class Engine:
             runtime.XFER["h2d"] += 8 * k
             args = ("kls_mv_times_mat_add_mv_host", y.data_ptr(), self.ld, self.ml, 1,
                     self.qptr if k else None, self.ld, k, c.ctypes.data if k else None,
-                    -1.0, 1.0, nrm, self.ws, self.wsb, self.st)
+                    -1.0, 1.0, nrm, self.segp, self.ws, self.wsb, self.st)
         else:
             dev = self.stage.push(coef)
             args = ("kls_mv_times_mat_add_mv", y.data_ptr(), self.ld, self.ml, 1, self.qptr,
-                    self.ld, k, dev.data_ptr(), -1.0, 1.0, nrm, self.ws, self.wsb, self.st)
+                    self.ld, k, dev.data_ptr(), -1.0, 1.0, nrm, self.segp, self.ws, self.wsb,
+                    self.st)
         rec = trace._active
         if rec is None:
             _lib.call(*args)
@@ -296,7 +320,7 @@ class Engine:
         c = np.ascontiguousarray(coef, dtype=np.float64)
         runtime.XFER["h2d"] += 8 * k
         args = ("kls_project_gram", self.qptr, self.ld, self.ml, k, y.data_ptr(), c.ctypes.data,
-                1, 0, self._out(k), self.ws, self.wsb, self.st)
+                1, 0, self._out(k), self.segp, self.ws, self.wsb, self.st)
         rec = trace._active
         if rec is None:
             _lib.call(*args)
@@ -316,38 +340,33 @@ class Engine:
         trace.note("mtm", 8 * self.ml * (k + 2))
         if k <= _PACK:
             _lib.call("kls_mv_times_mat_add_mv_host", y.data_ptr(), self.ld, self.ml, 1, self.qptr,
-                      self.ld, k, c.ctypes.data, 1.0, 1.0, None, self.ws, self.wsb, self.st)
+                      self.ld, k, c.ctypes.data, 1.0, 1.0, None, None, self.ws, self.wsb,
+                      self.st)
         else:
             dev = self.stage.push(c)
             _lib.call("kls_mv_times_mat_add_mv", y.data_ptr(), self.ld, self.ml, 1, self.qptr,
-                      self.ld, k, dev.data_ptr(), 1.0, 1.0, None, self.ws, self.wsb, self.st)
+                      self.ld, k, dev.data_ptr(), 1.0, 1.0, None, None, self.ws, self.wsb,
+                      self.st)
 
     def resid_norms(self, b, ax, x):
         """[||b - ax||^2, ||x||^2, ||b||^2] over all ranks, one pass."""
         out = self._out(3)
         trace.note("resid_norms", 24 * self.ml)
         _lib.call("kls_resid_norms", b.data_ptr(), ax.data_ptr(), x.data_ptr(), self.ml, out,
-                  self.ws, self.wsb, self.st)
+                  self.segp, self.ws, self.wsb, self.st)
         return self._finish(3)
 
     def resid_norms_queue(self, b, ax, x, out):
-        """resid_norms into the device tensor `out` (3 doubles, summed over
+        """resid_norms into the device tensor `out` (3 doubles, combined over
         ranks) without waiting: for diagnostics read back later in bulk."""
         trace.note("resid_norms", 24 * self.ml)
         if self.world == 1:
             _lib.call("kls_resid_norms", b.data_ptr(), ax.data_ptr(), x.data_ptr(), self.ml,
-                      out.data_ptr(), self.ws, self.wsb, self.st)
-            return
-        if self.peer is not None:
-            self.stage.ensure(3)
-            src = self.stage.dev_out.data_ptr()
-            _lib.call("kls_resid_norms", b.data_ptr(), ax.data_ptr(), x.data_ptr(), self.ml, src,
-                      self.ws, self.wsb, self.st)
-            self.peer.allreduce(src, 3, out.data_ptr(), self.st)
+                      out.data_ptr(), self.segp, self.ws, self.wsb, self.st)
             return
         _lib.call("kls_resid_norms", b.data_ptr(), ax.data_ptr(), x.data_ptr(), self.ml,
-                  out.data_ptr(), self.ws, self.wsb, self.st)
-        self.comm.allreduce_(out)
+                  self._out(3), self.segp, self.ws, self.wsb, self.st)
+        self._combine_into(3, out.data_ptr(), out)
 
     def divide_into(self, dst, src, alpha):
         trace.note("scale", 16 * self.ml)
@@ -369,8 +388,8 @@ class Engine:
                 and not getattr(self.op, "_peer", False)):
             ecol, evals, elen, width, ld = ell
             _lib.call("kls_ell_resid_norms", ecol.data_ptr(), evals.data_ptr(), elen.data_ptr(),
-                      width, self.ml, ld, x.data_ptr(), b.data_ptr(), out.data_ptr(), self.ws,
-                      self.wsb, self.st)
+                      width, self.ml, ld, x.data_ptr(), b.data_ptr(), out.data_ptr(), self.segp,
+                      self.ws, self.wsb, self.st)
             return
         self.apply(x, y)
         self.resid_norms_queue(b, y, x, out)
@@ -396,6 +415,7 @@ class Engine:
             if desc is not None:
                 p = _lib.KlsStepPlan()
                 p.Q, p.ldq, p.m = self.qptr, self.ld, self.ml
+                p.segs = self.segs.c
                 p.gdev, p.cdev = self.gdev.data_ptr(), self.cdev.data_ptr()
                 p.gout[0], p.gout[1] = self.slot_dev
                 p.ws, p.ws_bytes, p.stream = self.ws, self.wsb, self.st

@@ -26,17 +26,17 @@ SIGNATURES = {
     "kls_stream_sync": (ctypes.c_int, [c_dp]),
     "kls_host_device_ptr": (ctypes.c_int, [c_dp, ctypes.POINTER(ctypes.c_void_p)]),
     "kls_workspace_bytes": (sz, [i64, i32]),
-    "kls_mv_trans_mv": (ctypes.c_int, [c_dp, i64, i64, i32, c_dp, c_dp, c_dp, i32, i32, c_dp, c_dp, sz, c_dp]),
-    "kls_project_gram": (ctypes.c_int, [c_dp, i64, i64, i32, c_dp, c_dp, i32, i32, c_dp, c_dp, sz, c_dp]),
+    "kls_mv_trans_mv": (ctypes.c_int, [c_dp, i64, i64, i32, c_dp, c_dp, c_dp, i32, i32, c_dp, c_dp, c_dp, sz, c_dp]),
+    "kls_project_gram": (ctypes.c_int, [c_dp, i64, i64, i32, c_dp, c_dp, i32, i32, c_dp, c_dp, c_dp, sz, c_dp]),
     "kls_ipc_handle_bytes": (sz, []),
     "kls_peer_buffer_alloc": (ctypes.c_int, [sz, ctypes.POINTER(ctypes.c_void_p), c_dp]),
     "kls_peer_buffer_open": (ctypes.c_int, [c_dp, ctypes.POINTER(ctypes.c_void_p)]),
     "kls_peer_buffer_close": (ctypes.c_int, [c_dp]),
     "kls_peer_buffer_free": (ctypes.c_int, [c_dp]),
     "kls_gram_dcgs2_step": (ctypes.c_int, [c_dp, i64, i64, i32, c_dp, c_dp, c_dp, c_dp, c_dp, i32,
-                                           c_dp, sz, c_dp]),
+                                           c_dp, c_dp, sz, c_dp]),
     "kls_gram_dcgs2_peer_step": (ctypes.c_int, [c_dp, i64, i64, i32, c_dp, c_dp, c_dp, c_dp, c_dp,
-                                                i32, c_dp, sz, c_dp, i32, i32, i32,
+                                                i32, c_dp, c_dp, sz, c_dp, i32, i32, i32,
                                                 ctypes.c_uint64, c_dp,
                                                 c_dp]),
     "kls_dcgs2_host_step": (ctypes.c_int, [c_dp, i32, i64, f64, c_dp, c_dp, i64, c_dp, c_dp, c_dp,
@@ -52,12 +52,12 @@ SIGNATURES = {
     "kls_dcgs2_run": (ctypes.c_int, [c_dp, i32, i32, i32, i32, c_dp]),
     "kls_hessenberg_reduce": (ctypes.c_int, [c_dp, c_dp, i64, c_dp]),
     "kls_ell_resid_norms": (ctypes.c_int, [c_dp, c_dp, c_dp, i32, i64, i64, c_dp, c_dp, c_dp,
-                                           c_dp, sz, c_dp]),
+                                           c_dp, c_dp, sz, c_dp]),
     "kls_schur_sweeps": (ctypes.c_int, [c_dp, c_dp, i64, i64, c_dp]),
     "kls_schur_swap": (ctypes.c_int, [c_dp, c_dp, i64, i64, i32, i32, c_dp]),
     "kls_schur_move_front": (i64, [c_dp, c_dp, i64, c_dp, i64, c_dp]),
     "kls_schur_eigenvectors": (ctypes.c_int, [c_dp, c_dp, i64, i64, c_dp, i64, c_dp, c_dp, c_dp]),
-    "kls_gram_dcgs2": (ctypes.c_int, [c_dp, i64, i64, i32, c_dp, c_dp, c_dp, c_dp, sz, c_dp]),
+    "kls_gram_dcgs2": (ctypes.c_int, [c_dp, i64, i64, i32, c_dp, c_dp, c_dp, c_dp, c_dp, sz, c_dp]),
     "kls_dcgs2_update": (ctypes.c_int, [c_dp, i64, i64, i32, c_dp, c_dp, c_dp, f64, i32, c_dp]),
     "kls_dcgs2_scalars": (ctypes.c_int, [c_dp, i32, i32, c_dp, c_dp, c_dp]),
     "kls_dcgs2_update_dev": (ctypes.c_int, [c_dp, i64, i64, i32, c_dp, c_dp, c_dp, c_dp, i32,
@@ -65,11 +65,11 @@ SIGNATURES = {
     "kls_dcgs2_update_host": (ctypes.c_int, [c_dp, i64, i64, i32, c_dp, c_dp, c_dp, f64, i32, c_dp]),
     "kls_mv_times_mat_add_mv": (
         ctypes.c_int,
-        [c_dp, i64, i64, i32, c_dp, i64, i32, c_dp, f64, f64, c_dp, c_dp, sz, c_dp],
+        [c_dp, i64, i64, i32, c_dp, i64, i32, c_dp, f64, f64, c_dp, c_dp, c_dp, sz, c_dp],
     ),
     "kls_mv_times_mat_add_mv_host": (
         ctypes.c_int,
-        [c_dp, i64, i64, i32, c_dp, i64, i32, c_dp, f64, f64, c_dp, c_dp, sz, c_dp],
+        [c_dp, i64, i64, i32, c_dp, i64, i32, c_dp, f64, f64, c_dp, c_dp, c_dp, sz, c_dp],
     ),
     "kls_csr_spmv": (ctypes.c_int, [c_dp, c_dp, c_dp, i64, c_dp, c_dp, c_dp]),
     "kls_csr_to_ell": (ctypes.c_int, [c_dp, c_dp, c_dp, i64, i32, i64, c_dp, c_dp, c_dp, c_dp]),
@@ -78,7 +78,7 @@ SIGNATURES = {
     "kls_dense_gemv": (ctypes.c_int, [c_dp, i64, i64, c_dp, c_dp, c_dp]),
     "kls_scale": (ctypes.c_int, [c_dp, c_dp, i64, f64, i32, c_dp]),
     "kls_sub": (ctypes.c_int, [c_dp, c_dp, c_dp, i64, c_dp]),
-    "kls_resid_norms": (ctypes.c_int, [c_dp, c_dp, c_dp, i64, c_dp, c_dp, sz, c_dp]),
+    "kls_resid_norms": (ctypes.c_int, [c_dp, c_dp, c_dp, i64, c_dp, c_dp, c_dp, sz, c_dp]),
     "kls_tsgemm_inplace": (ctypes.c_int, [c_dp, i64, i64, i32, c_dp, c_dp]),
     "kls_tsgemm_inplace_cols": (ctypes.c_int, [c_dp, i64, i64, i32, i32, c_dp, c_dp]),
     "kls_peer_buffer_bytes": (sz, [i32]),
@@ -86,10 +86,13 @@ SIGNATURES = {
     "kls_build_lap7_csr": (ctypes.c_int, [i64, i64, i64, i64, i64, i64, c_dp, c_dp, c_dp, c_dp]),
     "kls_mant5_nnz": (i64, [i64, i64, i64]),
     "kls_build_mant5_csr": (ctypes.c_int, [i64, i64, i64, i64, f64, f64, c_dp, c_dp, c_dp, c_dp]),
-    "kls_peer_allreduce": (ctypes.c_int, [c_dp, i32, c_dp, c_dp, i32, i32, i32, ctypes.c_uint64,
-                                          c_dp, c_dp]),
-    "kls_gram_dcgs2_peer": (ctypes.c_int, [c_dp, i64, i64, i32, c_dp, c_dp, c_dp, c_dp, sz, c_dp,
-                                           i32, i32, i32, ctypes.c_uint64, c_dp, c_dp]),
+    "kls_peer_seg_combine": (ctypes.c_int, [c_dp, i32, c_dp, c_dp, i32, i32, i32, ctypes.c_uint64,
+                                            c_dp, c_dp]),
+    "kls_gram_dcgs2_peer": (ctypes.c_int, [c_dp, i64, i64, i32, c_dp, c_dp, c_dp, c_dp, c_dp, sz,
+                                           c_dp, i32, i32, i32, ctypes.c_uint64, c_dp, c_dp]),
+    "kls_seg_rows": (ctypes.c_int, [c_dp, ctypes.POINTER(i64), ctypes.POINTER(i64)]),
+    "kls_seg_exports": (ctypes.c_int, [i32, i32, c_dp]),
+    "kls_seg_combine": (ctypes.c_int, [c_dp, i32, i64, i32, c_dp, c_dp]),
     "kls_peer_signal": (ctypes.c_int, [c_dp, i32, i32, i32, ctypes.c_uint64, c_dp]),
     "kls_stencil7_peer": (ctypes.c_int, [c_dp, c_dp, c_dp, c_dp, i64, i64, i64, c_dp, i32,
                                          ctypes.c_uint64, c_dp, c_dp]),
@@ -101,9 +104,16 @@ _NO_LAUNCH = frozenset({"kls_version", "kls_last_error", "kls_device_sm_count", 
                         "kls_lap7_nnz", "kls_mant5_nnz", "kls_ipc_handle_bytes",
                         "kls_peer_buffer_alloc", "kls_peer_buffer_open", "kls_peer_buffer_close",
                         "kls_peer_buffer_free", "kls_dcgs2_host_step", "kls_event_create",
+                        "kls_seg_rows", "kls_seg_exports",
                         "kls_event_destroy", "kls_event_record", "kls_event_sync",
                         "kls_hessenberg_reduce", "kls_schur_sweeps", "kls_schur_swap",
                         "kls_schur_move_front", "kls_schur_eigenvectors"})
+
+
+class KlsSegs(ctypes.Structure):
+    """include/klsgpu.h KlsSegs: the rank-count-independent reduction layout."""
+
+    _fields_ = [("m", i64), ("unit", i64), ("world", i32), ("rank", i32)]
 
 
 class KlsOpDesc(ctypes.Structure):
@@ -123,7 +133,7 @@ class KlsHostBlas(ctypes.Structure):
 class KlsStepPlan(ctypes.Structure):
     """include/klsgpu.h KlsStepPlan (kls_dcgs2_queue_step)."""
 
-    _fields_ = [("Q", c_dp), ("ldq", i64), ("m", i64), ("gdev", c_dp), ("cdev", c_dp),
+    _fields_ = [("Q", c_dp), ("ldq", i64), ("m", i64), ("segs", KlsSegs), ("gdev", c_dp), ("cdev", c_dp),
                 ("gout", c_dp * 2), ("ws", c_dp), ("ws_bytes", sz), ("stream", c_dp),
                 ("event", c_dp * 2), ("divide", i32), ("qr", i32), ("op", KlsOpDesc)]
 

@@ -3,6 +3,7 @@
 // the GMRES residual and backward-error norms (gmres.py:46-60, :151), and
 // the Krylov-Schur basis rotation V(:, a:b) <- V(:, a:b) Z (eig.py:237).
 #include "reduce.cuh"
+#include "seg.cuh"
 
 namespace {
 
@@ -30,61 +31,26 @@ __global__ void sub_kernel(const double* __restrict__ a, const double* __restric
     out[i] = a[i] - b[i];
 }
 
-// out[0] = ||b - ax||^2, out[1] = ||x||^2, out[2] = ||b||^2 in one pass;
-// 128-bit loads, two row pairs per thread per trip (6 loads in flight)
+// out[0] = ||b - ax||^2, out[1] = ||x||^2, out[2] = ||b||^2 in one pass,
+// reduced over the fixed segment tree (seg.cuh).  Thread t of virtual CTA v
+// takes the segment's rows v * 256 + t, stepping by V * 256 -- the same
+// grouping as the ELL-fused kernel (spmv.cu), so both give the same bits
+// for the same A x.
 __global__ void __launch_bounds__(kThreads) resid_norms_kernel(const double* __restrict__ b,
                                                                const double* __restrict__ ax,
                                                                const double* __restrict__ x,
-                                                               int64_t n, RedWs ws,
-                                                               double* out) {
-  double v[3] = {0.0, 0.0, 0.0};
-  const int64_t npair = n / 2;
-  const int64_t nthreads = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const double2* b2 = reinterpret_cast<const double2*>(b);
-  const double2* a2 = reinterpret_cast<const double2*>(ax);
-  const double2* x2 = reinterpret_cast<const double2*>(x);
-  auto acc = [&](double bi, double ai, double xi) {
-    const double r = bi - ai;
-    v[0] = fma(r, r, v[0]);
-    v[1] = fma(xi, xi, v[1]);
-    v[2] = fma(bi, bi, v[2]);
-  };
-  int64_t i = tid;
-  for (; i + nthreads < npair; i += 2 * nthreads) {
-    const double2 bb0 = __ldcs(b2 + i), aa0 = __ldcs(a2 + i), xx0 = __ldcs(x2 + i);
-    const double2 bb1 = __ldcs(b2 + i + nthreads), aa1 = __ldcs(a2 + i + nthreads),
-                  xx1 = __ldcs(x2 + i + nthreads);
-    acc(bb0.x, aa0.x, xx0.x);
-    acc(bb0.y, aa0.y, xx0.y);
-    acc(bb1.x, aa1.x, xx1.x);
-    acc(bb1.y, aa1.y, xx1.y);
-  }
-  for (; i < npair; i += nthreads) {
-    const double2 bb = __ldcs(b2 + i), aa = __ldcs(a2 + i), xx = __ldcs(x2 + i);
-    acc(bb.x, aa.x, xx.x);
-    acc(bb.y, aa.y, xx.y);
-  }
-  if ((n & 1) && tid == 0) acc(b[n - 1], ax[n - 1], x[n - 1]);
-  grid_reduce_finish<3>(v, ws, out);
-}
-
-// scalar-load form for operands that are not 16-byte aligned
-__global__ void __launch_bounds__(kThreads) resid_norms_scalar_kernel(
-    const double* __restrict__ b, const double* __restrict__ ax, const double* __restrict__ x,
-    int64_t n, RedWs ws, double* out) {
-  double v[3] = {0.0, 0.0, 0.0};
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-       i += stride) {
-    const double bi = b[i];
-    const double r = bi - ax[i];
-    const double xi = x[i];
-    v[0] = fma(r, r, v[0]);
-    v[1] = fma(xi, xi, v[1]);
-    v[2] = fma(bi, bi, v[2]);
-  }
-  grid_reduce_finish<3>(v, ws, out);
+                                                               const __grid_constant__ seg::SimpleArgs a) {
+  seg::run_simple<kThreads, 3>(a, [&](int64_t r0, int64_t rows, int v, int V, double (&acc)[3]) {
+    const int64_t step = static_cast<int64_t>(V) * kThreads;
+    for (int64_t i = static_cast<int64_t>(v) * kThreads + threadIdx.x; i < rows; i += step) {
+      const double bi = __ldcs(b + r0 + i);
+      const double r = bi - __ldcs(ax + r0 + i);
+      const double xi = __ldcs(x + r0 + i);
+      acc[0] = fma(r, r, acc[0]);
+      acc[1] = fma(xi, xi, acc[1]);
+      acc[2] = fma(bi, bi, acc[2]);
+    }
+  });
 }
 
 // V(:, 0:k) <- V(:, 0:k) Z in place, Z k x k column-major (device).  A CTA
@@ -267,21 +233,16 @@ KLS_API int kls_sub(const double* a, const double* b, double* out, int64_t n, vo
 }
 
 KLS_API int kls_resid_norms(const double* b, const double* ax, const double* x, int64_t n,
-                            double* out, void* ws, size_t ws_bytes, void* stream) {
+                            double* out, const KlsSegs* segs, void* ws, size_t ws_bytes,
+                            void* stream) {
   if (b == nullptr || ax == nullptr || x == nullptr || out == nullptr || ws == nullptr || n < 0)
     return fail(KLS_EINVAL, "resid_norms: bad arguments");
-  const bool vec = ((reinterpret_cast<uintptr_t>(b) | reinterpret_cast<uintptr_t>(ax) |
-                     reinterpret_cast<uintptr_t>(x)) & 15) == 0;
-  const int grid = vec ? grid_1d((n + 3) / 4, 4) : grid_1d(n, 4);
-  if (!red_ws_fits(ws_bytes, grid, 3)) return fail(KLS_ENOSPC, "resid_norms: workspace too small");
-  if (vec) {
-    resid_norms_kernel<<<grid, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(b, ax, x, n,
-                                                                                 red_ws(ws), out);
-    return check_launch("resid_norms_kernel");
-  }
-  resid_norms_scalar_kernel<<<grid, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
-      b, ax, x, n, red_ws(ws), out);
-  return check_launch("resid_norms_scalar_kernel");
+  seg::SimpleArgs a;
+  int rc = seg::make_plan_simple(segs, n, kThreads, a, ws, ws_bytes, 3, out);
+  if (rc) return rc;
+  const int grid = std::max(1, std::min(a.P.nitems, 4 * sm_count()));
+  resid_norms_kernel<<<grid, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(b, ax, x, a);
+  return check_launch("resid_norms_kernel");
 }
 
 KLS_API int kls_tsgemm_inplace(double* V, int64_t ldv, int64_t m, int32_t k, const double* Z,

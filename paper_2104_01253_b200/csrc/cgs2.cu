@@ -28,6 +28,7 @@ using namespace kls::gram;
 
 constexpr int kPRP = 1;        // row pairs per lane: 8 warps x 64 rows = 512-row chunks
 constexpr int kPBlocks = 3;    // CTAs per SM
+constexpr int kPVirt = 148;    // virtual CTAs per segment (a third of the grid)
 
 template <int NC>
 struct PgPack {
@@ -63,8 +64,16 @@ __device__ __forceinline__ double2 load_pair_pol(const double* col, int64_t r, i
   return v;
 }
 
+// Operands of one segment (pointers offset to its first row).
+struct PgRows {
+  const double* Q;
+  int64_t ldq;
+  int32_t k;
+  int64_t m;  // the segment's rows
+};
+
 template <bool CHECK>
-__device__ __forceinline__ void pg_chunk(const GramParams& p, double* v, const double* ss,
+__device__ __forceinline__ void pg_chunk(const PgRows& p, double* v, const double* ss,
                                          int64_t wbase, int lane, double* wacc, double& xn) {
   constexpr int RP = kPRP;
   const uint64_t keep = policy_evict_last();
@@ -138,92 +147,128 @@ __device__ __forceinline__ void pg_chunk(const GramParams& p, double* v, const d
   }
 }
 
+// Launch arguments shared by both variants.
+struct PgArgs {
+  const double* Q;
+  int64_t ldq;
+  int32_t k;
+  int32_t xnorm;
+  seg::Plan P;
+  seg::Ws ws;
+  seg::Dest d;
+};
+
+// Item epilogue of both variants: the 8 warps' accumulators (sacc rows,
+// stride) and xn in warp order -> the item partial; the finishing CTA runs
+// the segment tree.  Returns whether this CTA finished the launch.
+__device__ __forceinline__ bool pg_commit(const PgArgs& a, int it, int s, int V, const double* sacc,
+                                          int stride, double xn, double* s_red, int* s_flag) {
+  __shared__ double sx[kWarps];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const double t = warp_sum(xn);
+  if (lane == 0) sx[warp] = t;
+  __syncthreads();
+  const int nv = a.k + (a.xnorm ? 1 : 0);
+  return seg::item_commit<kThreads, 0>(a.P, a.ws, it, s, V, nv, threadIdx.x, s_red, s_flag, [&](int i) {
+    double r = 0.0;
+    if (i < a.k) {
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) r += sacc[w * stride + i];
+    } else {
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) r += sx[w];
+    }
+    return r;
+  });
+}
+
 template <int NC>
 __global__ void __launch_bounds__(kThreads, kPBlocks)
-    project_gram_kernel(GramParams p, double* v, const double* s_dev,
+    project_gram_kernel(PgArgs a, double* v, const double* s_dev,
                         const __grid_constant__ PgPack<NC> pk) {
   extern __shared__ double sm[];
-  const int ng = (p.k + kG - 1) / kG;
+  __shared__ double s_red[kThreads];
+  __shared__ int s_flag, s_ok;
+  const int ng = (a.k + kG - 1) / kG;
   const int stride = ng * kG;
   double* ss = sm;                  // coefficients, zero-padded to ng * kG
   double* sacc = sm + stride;       // [kWarps][stride]
   const double* s = NC > 0 ? pk.v : s_dev;
-  for (int i = threadIdx.x; i < stride; i += kThreads) ss[i] = i < p.k ? s[i] : 0.0;
+  for (int i = threadIdx.x; i < stride; i += kThreads) ss[i] = i < a.k ? s[i] : 0.0;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   double* wacc = sacc + warp * stride;
-  for (int i = lane; i < stride; i += 32) wacc[i] = 0.0;
-  __syncthreads();
-  double ex[1] = {0.0};
-  double xn = 0.0;
   constexpr int64_t WROWS = 64 * kPRP;
   constexpr int64_t CROWS = WROWS * kWarps;
-  const int64_t nchunks = (p.m + CROWS - 1) / CROWS;
-  for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
-    const int64_t cbase = ch * CROWS;
-    const int64_t wbase = cbase + warp * WROWS;
-    if (cbase + CROWS <= p.m)
-      pg_chunk<false>(p, v, ss, wbase, lane, wacc, xn);
-    else
-      pg_chunk<true>(p, v, ss, wbase, lane, wacc, xn);
+  bool fin = false;
+  for (int it = blockIdx.x; it < a.P.nitems; it += gridDim.x) {
+    int sg, vi, V;
+    seg::item_of(a.P, it, sg, vi, V);
+    const int64_t base = a.P.L.off[sg];
+    const PgRows pr{a.Q + base, a.ldq, a.k, a.P.L.off[sg + 1] - base};
+    double* vs = v + base;
+    for (int i = lane; i < stride; i += 32) wacc[i] = 0.0;
+    __syncthreads();
+    double xn = 0.0;
+    const int64_t nchunks = (pr.m + CROWS - 1) / CROWS;
+    for (int64_t ch = vi; ch < nchunks; ch += V) {
+      const int64_t cbase = ch * CROWS;
+      const int64_t wbase = cbase + warp * WROWS;
+      if (cbase + CROWS <= pr.m)
+        pg_chunk<false>(pr, vs, ss, wbase, lane, wacc, xn);
+      else
+        pg_chunk<true>(pr, vs, ss, wbase, lane, wacc, xn);
+    }
+    fin = pg_commit(a, it, sg, V, sacc, stride, xn, s_red, &s_flag) || fin;
   }
-  gram_epilogue<1>(p, sacc, stride, ex, xn);
+  if (fin) seg::seg_final<kThreads, 0>(a.P.L, a.ws, a.k + (a.xnorm ? 1 : 0), a.d, threadIdx.x, &s_ok,
+                                       [](int o) { return (int64_t)o; });
 }
 
 template <int NC>
-int launch_pg(GramParams p, double* v, const double* s, bool host, size_t ws_bytes,
-              cudaStream_t st) {
+int launch_pg(PgArgs a, double* v, const double* s, bool host, size_t ws_bytes, cudaStream_t st) {
   PgPack<NC> pk;
-  if (NC > 0) std::memcpy(pk.v, s, sizeof(double) * p.k);
+  if (NC > 0) std::memcpy(pk.v, s, sizeof(double) * a.k);
   constexpr int64_t CROWS = 64 * kPRP * kWarps;
-  const int64_t nchunks = ceil_div(p.m, CROWS);
-  int grid = static_cast<int>(std::min<int64_t>(nchunks, (int64_t)kPBlocks * sm_count()));
-  if (grid < 1) grid = 1;
-  const int64_t nv = static_cast<int64_t>(p.k) + (p.xnorm ? 1 : 0);
-  if (!red_ws_fits(ws_bytes, grid, static_cast<int>(nv)))
-    return fail(KLS_ENOSPC, "project_gram: workspace too small");
-  const int ng = (p.k + kG - 1) / kG;
+  seg::make_plan(a.P.L, CROWS, kPVirt, a.P);
+  const int nv = a.k + (a.xnorm ? 1 : 0);
+  if (seg::plan_ws_bytes(a.P, nv) > ws_bytes) return fail(KLS_ENOSPC, "project_gram: workspace too small");
+  a.ws = seg::ws_of(a.ws.tick, a.P.nitems, nv);
+  const int grid = std::max(1, std::min(a.P.nitems, kPBlocks * sm_count()));
+  const int ng = (a.k + kG - 1) / kG;
   const size_t smem = sizeof(double) * static_cast<size_t>(ng * kG) * (1 + kWarps);
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(project_gram_kernel<NC>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return fail(KLS_ECUDA, "project_gram smem: %s", cudaGetErrorString(e));
   }
-  project_gram_kernel<NC><<<grid, kThreads, smem, st>>>(p, v, host ? nullptr : s, pk);
+  project_gram_kernel<NC><<<grid, kThreads, smem, st>>>(a, v, host ? nullptr : s, pk);
   return check_launch("project_gram_kernel");
-}
-
-
-// KLS_PROJECT_GRAM=ldg forces the L2-reuse variant (experiments).
-inline bool l2_variant() {
-  static const bool on = [] {
-    const char* e = getenv("KLS_PROJECT_GRAM");
-    return e != nullptr && e[0] == 'l';
-  }();
-  return on;
 }
 
 // ---------------------------------------------------------------------------
 // Register-resident variant (default for k <= 256): Q crosses HBM once and
-// is never re-read.  A CTA takes row chunks of R = 64 * RB rows; consumer
-// warp w owns the columns w, w + 8, ... (CPW of them) and holds its
-// CPW x RB row pairs of the chunk in registers.  Phase A forms its partial
-// Q s per row; the 8 partials are combined in fixed warp order through
-// shared memory into w = v - Q s (written back over v); phase B takes
-// q_c . w from the same registers, accumulating per lane across chunks; the
-// cross-lane sums run once per launch.  CPW * RB = 16 row pairs (or 32 at
-// CPW = 32) keep 16-32 KB of loads in flight per CTA; the window between
-// the two looks at Q is a register file, not a cache.
+// is never re-read.  A virtual CTA takes row chunks of R = 64 * RB rows of
+// its segment; consumer warp w owns the columns w, w + 8, ... (CPW of them)
+// and holds its CPW x RB row pairs of the chunk in registers.  Phase A forms
+// its partial Q s per row; the 8 partials are combined in fixed warp order
+// through shared memory into w = v - Q s (written back over v); phase B
+// takes q_c . w from the same registers, accumulating per lane across the
+// item's chunks (one cross-lane reduction per item).  CPW * RB = 16 row
+// pairs (or 32 at CPW = 32) keep 16-32 KB of loads in flight per CTA; the
+// window between the two looks at Q is a register file, not a cache.
 
 constexpr int kRegMaxK = 32 * kWarps;
 
 template <int CPW, int RB, int NC>
 __global__ void __launch_bounds__(kThreads, CPW >= 32 ? 1 : 2)
-    project_gram_reg_kernel(GramParams p, double* v, const double* s_dev,
+    project_gram_reg_kernel(PgArgs a, double* v, const double* s_dev,
                             const __grid_constant__ PgPack<NC> pk) {
   constexpr int R = 64 * RB;
   extern __shared__ __align__(16) double rsm[];
-  const int k = p.k;
+  __shared__ double s_red[kThreads];
+  __shared__ int s_flag, s_ok;
+  const int k = a.k;
   const int stride = (k + kG - 1) / kG * kG;
   constexpr int kSs = CPW * kWarps;                // >= stride
   double* ss = rsm;                                // coefficients, zero-padded to kSs
@@ -232,105 +277,119 @@ __global__ void __launch_bounds__(kThreads, CPW >= 32 ? 1 : 2)
   double* wbuf = part + kWarps * R;                // [R]
   const double* s = NC > 0 ? pk.v : s_dev;
   for (int i = threadIdx.x; i < kSs; i += kThreads) ss[i] = i < k ? s[i] : 0.0;
-  for (int i = threadIdx.x; i < kWarps * stride; i += kThreads) sacc[i] = 0.0;
-  __syncthreads();
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  double acc[CPW];
-#pragma unroll
-  for (int i = 0; i < CPW; ++i) acc[i] = 0.0;
   double* mypart = part + warp * R;
-  double xn = 0.0;
-  const int64_t nfull = p.m / R;
-  for (int64_t ch = blockIdx.x; ch < nfull; ch += gridDim.x) {
-    const int64_t base = ch * R;
-    // v for the rows this thread combines, fetched early
-    constexpr int NV = (R + kThreads - 1) / kThreads;
-    double vv[NV];
+  double* wacc = sacc + warp * stride;
+  bool fin = false;
+  for (int it = blockIdx.x; it < a.P.nitems; it += gridDim.x) {
+    int sg, vi, V;
+    seg::item_of(a.P, it, sg, vi, V);
+    const int64_t base = a.P.L.off[sg];
+    const int64_t rows = a.P.L.off[sg + 1] - base;
+    const double* Q = a.Q + base;
+    double* vs = v + base;
+    for (int i = lane; i < stride; i += 32) wacc[i] = 0.0;
+    __syncthreads();
+    double acc[CPW];
 #pragma unroll
-    for (int i = 0; i < NV; ++i) {
-      const int row = threadIdx.x + kThreads * i;
-      if (row < R) vv[i] = v[base + row];
+    for (int i = 0; i < CPW; ++i) acc[i] = 0.0;
+    double xn = 0.0;
+    const int64_t nfull = rows / R;
+    for (int64_t ch = vi; ch < nfull; ch += V) {
+      const int64_t cb = ch * R;
+      // v for the rows this thread combines, fetched early
+      constexpr int NV = (R + kThreads - 1) / kThreads;
+      double vv[NV];
+#pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        const int row = threadIdx.x + kThreads * i;
+        if (row < R) vv[i] = vs[cb + row];
+      }
+      double2 q[CPW][RB];
+#pragma unroll
+      for (int i = 0; i < CPW; ++i) {
+        const int col = warp + kWarps * i;
+        const double* cp = Q + static_cast<int64_t>(col < k ? col : 0) * a.ldq + cb + 2 * lane;
+#pragma unroll
+        for (int b = 0; b < RB; ++b)
+          q[i][b] = col < k ? ld_stream2(cp + 64 * b) : make_double2(0.0, 0.0);
+      }
+      // phase A
+#pragma unroll
+      for (int b = 0; b < RB; ++b) {
+        double2 av = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int i = 0; i < CPW; ++i) {
+          const double sc = ss[warp + kWarps * i];  // zero past k (padded)
+          av.x = fma(q[i][b].x, sc, av.x);
+          av.y = fma(q[i][b].y, sc, av.y);
+        }
+        *reinterpret_cast<double2*>(mypart + 64 * b + 2 * lane) = av;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        const int row = threadIdx.x + kThreads * i;
+        if (row < R) {
+          double t = 0.0;
+#pragma unroll
+          for (int w = 0; w < kWarps; ++w) t += part[w * R + row];
+          const double wv = vv[i] + -1.0 * t;
+          wbuf[row] = wv;
+          vs[cb + row] = wv;
+          xn = fma(wv, wv, xn);
+        }
+      }
+      __syncthreads();
+      // phase B from the registers
+#pragma unroll
+      for (int b = 0; b < RB; ++b) {
+        const double2 wv = *reinterpret_cast<const double2*>(wbuf + 64 * b + 2 * lane);
+#pragma unroll
+        for (int i = 0; i < CPW; ++i) {
+          acc[i] = fma(q[i][b].x, wv.x, acc[i]);
+          acc[i] = fma(q[i][b].y, wv.y, acc[i]);
+        }
+      }
     }
-    double2 q[CPW][RB];
 #pragma unroll
     for (int i = 0; i < CPW; ++i) {
       const int col = warp + kWarps * i;
-      const double* cp = p.Q + static_cast<int64_t>(col < k ? col : 0) * p.ldq + base + 2 * lane;
-#pragma unroll
-      for (int b = 0; b < RB; ++b)
-        q[i][b] = col < k ? ld_stream2(cp + 64 * b) : make_double2(0.0, 0.0);
+      const double t = warp_sum(acc[i]);
+      if (lane == 0 && col < k) wacc[col] = t;
     }
-    // phase A
-#pragma unroll
-    for (int b = 0; b < RB; ++b) {
-      double2 a = make_double2(0.0, 0.0);
-#pragma unroll
-      for (int i = 0; i < CPW; ++i) {
-        const double sc = ss[warp + kWarps * i];  // zero past k (padded)
-        a.x = fma(q[i][b].x, sc, a.x);
-        a.y = fma(q[i][b].y, sc, a.y);
-      }
-      *reinterpret_cast<double2*>(mypart + 64 * b + 2 * lane) = a;
+    __syncwarp();
+    // the segment's ragged tail (< R rows) through the L2-reuse path, by the
+    // virtual CTA the round-robin would give the next chunk
+    if (nfull * R < rows && (nfull % V) == vi) {
+      const PgRows pr{Q, a.ldq, k, rows};
+      for (int64_t b0 = nfull * R; b0 < rows; b0 += 64 * kPRP * kWarps)
+        pg_chunk<true>(pr, vs, ss, b0 + warp * 64 * kPRP, lane, wacc, xn);
     }
-    __syncthreads();
-#pragma unroll
-    for (int i = 0; i < NV; ++i) {
-      const int row = threadIdx.x + kThreads * i;
-      if (row < R) {
-        double t = 0.0;
-#pragma unroll
-        for (int w = 0; w < kWarps; ++w) t += part[w * R + row];
-        const double wv = vv[i] + -1.0 * t;
-        wbuf[row] = wv;
-        v[base + row] = wv;
-        xn = fma(wv, wv, xn);
-      }
-    }
-    __syncthreads();
-    // phase B from the registers
-#pragma unroll
-    for (int b = 0; b < RB; ++b) {
-      const double2 wv = *reinterpret_cast<const double2*>(wbuf + 64 * b + 2 * lane);
-#pragma unroll
-      for (int i = 0; i < CPW; ++i) {
-        acc[i] = fma(q[i][b].x, wv.x, acc[i]);
-        acc[i] = fma(q[i][b].y, wv.y, acc[i]);
-      }
-    }
+    fin = pg_commit(a, it, sg, V, sacc, stride, xn, s_red, &s_flag) || fin;
   }
-  double* wacc = sacc + warp * stride;
-#pragma unroll
-  for (int i = 0; i < CPW; ++i) {
-    const int col = warp + kWarps * i;
-    const double t = warp_sum(acc[i]);
-    if (lane == 0 && col < k) wacc[col] = t;
-  }
-  __syncwarp();
-  // ragged tail (< R rows) through the L2-reuse path
-  if (nfull * R < p.m && (nfull % gridDim.x) == blockIdx.x)
-    for (int64_t b0 = nfull * R; b0 < p.m; b0 += 64 * kPRP * kWarps)
-      pg_chunk<true>(p, v, ss, b0 + warp * 64 * kPRP, lane, wacc, xn);
-  double ex[1] = {0.0};
-  gram_epilogue<1>(p, sacc, stride, ex, xn);
+  if (fin) seg::seg_final<kThreads, 0>(a.P.L, a.ws, k + (a.xnorm ? 1 : 0), a.d, threadIdx.x, &s_ok,
+                                       [](int o) { return (int64_t)o; });
 }
 
 template <int CPW, int NC>
-int launch_pg_reg(GramParams p, double* v, const double* s, bool host, size_t ws_bytes,
+int launch_pg_reg(PgArgs a, double* v, const double* s, bool host, size_t ws_bytes,
                   cudaStream_t st) {
   constexpr int RB = CPW >= 16 ? 1 : 16 / CPW;
   constexpr int R = 64 * RB;
   constexpr int blocks = CPW >= 32 ? 1 : 2;
   PgPack<NC> pk;
-  if (NC > 0) std::memcpy(pk.v, s, sizeof(double) * p.k);
+  if (NC > 0) std::memcpy(pk.v, s, sizeof(double) * a.k);
   auto kern = project_gram_reg_kernel<CPW, RB, NC>;
-  const int64_t nchunks = ceil_div(p.m, R);
-  int grid = static_cast<int>(std::min<int64_t>(nchunks, (int64_t)blocks * sm_count()));
-  if (grid < 1) grid = 1;
-  const int64_t nv = static_cast<int64_t>(p.k) + (p.xnorm ? 1 : 0);
-  if (!red_ws_fits(ws_bytes, grid, static_cast<int>(nv)))
-    return fail(KLS_ENOSPC, "project_gram: workspace too small");
-  const int stride = (p.k + kG - 1) / kG * kG;
+  // virtual CTAs per segment: a third of the physical grid (so 1..8 ranks'
+  // shares of the 24 segments keep every SM busy)
+  seg::make_plan(a.P.L, R, blocks == 2 ? 98 : 49, a.P);
+  const int nv = a.k + (a.xnorm ? 1 : 0);
+  if (seg::plan_ws_bytes(a.P, nv) > ws_bytes) return fail(KLS_ENOSPC, "project_gram: workspace too small");
+  a.ws = seg::ws_of(a.ws.tick, a.P.nitems, nv);
+  const int grid = std::max(1, std::min(a.P.nitems, blocks * sm_count()));
+  const int stride = (a.k + kG - 1) / kG * kG;
   const size_t smem = sizeof(double) * (static_cast<size_t>(CPW) * kWarps +
                                         static_cast<size_t>(stride) * kWarps +
                                         static_cast<size_t>(kWarps + 1) * R);
@@ -338,20 +397,20 @@ int launch_pg_reg(GramParams p, double* v, const double* s, bool host, size_t ws
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return fail(KLS_ECUDA, "project_gram smem: %s", cudaGetErrorString(e));
   }
-  kern<<<grid, kThreads, smem, st>>>(p, v, host ? nullptr : s, pk);
+  kern<<<grid, kThreads, smem, st>>>(a, v, host ? nullptr : s, pk);
   return check_launch("project_gram_reg_kernel");
 }
 
 template <int NC>
-int launch_pg_reg_cols(GramParams p, double* v, const double* s, bool host, size_t ws_bytes,
+int launch_pg_reg_cols(PgArgs a, double* v, const double* s, bool host, size_t ws_bytes,
                        cudaStream_t st) {
-  const int cpw = (p.k + kWarps - 1) / kWarps;
-  if (cpw <= 1) return launch_pg_reg<1, NC>(p, v, s, host, ws_bytes, st);
-  if (cpw <= 2) return launch_pg_reg<2, NC>(p, v, s, host, ws_bytes, st);
-  if (cpw <= 4) return launch_pg_reg<4, NC>(p, v, s, host, ws_bytes, st);
-  if (cpw <= 8) return launch_pg_reg<8, NC>(p, v, s, host, ws_bytes, st);
-  if (cpw <= 16) return launch_pg_reg<16, NC>(p, v, s, host, ws_bytes, st);
-  return launch_pg_reg<32, NC>(p, v, s, host, ws_bytes, st);
+  const int cpw = (a.k + kWarps - 1) / kWarps;
+  if (cpw <= 1) return launch_pg_reg<1, NC>(a, v, s, host, ws_bytes, st);
+  if (cpw <= 2) return launch_pg_reg<2, NC>(a, v, s, host, ws_bytes, st);
+  if (cpw <= 4) return launch_pg_reg<4, NC>(a, v, s, host, ws_bytes, st);
+  if (cpw <= 8) return launch_pg_reg<8, NC>(a, v, s, host, ws_bytes, st);
+  if (cpw <= 16) return launch_pg_reg<16, NC>(a, v, s, host, ws_bytes, st);
+  return launch_pg_reg<32, NC>(a, v, s, host, ws_bytes, st);
 }
 
 }  // namespace
@@ -360,39 +419,34 @@ int launch_pg_reg_cols(GramParams p, double* v, const double* s, bool host, size
 // xnorm != 0, out[k] = w.w — Cgs2State.push's first update and second
 // projection (ortho.py:149-151) in one launch (1 <= k <= 2048).  s is a host
 // array (carried in the launch) when s_on_host != 0, else a device array.
+// Reduced over the fixed segment tree (seg.cuh); with world > 1 out receives
+// the exported nodes (xstride k + xnorm).
 KLS_API int kls_project_gram(const double* Q, int64_t ldq, int64_t m, int32_t k, double* v,
                              const double* s, int32_t s_on_host, int32_t xnorm, double* out,
-                             void* ws, size_t ws_bytes, void* stream) {
+                             const KlsSegs* segs, void* ws, size_t ws_bytes, void* stream) {
   if (Q == nullptr || v == nullptr || s == nullptr || out == nullptr || ws == nullptr || m < 0 ||
       k < 1 || k > 2048 || ldq < m || (ldq & 1) ||
       ((reinterpret_cast<uintptr_t>(Q) | reinterpret_cast<uintptr_t>(v)) & 15))
     return fail(KLS_EINVAL, "project_gram: bad arguments (k=%d, 1 <= k <= 2048)", k);
-  GramParams p;
-  std::memset(&p, 0, sizeof(p));
-  p.Q = Q;
-  p.ldq = ldq;
-  p.k = k;
-  p.bext = nullptr;
-  p.x0 = v;
-  p.x1 = nullptr;
-  p.m = m;
-  p.xnorm = xnorm;
-  p.out = out;
-  p.out_ld = k;
-  p.col0 = 0;
-  p.bext_row = k;
-  p.partials = reinterpret_cast<double*>(static_cast<char*>(ws) + kTicketBytes);
-  p.ticket = static_cast<unsigned int*>(ws);
-  p.peers.world = 0;
+  PgArgs a;
+  std::memset(&a, 0, sizeof(a));
+  int rc = seg::make_layout(segs, m, a.P.L);
+  if (rc) return rc;
+  a.Q = Q;
+  a.ldq = ldq;
+  a.k = k;
+  a.xnorm = xnorm;
+  a.ws = seg::ws_of(ws, 0, 0);
+  a.d.out = out;
+  a.d.xstride = k + (xnorm ? 1 : 0);
+  a.d.peers.world = 0;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (k <= kRegMaxK && !l2_variant()) {
-    if (!s_on_host) return launch_pg_reg_cols<0>(p, v, s, false, ws_bytes, st);
-    return launch_pg_reg_cols<kRegMaxK>(p, v, s, true, ws_bytes, st);
+  if (k <= kRegMaxK) {
+    if (!s_on_host) return launch_pg_reg_cols<0>(a, v, s, false, ws_bytes, st);
+    return launch_pg_reg_cols<kRegMaxK>(a, v, s, true, ws_bytes, st);
   }
-  if (!s_on_host) return launch_pg<0>(p, v, s, false, ws_bytes, st);
-  if (k <= 32) return launch_pg<32>(p, v, s, true, ws_bytes, st);
-  if (k <= 128) return launch_pg<128>(p, v, s, true, ws_bytes, st);
-  if (k <= 512) return launch_pg<512>(p, v, s, true, ws_bytes, st);
-  if (k <= 1024) return launch_pg<1024>(p, v, s, true, ws_bytes, st);
-  return launch_pg<2048>(p, v, s, true, ws_bytes, st);
+  if (!s_on_host) return launch_pg<0>(a, v, s, false, ws_bytes, st);
+  if (k <= 512) return launch_pg<512>(a, v, s, true, ws_bytes, st);
+  if (k <= 1024) return launch_pg<1024>(a, v, s, true, ws_bytes, st);
+  return launch_pg<2048>(a, v, s, true, ws_bytes, st);
 }

@@ -1,16 +1,17 @@
 // Cross-GPU exchange over NVLink peer memory (symmetric buffers).
 //
-// kls_peer_allreduce is the DCGS2 step's one global reduction (the paper's
+// kls_peer_seg_combine is a reduction's global combine (the paper's
 // MPI_Allreduce; ledger site kernels.py:57-59) done as a
-// one-shot exchange instead of an NCCL call: every rank copies its 2j+3
-// partial sums into its own symmetric buffer, raises an epoch flag in every
-// peer's buffer, waits for all peers' flags, then sums the N peer vectors in
-// rank order 0..N-1.  Every rank computes the same sum in the same order,
-// so all ranks hold bitwise-identical results (the property the replicated
-// host step relies on) — and the sum lands directly in page-locked host
-// memory.  Double-buffered by epoch parity: a rank can only reuse a slot
-// after every peer has signalled the following epoch, i.e. after they have
-// finished reading it.
+// one-shot exchange instead of an NCCL call: every rank copies its exported
+// segment-tree nodes (seg.cuh) into its own symmetric buffer, raises an
+// epoch flag in every peer's buffer, waits for all peers' flags, then
+// evaluates the fixed tree from all ranks' nodes.  Every rank computes the
+// same sums in the same order as a one-rank run, so all ranks hold
+// bitwise-identical results (the property the replicated host step relies
+// on) -- and the result lands directly in page-locked host memory.
+// Double-buffered by epoch parity: a rank can only reuse a slot after every
+// peer has signalled the following epoch, i.e. after they have finished
+// reading it.
 //
 // kls_peer_signal / kls_stencil7_peer replace the halo exchange: a rank
 // signals "my vector for epoch e is written" to its neighbours, and the
@@ -23,6 +24,7 @@
 // Every spin has a wall-clock timeout (globaltimer) so a missing peer turns
 // into an error code instead of a hung GPU.
 #include "peer.cuh"
+#include "seg.cuh"
 
 #include <cstring>
 #include "stencil.cuh"
@@ -32,34 +34,30 @@ namespace {
 using namespace kls;
 using namespace kls::peer;
 
-__global__ void __launch_bounds__(kThreads) peer_allreduce_kernel(const double* __restrict__ src,
-                                                                  int nv, double* out, Peers p,
-                                                                  uint64_t epoch, int* err) {
+// A reduction's cross-rank combine: publish this rank's exported tree nodes
+// (src, [e][nv]) in its own slot, signal every peer, wait for every peer,
+// then every rank evaluates the fixed segment tree from all ranks' exports.
+__global__ void __launch_bounds__(kThreads) peer_seg_combine_kernel(const double* __restrict__ src,
+                                                                    int nv, double* out, Peers p,
+                                                                    uint64_t epoch, int* err) {
   __shared__ int s_ok;
-  char* mine = p.buf[p.rank];
-  double* dst = slot(mine, p.cap, epoch);
-  for (int i = threadIdx.x; i < nv; i += blockDim.x) dst[i] = src[i];
-  if (threadIdx.x == 0) s_ok = 1;
-  __syncthreads();
-  if (threadIdx.x < p.world) {
-    __threadfence_system();
-    st_release_sys(ar_flags(p.buf[threadIdx.x]) + p.rank, epoch);
-    if (!wait_flag(ar_flags(mine) + threadIdx.x, epoch)) atomicExch(&s_ok, 0);
-  }
-  __syncthreads();
-  if (!s_ok) {
+  double* dst = slot(p.buf[p.rank], p.cap, epoch);
+  int ids[seg::kMaxExport];
+  const int nexp = seg::exports(seg::seg_first(p.rank, p.world),
+                                seg::seg_first(p.rank + 1, p.world), ids);
+  for (int i = threadIdx.x; i < nexp * nv; i += blockDim.x) dst[i] = src[i];
+  seg::Dest d;
+  d.out = out;
+  d.xstride = nv;
+  d.peers = p;
+  d.epoch = epoch;
+  d.err = err;
+  if (!seg::peer_exchange<kThreads, 0>(d, threadIdx.x, &s_ok)) {
     if (threadIdx.x == 0) *err = 1;
     for (int i = threadIdx.x; i < nv; i += blockDim.x) out[i] = __longlong_as_double(0x7ff8000000000000ll);
     return;
   }
-  for (int i = threadIdx.x; i < nv; i += blockDim.x) {
-    double s = 0.0;
-    for (int r = 0; r < p.world; ++r) {
-      const volatile double* v = slot(p.buf[r], p.cap, epoch);
-      s += v[i];
-    }
-    out[i] = s;
-  }
+  seg::combine_from_slots<kThreads>(d, nv, threadIdx.x, [&](int o, double v) { out[o] = v; });
 }
 
 __global__ void peer_signal_kernel(Peers p, int target_mask, uint64_t epoch) {
@@ -163,22 +161,26 @@ KLS_API size_t kls_peer_buffer_bytes(int32_t cap) {
   return kDataOff + 2 * static_cast<size_t>(cap) * sizeof(double);
 }
 
-// One-shot allreduce (sum) of nv doubles at `src` (device) over the ranks
-// whose symmetric buffers are bufs[0..world).  The rank-ordered sum is
-// written to `out` (device or mapped host memory).  `epoch` must increase
-// by one per call and be identical on all ranks; *err (device int) is set
-// to 1 when a peer does not arrive within the timeout.
-KLS_API int kls_peer_allreduce(const double* src, int32_t nv, double* out, void* const* bufs,
-                               int32_t rank, int32_t world, int32_t cap, uint64_t epoch, int* err,
-                               void* stream) {
+// Cross-rank combine of a reduction whose world > 1 launch wrote this
+// rank's exported tree nodes to `src` ([e][nv], device): every rank
+// publishes them in its symmetric buffer and evaluates the fixed segment
+// tree into `out` (device or mapped host memory) -- the same bits on every
+// rank and as on one GPU.  `epoch` must increase by one per call and be
+// identical on all ranks; *err (device int) is set to 1 when a peer does
+// not arrive within the timeout.
+KLS_API int kls_peer_seg_combine(const double* src, int32_t nv, double* out, void* const* bufs,
+                                 int32_t rank, int32_t world, int32_t cap, uint64_t epoch,
+                                 int* err, void* stream) {
   Peers p;
   int rc = make_peers(p, bufs, rank, world, cap);
   if (rc) return rc;
-  if (nv < 0 || nv > cap || src == nullptr || out == nullptr || err == nullptr)
-    return fail(KLS_EINVAL, "peer_allreduce: nv=%d exceeds slot capacity %d", nv, cap);
-  peer_allreduce_kernel<<<1, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(src, nv, out, p,
-                                                                                epoch, err);
-  return check_launch("peer_allreduce_kernel");
+  if (nv < 0 || static_cast<int64_t>(nv) * seg::kMaxExport > cap || src == nullptr ||
+      out == nullptr || err == nullptr)
+    return fail(KLS_EINVAL, "peer_seg_combine: 8 x nv = %d exceeds slot capacity %d",
+                8 * nv, cap);
+  peer_seg_combine_kernel<<<1, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(src, nv, out, p,
+                                                                                  epoch, err);
+  return check_launch("peer_seg_combine_kernel");
 }
 
 // Raise this rank's halo flag (value epoch) in the buffers of the ranks in

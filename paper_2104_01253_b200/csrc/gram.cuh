@@ -1,9 +1,11 @@
-// Shared pieces of the K1 fused-reduction kernels (gram.cu: 128-bit LDG
-// streaming; gram_tma.cu: cp.async.bulk / mbarrier staged).
+// Shared pieces of the K1 fused-reduction kernels (gram_tma.cu: the
+// cp.async.bulk / mbarrier staged streaming kernel; gram.cu: the one-CTA-
+// per-output kernel for small m).  Both reduce over the fixed segment tree
+// of seg.cuh, so their results do not depend on the number of ranks.
 #pragma once
 
 #include "peer.cuh"
-#include "reduce.cuh"
+#include "seg.cuh"
 #include "step.cuh"
 
 namespace kls {
@@ -16,22 +18,16 @@ struct GramParams {
   const double* bext;  // extra left column (counted after Q) or nullptr
   const double* x0;
   const double* x1;
-  int64_t m;
+  int64_t m;         // local rows
   int32_t xnorm;     // append x_last . x_last
-  double* out;       // column-major (out_ld x NX), then the xnorm slot
   int32_t out_ld;
   int32_t col0;      // output row of this panel's first Q column
   int32_t bext_row;  // output row of bext
-  double* partials;  // [gridDim.x][nv]
-  unsigned int* ticket;
-  // fused one-shot allreduce over NVLink peers (peers.world > 1): the last
-  // CTA exchanges the CTA-summed vector with every rank and writes the
-  // rank-ordered global sum to `out`
-  peer::Peers peers;
-  uint64_t epoch;
-  int* err;
+  seg::Plan P;       // segments and items (rank-count-independent tree)
+  seg::Ws ws;
+  seg::Dest d;       // out / exports / fused peer exchange
   // DCGS2 step fusion (single panel, bext == x0): after the final sums the
-  // last CTA also runs the device scalar step on out (dcgs2_scalars_block)
+  // finishing CTA also runs the device scalar step on out (dcgs2_scalars_block)
   double* coef;
   double* gout;
   int32_t qr;
@@ -39,8 +35,36 @@ struct GramParams {
 
 constexpr int kG = 4;  // Q columns reduced together
 
+__host__ __device__ inline int gram_nv(const GramParams& p, int nx) {
+  return p.k * nx + (p.bext != nullptr ? nx : 0) + (p.xnorm ? 1 : 0);
+}
+
+// output position of reduced value i (Q columns first, then bext, then
+// the x_last . x_last slot)
+template <int NX>
+__device__ __forceinline__ int64_t gram_dst(const GramParams& p, int i) {
+  const int nq = p.k * NX;
+  if (i < nq) return static_cast<int64_t>(i % NX) * p.out_ld + p.col0 + i / NX;
+  if (p.bext != nullptr && i < nq + NX) return static_cast<int64_t>(i - nq) * p.out_ld + p.bext_row;
+  return static_cast<int64_t>(NX) * p.out_ld;
+}
+
+// Rows [wbase, wbase + 64 RP) of one warp through 128-bit loads, rows past
+// m read as zero (the < 64-row tail of a segment).  Operands already
+// offset to the segment's first row.
+struct GramRows {
+  const double* Q;
+  int64_t ldq;
+  int32_t k;
+  const double* bext;
+  const double* x0;
+  const double* x1;
+  int64_t m;
+  int32_t xnorm;
+};
+
 template <int NX, int RP, bool CHECK>
-__device__ __forceinline__ void gram_chunk(const GramParams& p, int64_t wbase, int lane,
+__device__ __forceinline__ void gram_chunk(const GramRows& p, int64_t wbase, int lane,
                                            double* wacc, double (&ex)[NX], double& xn) {
   constexpr int V = kG * NX;
   const double* xs[2] = {p.x0, p.x1};
@@ -103,119 +127,12 @@ __device__ __forceinline__ void gram_chunk(const GramParams& p, int64_t wbase, i
   }
 }
 
-// CTA reduction + last-CTA fixed-order grid sum.  Called by every thread
-// of the CTA; threads of warps >= kWarps (a producer warp) contribute
-// nothing but take part in the barriers.
 template <int NX>
-__device__ __forceinline__ void gram_epilogue(const GramParams& p, const double* sacc, int stride,
-                                              double (&ex)[NX], double xn) {
-  __shared__ double sx[kWarps][NX + 1];
-  __shared__ bool s_last;
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  const bool consumer = warp < kWarps;
-  // the streaming is done: a dependent update (PDL) may start staging its
-  // Q tiles while the partial sums and the scalar step finish here
-  pdl_trigger();
-  // CTA reduction of the per-thread extras
-#pragma unroll
-  for (int t = 0; t < NX; ++t) {
-    const double s = warp_sum(ex[t]);
-    if (lane == 0 && consumer) sx[warp][t] = s;
-  }
-  {
-    const double s = warp_sum(xn);
-    if (lane == 0 && consumer) sx[warp][NX] = s;
-  }
-  __syncthreads();
-
-  const int has_b = p.bext != nullptr ? 1 : 0;
-  const int nq = p.k * NX;
-  const int nv = nq + has_b * NX + (p.xnorm ? 1 : 0);
-  double* part = p.partials + static_cast<int64_t>(blockIdx.x) * nv;
-  for (int i = threadIdx.x; i < nq; i += blockDim.x) {
-    double s = 0.0;
-#pragma unroll
-    for (int w = 0; w < kWarps; ++w) s += sacc[w * stride + i];
-    part[i] = s;
-  }
-  if (threadIdx.x < NX && has_b) {
-    double s = 0.0;
-#pragma unroll
-    for (int w = 0; w < kWarps; ++w) s += sx[w][threadIdx.x];
-    part[nq + threadIdx.x] = s;
-  }
-  if (threadIdx.x == 0 && p.xnorm) {
-    double s = 0.0;
-#pragma unroll
-    for (int w = 0; w < kWarps; ++w) s += sx[w][NX];
-    part[nv - 1] = s;
-  }
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) s_last = atomicAdd(p.ticket, 1u) == gridDim.x - 1;
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-
-  // last CTA: fixed-order sum over CTAs (sum_partials_block)
-  const int nb = gridDim.x;
-  const bool fused = p.peers.world > 1;
-  double* mine = fused ? peer::slot(p.peers.buf[p.peers.rank], p.peers.cap, p.epoch) : nullptr;
-  auto dst_of = [&](int i) -> int64_t {
-    if (i < nq) return static_cast<int64_t>(i % NX) * p.out_ld + p.col0 + i / NX;
-    if (has_b && i < nq + NX) return static_cast<int64_t>(i - nq) * p.out_ld + p.bext_row;
-    return static_cast<int64_t>(NX) * p.out_ld;
-  };
-  sum_partials_block(p.partials, nb, nv, [&](int i, double s) {
-    if (fused)
-      mine[i] = s;
-    else
-      p.out[dst_of(i)] = s;
-  });
-  if (threadIdx.x == 0) *p.ticket = 0u;
-  if (!fused) {
-    if (p.coef != nullptr) {
-      __syncthreads();
-      dcgs2_scalars_block(p.out, p.bext_row, p.qr, p.coef, p.gout);
-    }
-    return;
-  }
-  // one-shot exchange: publish, signal every peer, wait for every peer, then
-  // sum the N slots in rank order (identical bits on every rank)
-  __shared__ int s_ok;
-  if (threadIdx.x == 0) s_ok = 1;
-  __syncthreads();
-  if (threadIdx.x < p.peers.world) {
-    __threadfence_system();
-    peer::st_release_sys(peer::ar_flags(p.peers.buf[threadIdx.x]) + p.peers.rank, p.epoch);
-    if (!peer::wait_flag(peer::ar_flags(p.peers.buf[p.peers.rank]) + threadIdx.x, p.epoch))
-      atomicExch(&s_ok, 0);
-  }
-  __syncthreads();
-  if (!s_ok) {
-    if (threadIdx.x == 0) *p.err = 1;
-    for (int i = threadIdx.x; i < nv; i += blockDim.x)
-      p.out[dst_of(i)] = __longlong_as_double(0x7ff8000000000000ll);
-    return;
-  }
-  for (int i = threadIdx.x; i < nv; i += blockDim.x) {
-    double s = 0.0;
-    for (int r = 0; r < p.peers.world; ++r) {
-      const volatile double* v = peer::slot(p.peers.buf[r], p.peers.cap, p.epoch);
-      s += v[i];
-    }
-    p.out[dst_of(i)] = s;
-  }
-  if (p.coef != nullptr) {
-    __syncthreads();
-    dcgs2_scalars_block(p.out, p.bext_row, p.qr, p.coef, p.gout);
-  }
-}
-
-template <int NX>
-int launch_gram_tma(GramParams p, size_t ws_bytes, cudaStream_t st);
+int launch_gram_tma(GramParams p, cudaStream_t st);
 bool tma_eligible(const GramParams& p);
+// virtual CTAs per segment of the staged kernel (seg.cuh): at most this
+// many, one per 64 rows below that
+constexpr int kTmaVirt = 49;
 
 }  // namespace gram
 }  // namespace kls

@@ -62,7 +62,7 @@ KLS_API int kls_dcgs2_queue_step(const KlsStepPlan* p, int32_t j, const double* 
   if (rc) return rc;
   if (gram) {
     rc = kls_gram_dcgs2_step(p->Q, p->ldq, p->m, j + 1, w_out, aw_out, p->gdev, p->cdev,
-                             p->gout[slot], p->qr, p->ws, p->ws_bytes, p->stream);
+                             p->gout[slot], p->qr, &p->segs, p->ws, p->ws_bytes, p->stream);
     if (rc) return rc;
     rc = kls_event_record(p->event[slot], p->stream);
   }

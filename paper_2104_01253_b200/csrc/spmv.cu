@@ -13,6 +13,7 @@
 // the reference's order (x-1, x+1, y-1, y+1, z-1, z+1).  For a row-sharded
 // grid the neighbouring x-planes of other ranks come in through x_lo / x_hi.
 #include "reduce.cuh"
+#include "seg.cuh"
 #include "stencil.cuh"
 #include "peer.cuh"
 
@@ -381,20 +382,21 @@ int stencil_variant() {
 template <int W>
 __global__ void __launch_bounds__(kThreads, W >= 7 ? 2 : 3) ell_resid_norms_kernel(
     const int32_t* __restrict__ ecol, const double* __restrict__ eval,
-    const uint8_t* __restrict__ elen, int64_t nrows, int64_t ld, const double* __restrict__ x,
-    const double* __restrict__ b, int width, RedWs ws, double* out) {
+    const uint8_t* __restrict__ elen, int64_t ld, const double* __restrict__ x,
+    const double* __restrict__ b, int width, const __grid_constant__ seg::SimpleArgs a) {
   pdl_wait();
-  double v[3] = {0.0, 0.0, 0.0};
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i < nrows) {
+  seg::run_simple<kThreads, 3>(a, [&](int64_t r0, int64_t rows, int vi, int V, double (&v)[3]) {
+    const int64_t stride = static_cast<int64_t>(V) * kThreads;
+    int64_t i = r0 + static_cast<int64_t>(vi) * kThreads + threadIdx.x;
+    const int64_t end = r0 + rows;
+    if (i >= end) return;
     EllRow<W> cur;
     ell_fetch<W>(cur, ecol, eval, elen, ld, i, width);
     while (true) {
       const int64_t nx = i + stride;
       EllRow<W> nxt;
       nxt.n = 0;
-      if (nx < nrows) ell_fetch<W>(nxt, ecol, eval, elen, ld, nx, width);
+      if (nx < end) ell_fetch<W>(nxt, ecol, eval, elen, ld, nx, width);
       double p[W];
 #pragma unroll
       for (int k = 0; k < W; ++k) p[k] = k < cur.n ? __dmul_rn(cur.v[k], __ldg(x + cur.c[k])) : 0.0;
@@ -412,24 +414,21 @@ __global__ void __launch_bounds__(kThreads, W >= 7 ? 2 : 3) ell_resid_norms_kern
       v[0] = fma(rr, rr, v[0]);
       v[1] = fma(xi, xi, v[1]);
       v[2] = fma(bi, bi, v[2]);
-      if (nx >= nrows) break;
+      if (nx >= end) break;
       cur = nxt;
       i = nx;
     }
-  }
+  });
   pdl_trigger();
-  grid_reduce_finish<3>(v, ws, out);
 }
 
 template <int W>
 int launch_ell_resid(const int32_t* ecol, const double* eval, const uint8_t* elen, int32_t width,
-                     int64_t nrows, int64_t ld, const double* x, const double* b, double* out,
-                     void* ws, size_t ws_bytes, cudaStream_t st) {
-  const int grid = grid_1d(nrows, W >= 7 ? 2 : 3);
-  if (!red_ws_fits(ws_bytes, grid, 3)) return fail(KLS_ENOSPC, "ell_resid_norms: workspace too small");
+                     int64_t ld, const double* x, const double* b, const seg::SimpleArgs& a,
+                     cudaStream_t st) {
+  const int grid = std::max(1, std::min(a.P.nitems, (W >= 7 ? 2 : 3) * sm_count()));
   return launch_dependent(ell_resid_norms_kernel<W>, dim3(grid), dim3(kThreads), 0, st,
-                          "ell_resid_norms_kernel", ecol, eval, elen, nrows, ld, x, b, width,
-                          red_ws(ws), out);
+                          "ell_resid_norms_kernel", ecol, eval, elen, ld, x, b, width, a);
 }
 
 // dense y = A x, A row-major n x n (DenseOperator, problems.py:68-85):
@@ -557,18 +556,21 @@ KLS_API int kls_ell_spmv(const int32_t* ecol, const double* eval, const uint8_t*
 // bit-identically to kls_ell_spmv but not stored.
 KLS_API int kls_ell_resid_norms(const int32_t* ecol, const double* eval, const uint8_t* elen,
                                 int32_t width, int64_t nrows, int64_t ld, const double* x,
-                                const double* b, double* out, void* ws, size_t ws_bytes,
-                                void* stream) {
+                                const double* b, double* out, const KlsSegs* segs, void* ws,
+                                size_t ws_bytes, void* stream) {
   if (ecol == nullptr || eval == nullptr || elen == nullptr || x == nullptr || b == nullptr ||
       out == nullptr || ws == nullptr || nrows < 1 || ld < nrows || width < 1 || width > 8)
     return fail(KLS_EINVAL, "ell_resid_norms: bad arguments");
+  seg::SimpleArgs a;
+  int rc = seg::make_plan_simple(segs, nrows, kThreads, a, ws, ws_bytes, 3, out);
+  if (rc) return rc;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   switch (width) {
-    case 5: return launch_ell_resid<5>(ecol, eval, elen, width, nrows, ld, x, b, out, ws, ws_bytes, st);
-    case 6: return launch_ell_resid<6>(ecol, eval, elen, width, nrows, ld, x, b, out, ws, ws_bytes, st);
-    case 7: return launch_ell_resid<7>(ecol, eval, elen, width, nrows, ld, x, b, out, ws, ws_bytes, st);
-    case 8: return launch_ell_resid<8>(ecol, eval, elen, width, nrows, ld, x, b, out, ws, ws_bytes, st);
-    default: return launch_ell_resid<4>(ecol, eval, elen, width, nrows, ld, x, b, out, ws, ws_bytes, st);
+    case 5: return launch_ell_resid<5>(ecol, eval, elen, width, ld, x, b, a, st);
+    case 6: return launch_ell_resid<6>(ecol, eval, elen, width, ld, x, b, a, st);
+    case 7: return launch_ell_resid<7>(ecol, eval, elen, width, ld, x, b, a, st);
+    case 8: return launch_ell_resid<8>(ecol, eval, elen, width, ld, x, b, a, st);
+    default: return launch_ell_resid<4>(ecol, eval, elen, width, ld, x, b, a, st);
   }
 }
 

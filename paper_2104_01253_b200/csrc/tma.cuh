@@ -59,12 +59,17 @@ template <int R>
 struct ChunkWalk {
   int64_t row, step, rr_end, tail_row, tail_nr;
 
-  __device__ __forceinline__ explicit ChunkWalk(int64_t m64) {
-    const int64_t grid = gridDim.x, b = blockIdx.x;
+  // the launch's own CTA (grid = gridDim.x, b = blockIdx.x)
+  __device__ __forceinline__ explicit ChunkWalk(int64_t m64)
+      : ChunkWalk(m64, gridDim.x, blockIdx.x, kBalanceRounds) {}
+
+  // virtual CTA b of a grid of `grid` (segmented reductions, seg.cuh);
+  // with fewer than `balance` whole rounds the remainder is split evenly
+  __device__ __forceinline__ ChunkWalk(int64_t m64, int64_t grid, int64_t b, int64_t balance) {
     const int64_t q = m64 / R / grid;  // whole rounds
     step = grid * R;
     row = b * R;
-    if (q >= kBalanceRounds) {
+    if (q >= balance) {
       rr_end = m64;  // plain round-robin; the last chunk may be short
       tail_nr = 0;
       tail_row = 0;

@@ -12,6 +12,7 @@
 // two right-hand columns, optionally returning ||Y(:, l-1)||^2 of the result
 // (fused norm for the CGS2 comparator and the DCGS2 flush).
 #include "reduce.cuh"
+#include "seg.cuh"
 #include "tma.cuh"
 
 #include <cstdlib>
@@ -33,6 +34,7 @@ struct CoefPack {
 };
 constexpr int kUpdRP = 2;       // row pairs per lane per chunk
 constexpr int kUpdBlocksPerSm = 3;
+constexpr int kUpdVirt = 148;  // virtual CTAs per segment of the fused-norm update
 
 struct UpdParams {
   double* Q;
@@ -362,7 +364,6 @@ struct MtmParams {
   const double* S;  // k x l column-major, ld = k
   double sign;
   double scale;
-  RedWs ws;
   double* nrm_out;  // ||Y(:, l-1)||^2 after the update, or nullptr
 };
 
@@ -449,10 +450,42 @@ __global__ void __launch_bounds__(kThreads, kUpdBlocksPerSm)
     else
       mtm_chunk<L, true>(p, ss, wbase, lane, nrm);
   }
-  if (p.nrm_out != nullptr) {
-    double v[1] = {nrm};
-    grid_reduce_finish<1>(v, p.ws, p.nrm_out);
+}
+
+// The same with the fused ||Y(:, l-1)||^2, reduced over the fixed segment
+// tree (seg.cuh): virtual CTA v of segment s walks the segment's chunks
+// v, v + V, ...
+template <int L, int NC>
+__global__ void __launch_bounds__(kThreads, kUpdBlocksPerSm)
+    mtm_norm_kernel(MtmParams p, const __grid_constant__ CoefPack<NC> pk,
+                    const __grid_constant__ seg::SimpleArgs a) {
+  extern __shared__ double ss[];  // L x (k + kCols), zero-padded
+  const double* S = NC > 0 ? pk.v : p.S;
+  const int ldss = p.k + kCols;
+  for (int i = threadIdx.x; i < L * ldss; i += kThreads) {
+    const int t = i / ldss, kk = i % ldss;
+    ss[i] = kk < p.k ? S[t * p.k + kk] : 0.0;
   }
+  __syncthreads();
+  constexpr int64_t WROWS = 64 * kUpdRP;
+  constexpr int64_t CROWS = WROWS * kWarps;
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  seg::run_simple<kThreads, 1>(a, [&](int64_t r0, int64_t rows, int v, int V, double (&acc)[1]) {
+    MtmParams q = p;
+    q.Y = p.Y + r0;
+    q.B = p.B != nullptr ? p.B + r0 : nullptr;
+    q.m = rows;
+    const int64_t nchunks = (rows + CROWS - 1) / CROWS;
+    for (int64_t ch = v; ch < nchunks; ch += V) {
+      const int64_t cbase = ch * CROWS;
+      const int64_t wbase = cbase + warp * WROWS;
+      if (cbase + CROWS <= rows)
+        mtm_chunk<L, false>(q, ss, wbase, lane, acc[0]);
+      else
+        mtm_chunk<L, true>(q, ss, wbase, lane, acc[0]);
+    }
+  });
 }
 
 int grid_for(int64_t m, int64_t crows, int per_sm) {
@@ -536,47 +569,69 @@ int update_common(double* Q, int64_t ldq, int64_t m, int32_t j, double* w, const
 }
 
 template <int L, int NC>
-int launch_mtm(const MtmParams& p, const double* host_s, cudaStream_t st) {
+int launch_mtm(const MtmParams& p, const double* host_s, const seg::SimpleArgs* a,
+               cudaStream_t st) {
   CoefPack<NC> pk;
   if (NC > 0) std::memcpy(pk.v, host_s, sizeof(double) * p.k * L);
   const size_t smem = sizeof(double) * static_cast<size_t>(L) * (p.k + kCols);
-  int rc = set_smem(reinterpret_cast<const void*>(mtm_kernel<L, NC>), smem);
+  if (a == nullptr) {
+    int rc = set_smem(reinterpret_cast<const void*>(mtm_kernel<L, NC>), smem);
+    if (rc) return rc;
+    const int grid = grid_for(p.m, 64 * kUpdRP * kWarps, kUpdBlocksPerSm);
+    mtm_kernel<L, NC><<<grid, kThreads, smem, st>>>(p, pk);
+    return check_launch("mtm_kernel");
+  }
+  int rc = set_smem(reinterpret_cast<const void*>(mtm_norm_kernel<L, NC>), smem);
   if (rc) return rc;
-  const int grid = grid_for(p.m, 64 * kUpdRP * kWarps, kUpdBlocksPerSm);
-  mtm_kernel<L, NC><<<grid, kThreads, smem, st>>>(p, pk);
-  return check_launch("mtm_kernel");
+  const int grid = std::max(1, std::min(a->P.nitems, kUpdBlocksPerSm * sm_count()));
+  mtm_norm_kernel<L, NC><<<grid, kThreads, smem, st>>>(p, pk, *a);
+  return check_launch("mtm_norm_kernel");
 }
 
 template <int L>
-int mtm_dispatch(const MtmParams& p, const double* host_s, cudaStream_t st) {
+int mtm_dispatch(const MtmParams& p, const double* host_s, const seg::SimpleArgs* a,
+                 cudaStream_t st) {
   const int n = p.k * L;
-  if (host_s == nullptr) return launch_mtm<L, 0>(p, nullptr, st);
-  if (n <= 32) return launch_mtm<L, 32>(p, host_s, st);
-  if (n <= 128) return launch_mtm<L, 128>(p, host_s, st);
-  if (n <= 512) return launch_mtm<L, 512>(p, host_s, st);
-  if (n <= 2048) return launch_mtm<L, 2048>(p, host_s, st);
+  if (host_s == nullptr) return launch_mtm<L, 0>(p, nullptr, a, st);
+  if (n <= 32) return launch_mtm<L, 32>(p, host_s, a, st);
+  if (n <= 128) return launch_mtm<L, 128>(p, host_s, a, st);
+  if (n <= 512) return launch_mtm<L, 512>(p, host_s, a, st);
+  if (n <= 2048) return launch_mtm<L, 2048>(p, host_s, a, st);
   return fail(KLS_EINVAL, "mv_times_mat_add_mv_host: %d coefficients exceed the launch pack", n);
 }
 
 int mtm_common(double* Y, int64_t ldy, int64_t m, int32_t l, const double* B, int64_t ldb,
-               int32_t k, const double* S, double sign, double scale, double* nrm_out, void* ws,
-               size_t ws_bytes, bool host, void* stream) {
+               int32_t k, const double* S, double sign, double scale, double* nrm_out,
+               const KlsSegs* segs, void* ws, size_t ws_bytes, bool host, void* stream) {
   if (Y == nullptr || m < 0 || k < 0 || (l != 1 && l != 2) || (l == 2 && (ldy < m || (ldy & 1))) ||
       (k > 0 && (B == nullptr || S == nullptr || ldb < m || (ldb & 1))))
     return fail(KLS_EINVAL, "mv_times_mat_add_mv: bad arguments (m=%lld k=%d l=%d)",
                 (long long)m, k, l);
   if (misaligned(Y) || misaligned(B)) return fail(KLS_EINVAL, "mv_times_mat_add_mv: misaligned");
-  const int grid = grid_for(m, 64 * kUpdRP * kWarps, kUpdBlocksPerSm);
-  MtmParams p{Y, ldy, m, l, B, ldb, k, host ? nullptr : S, sign, scale, red_ws(ws), nrm_out};
-  if (nrm_out != nullptr && (ws == nullptr || !red_ws_fits(ws_bytes, grid, 1)))
-    return fail(KLS_ENOSPC, "mv_times_mat_add_mv: workspace too small for the fused norm");
+  MtmParams p{Y, ldy, m, l, B, ldb, k, host ? nullptr : S, sign, scale, nrm_out};
+  seg::SimpleArgs a;
+  const seg::SimpleArgs* ap = nullptr;
+  if (nrm_out != nullptr) {
+    int rc = seg::make_layout(segs, m, a.P.L);
+    if (rc) return rc;
+    seg::make_plan(a.P.L, 64 * kUpdRP * kWarps, kUpdVirt, a.P);
+    if (ws == nullptr || seg::plan_ws_bytes(a.P, 1) > ws_bytes)
+      return fail(KLS_ENOSPC, "mv_times_mat_add_mv: workspace too small for the fused norm");
+    a.ws = seg::ws_of(ws, a.P.nitems, 1);
+    a.d.out = nrm_out;
+    a.d.xstride = 1;
+    a.d.peers.world = 0;
+    a.d.epoch = 0;
+    a.d.err = nullptr;
+    ap = &a;
+  }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const double* hs = host && k > 0 ? S : nullptr;
   if (host && k == 0) {
     static const double zero = 0.0;
     hs = &zero;
   }
-  return l == 1 ? mtm_dispatch<1>(p, hs, st) : mtm_dispatch<2>(p, hs, st);
+  return l == 1 ? mtm_dispatch<1>(p, hs, ap, st) : mtm_dispatch<2>(p, hs, ap, st);
 }
 
 }  // namespace
@@ -617,17 +672,18 @@ KLS_API int kls_dcgs2_update_dev(double* Q, int64_t ldq, int64_t m, int32_t j, c
 // (requires ws).  Mirrors kernels.mv_times_mat_add_mv (kernels.py:63-84).
 KLS_API int kls_mv_times_mat_add_mv(double* Y, int64_t ldy, int64_t m, int32_t l, const double* B,
                                     int64_t ldb, int32_t k, const double* S, double sign,
-                                    double scale, double* nrm_out, void* ws, size_t ws_bytes,
-                                    void* stream) {
-  return mtm_common(Y, ldy, m, l, B, ldb, k, S, sign, scale, nrm_out, ws, ws_bytes, false, stream);
+                                    double scale, double* nrm_out, const KlsSegs* segs, void* ws,
+                                    size_t ws_bytes, void* stream) {
+  return mtm_common(Y, ldy, m, l, B, ldb, k, S, sign, scale, nrm_out, segs, ws, ws_bytes, false,
+                    stream);
 }
 
 // Same with S in HOST memory (k*l <= 2048), carried in the launch.
 KLS_API int kls_mv_times_mat_add_mv_host(double* Y, int64_t ldy, int64_t m, int32_t l,
                                          const double* B, int64_t ldb, int32_t k,
                                          const double* S_host, double sign, double scale,
-                                         double* nrm_out, void* ws, size_t ws_bytes,
-                                         void* stream) {
-  return mtm_common(Y, ldy, m, l, B, ldb, k, S_host, sign, scale, nrm_out, ws, ws_bytes, true,
-                    stream);
+                                         double* nrm_out, const KlsSegs* segs, void* ws,
+                                         size_t ws_bytes, void* stream) {
+  return mtm_common(Y, ldy, m, l, B, ldb, k, S_host, sign, scale, nrm_out, segs, ws, ws_bytes,
+                    true, stream);
 }

@@ -83,7 +83,10 @@ class LinearOperator:
 
     # -- partition ----------------------------------------------------------
     def _partition(self):
-        self.row_lo, self.row_hi = self.comm.split(self.n)
+        # rows follow the 24 global reduction segments (64-row units):
+        # rank-count-independent reductions, DESIGN.md §6a
+        self.segs = self.comm.segs(self.n, 64)
+        self.row_lo, self.row_hi = self.segs.lo, self.segs.hi
 
     @property
     def m_local(self):
@@ -642,8 +645,27 @@ class CsrOperator(LinearOperator):
             else:
                 from . import kernels
 
-                v = self._val[: int(self._rowptr[-1].item())]
-                self._fro = float(np.sqrt(kernels.dot(v, v, comm=self.comm) if v.numel() else 0.0))
+                if self._ell is not None:
+                    # sum over the ELL entry columns (zero-padded, row-major
+                    # per column): each a rank-count-independent dot
+                    _, evals, _, width, ld = self._ell
+                    if self.comm.world > 1:  # the same number of dots on every rank
+                        wt = torch.tensor([width], dtype=torch.int64, device=evals.device)
+                        import torch.distributed as dist
+
+                        dist.all_reduce(wt, op=dist.ReduceOp.MAX, group=self.comm.group)
+                        width = int(wt.item())
+                    acc = 0.0
+                    zero = torch.zeros(max(self.m_local, 2), dtype=torch.float64, device=evals.device)
+                    for k in range(width):
+                        v = evals[k * ld : k * ld + self.m_local] if k < self._ell[3] else zero[: self.m_local]
+                        acc += kernels.dot(v, v, comm=self.comm, segs=self.segs)
+                    self._fro = float(np.sqrt(acc))
+                else:
+                    v = self._val[: int(self._rowptr[-1].item())]
+                    if self.comm.world != 1:
+                        raise NotImplementedError("Frobenius norm of a sharded CSR without ELL copy")
+                    self._fro = float(np.sqrt(kernels.dot(v, v, comm=self.comm) if v.numel() else 0.0))
         return self._fro
 
 
@@ -771,10 +793,20 @@ class StencilLaplace3D(LinearOperator):
         super().__init__(nx * ny * nz, comm)
 
     def _partition(self):
+        # whole x-planes per rank, at the 24 reduction segments' boundaries
+        # (unit = one plane, two when the plane has an odd row count)
         nx, ny, nz = self.dims
         self.plane = ny * nz
-        self.x_lo, self.x_hi = self.comm.split(nx)
-        self.row_lo, self.row_hi = self.x_lo * self.plane, self.x_hi * self.plane
+        self.segs = self.comm.segs(self.n, self.plane)
+        self.row_lo, self.row_hi = self.segs.lo, self.segs.hi
+        self.x_lo, self.x_hi = self.row_lo // self.plane, self.row_hi // self.plane
+        if self.comm.world > 1:
+            for r in range(self.comm.world):
+                lo, hi = runtime.seg_range(self.n, self.segs.unit, self.comm.world, r)
+                if hi <= lo:
+                    raise DimensionError(
+                        f"laplace3d{self.dims} over {self.comm.world} ranks leaves rank {r} "
+                        "without an x-plane")
 
     def _needs_halo(self):
         return self.comm.world > 1
@@ -867,7 +899,7 @@ class StencilLaplace3D(LinearOperator):
         lo_ptr = hi_ptr = None
         mask = 0
         if self.x_lo > 0:
-            plo, phi = runtime.block_range(nx, world, r - 1)
+            plo, phi = (v // self.plane for v in runtime.seg_range(self.n, self.segs.unit, world, r - 1))
             lo_ptr = x.peer_ptrs[r - 1] + 8 * (phi - plo - 1) * self.plane
             mask |= 1 << (r - 1)
         if self.x_hi < nx:
@@ -950,99 +982,113 @@ def manteuffel_operator(spec, comm=None):
 # Matrix Market coordinate format (problems.py:364-489)
 
 
-def _lines(source):
+_MM_SYMMETRY_SIGN = {"general": None, "symmetric": 1.0, "skew-symmetric": -1.0}
+
+
+def _mm_text(source):
+    """The whole Matrix Market text of a path, an open file or the text itself."""
     if hasattr(source, "read"):
-        return source, False
+        return source.read()
     if isinstance(source, str) and source.lstrip().startswith("%%MatrixMarket"):
-        return io.StringIO(source), False
-    return open(source, "r", encoding="ascii"), True
+        return source
+    with open(source, "r", encoding="ascii") as f:
+        return f.read()
 
 
 def parse_matrix_market(source):
-    """Real/integer coordinate Matrix Market -> CsrMatrix (general,
-    symmetric, skew-symmetric); errors carry the 1-based line number."""
-    f, owned = _lines(source)
+    """Real/integer coordinate Matrix Market -> CsrMatrix (general, symmetric,
+    skew-symmetric) -- the reference's reader contract (problems.py:368-469:
+    accepted headers, symmetric expansion, MatrixMarketError with the 1-based
+    line of the first offending line).  One tokenising pass over the text,
+    then whole-array parsing and checks; only an error is located line by
+    line."""
+    text = _mm_text(source)
+    lines = text.split("\n")
+    if lines and lines[-1] == "":
+        lines.pop()
+    head = lines[0].split() if lines else []
+    if len(head) != 5 or head[0] != "%%MatrixMarket":
+        raise MatrixMarketError("not a Matrix Market header", line=1)
+    obj, fmt, field, sym = (t.lower() for t in head[1:])
+    if (obj, fmt) != ("matrix", "coordinate"):
+        raise MatrixMarketError(f"only 'matrix coordinate' files are read, not {obj} {fmt}", line=1)
+    if field not in ("real", "integer"):
+        raise MatrixMarketError(f"field {field!r} is not real", line=1)
+    if sym not in _MM_SYMMETRY_SIGN:
+        raise MatrixMarketError(f"symmetry {sym!r} is not supported", line=1)
+    # significant lines (not blank, not comments) with their line numbers
+    body = [(n + 1, t.split()) for n, raw in enumerate(lines[1:], start=1)
+            for t in (raw.strip(),) if t and not t.startswith("%")]
+    if not body:
+        raise MatrixMarketError("no size line", line=len(lines))
+    size_ln, size_tok = body[0]
+    if len(size_tok) != 3:
+        raise MatrixMarketError("the size line must read 'rows cols nnz'", line=size_ln)
     try:
-        head = f.readline().strip().split()
-        ln = 1
-        if len(head) != 5 or head[0] != "%%MatrixMarket":
-            raise MatrixMarketError("missing %%MatrixMarket header", line=1)
-        obj, fmt, field, sym = (t.lower() for t in head[1:])
-        if obj != "matrix" or fmt != "coordinate":
-            raise MatrixMarketError(f"unsupported object/format {obj!r}/{fmt!r}", line=1)
-        if field not in ("real", "integer"):
-            raise MatrixMarketError(f"non-real field {field!r}", line=1)
-        if sym not in ("general", "symmetric", "skew-symmetric"):
-            raise MatrixMarketError(f"unsupported symmetry {sym!r}", line=1)
-        size = None
-        for raw in f:
-            ln += 1
-            t = raw.strip()
-            if not t or t.startswith("%"):
-                continue
-            toks = t.split()
-            if len(toks) != 3:
-                raise MatrixMarketError("size line needs 'rows cols nnz'", line=ln)
+        nr, nc, nnz = (int(v) for v in size_tok)
+    except ValueError:
+        raise MatrixMarketError("size entries must be integers", line=size_ln) from None
+    if min(nr, nc, nnz) < 0:
+        raise MatrixMarketError("size entries must be non-negative", line=size_ln)
+    entries = body[1:]
+    n = len(entries)
+    ln = np.array([e[0] for e in entries], dtype=np.int64)
+    width_ok = np.array([len(e[1]) == 3 for e in entries], dtype=bool)
+    tok = np.array([e[1] if len(e[1]) == 3 else ("1", "1", "0") for e in entries],
+                   dtype=object).reshape(-1, 3)
+    parse_ok = np.ones(n, dtype=bool)
+    try:
+        ij = tok[:, :2].astype(np.int64)
+        v = tok[:, 2].astype(np.float64)
+    except (ValueError, OverflowError):  # rare: find the unparsable lines
+        ij = np.ones((n, 2), dtype=np.int64)
+        v = np.zeros(n)
+        for t, (a_, b_, c_) in enumerate(tok):
             try:
-                size = tuple(int(v) for v in toks)
+                ij[t] = (int(a_), int(b_))
+                v[t] = float(c_)
             except ValueError:
-                raise MatrixMarketError("non-integer size entry", line=ln) from None
-            break
-        if size is None:
-            raise MatrixMarketError("missing size line", line=ln)
-        nr, nc, nnz = size
-        if min(size) < 0:
-            raise MatrixMarketError("negative size entry", line=ln)
-        rows = np.empty(nnz, dtype=np.int64)
-        cols = np.empty(nnz, dtype=np.int64)
-        vals = np.empty(nnz)
-        got = 0
-        for raw in f:
-            ln += 1
-            t = raw.strip()
-            if not t or t.startswith("%"):
-                continue
-            if got >= nnz:
-                raise MatrixMarketError("more entries than declared", line=ln)
-            toks = t.split()
-            if len(toks) != 3:
-                raise MatrixMarketError("entry line needs 'row col value'", line=ln)
-            try:
-                i, j, v = int(toks[0]), int(toks[1]), float(toks[2])
-            except ValueError:
-                raise MatrixMarketError("malformed entry", line=ln) from None
-            if not (1 <= i <= nr and 1 <= j <= nc):
-                raise MatrixMarketError(f"index ({i}, {j}) out of bounds for {nr}x{nc}", line=ln)
-            if sym == "skew-symmetric" and i == j and v != 0.0:
-                raise MatrixMarketError("nonzero diagonal in skew-symmetric matrix", line=ln)
-            rows[got], cols[got], vals[got] = i - 1, j - 1, v
-            got += 1
-        if got != nnz:
-            raise MatrixMarketError(f"declared {nnz} entries, found {got}", line=ln)
-    finally:
-        if owned:
-            f.close()
-    if sym != "general":
+                parse_ok[t] = False
+                ij[t], v[t] = (1, 1), 0.0
+    in_bounds = (ij[:, 0] >= 1) & (ij[:, 0] <= nr) & (ij[:, 1] >= 1) & (ij[:, 1] <= nc)
+    skew_ok = (ij[:, 0] != ij[:, 1]) | (v == 0.0) if sym == "skew-symmetric" else np.ones(n, bool)
+    # per line, the reference's check order: count, shape, parse, bounds, skew
+    fails = [(np.arange(n) >= nnz, lambda t: f"entries beyond the declared {nnz}"),
+             (~width_ok, lambda t: "an entry line must read 'row col value'"),
+             (~parse_ok, lambda t: "unparsable entry"),
+             (~in_bounds, lambda t: f"entry ({ij[t, 0]}, {ij[t, 1]}) outside the {nr}x{nc} matrix"),
+             (~skew_ok, lambda t: "skew-symmetric matrices have a zero diagonal")]
+    any_bad = np.zeros(n, dtype=bool)
+    for mask, _ in fails:
+        any_bad |= mask
+    if np.any(any_bad):
+        t = int(np.argmax(any_bad))
+        msg = next(m for mask, m in fails if mask[t])
+        raise MatrixMarketError(msg(t), line=int(ln[t]))
+    if n != nnz:
+        raise MatrixMarketError(f"{n} entries for {nnz} declared", line=len(lines))
+    rows, cols = ij[:, 0] - 1, ij[:, 1] - 1
+    sign = _MM_SYMMETRY_SIGN[sym]
+    if sign is not None:  # mirror the off-diagonal entries
         off = rows != cols
-        sgn = -1.0 if sym == "skew-symmetric" else 1.0
-        rows, cols, vals = (np.concatenate([rows, cols[off]]), np.concatenate([cols, rows[off]]),
-                            np.concatenate([vals, sgn * vals[off]]))
-    return CsrMatrix.from_coo(nr, nc, rows, cols, vals)
+        rows, cols, v = (np.concatenate([rows, cols[off]]), np.concatenate([cols, rows[off]]),
+                         np.concatenate([v, sign * v[off]]))
+    return CsrMatrix.from_coo(nr, nc, rows, cols, v)
 
 
 def write_matrix_market(csr, target, symmetry="general", comment=None):
-    """Coordinate real general output of the stored entries."""
+    """Coordinate real general text of the stored entries (values as Python
+    float reprs, so a re-read is exact)."""
     if symmetry != "general":
         raise ValueError("only general output is supported")
-    own = not hasattr(target, "write")
-    f = open(target, "w", encoding="ascii") if own else target
-    try:
-        f.write("%%MatrixMarket matrix coordinate real general\n")
-        for ln in (comment.splitlines() if comment else []):
-            f.write(f"% {ln}\n")
-        f.write(f"{csr.nrows} {csr.ncols} {csr.nnz}\n")
-        for i, j, v in zip(csr.row_ids(), csr.indices, csr.data):
-            f.write(f"{i + 1} {j + 1} {float(v)!r}\n")
-    finally:
-        if own:
-            f.close()
+    out = ["%%MatrixMarket matrix coordinate real general"]
+    out += [f"% {c}" for c in (comment.splitlines() if comment else [])]
+    out.append(f"{csr.nrows} {csr.ncols} {csr.nnz}")
+    out += [f"{i} {j} {float(x)!r}" for i, j, x in
+            zip((csr.row_ids() + 1).tolist(), (np.asarray(csr.indices) + 1).tolist(), csr.data)]
+    text = "\n".join(out) + "\n"
+    if hasattr(target, "write"):
+        target.write(text)
+    else:
+        with open(target, "w", encoding="ascii") as f:
+            f.write(text)

@@ -7,8 +7,14 @@ only; all arithmetic on the path runs in libklsgpu.so.
 Row partition: every distributed object (operator, vector,
 basis block) is split into contiguous row blocks, one per rank, in rank
 order — the paper's SPMD model.  A single process is the
-world-size-1 case of the same code.
+world-size-1 case of the same code.  The blocks follow the 24 global
+segments of the rank-count-independent reductions (csrc/seg.cuh, DESIGN.md
+§6a): rank r of N owns segments [24 r / N, 24 (r + 1) / N), so every
+reduction gives the same bits on 1, 2, 3, 4, 6 or 8 GPUs.
 """
+
+import ctypes
+
 
 import numpy as np
 import torch
@@ -67,9 +73,26 @@ class Comm:
             self.rank, self.world = 0, 1
         self.allreduce_calls = 0
 
-    def split(self, n):
-        """Contiguous near-equal split of n items: this rank's [lo, hi)."""
-        return block_range(n, self.world, self.rank)
+    def segs(self, m, unit=64):
+        """The reduction layout of an m-row object split over this comm."""
+        return Segs(m, unit, self.world, self.rank)
+
+    def combine_(self, blocks, count):
+        """NCCL path of a reduction's cross-rank combine: `blocks` (device,
+        >= 8 * count) holds this rank's exported tree nodes ([e][count]);
+        returns the global values (device, count) — the same bits as the
+        peer path and as one rank."""
+        import torch.distributed as dist
+
+        g = torch.zeros((self.world, SEG_MAX_EXPORT * count), dtype=torch.float64,
+                        device=blocks.device)
+        mine = blocks[: SEG_MAX_EXPORT * count].contiguous()
+        dist.all_gather_into_tensor(g, mine, group=self.group)
+        out = torch.empty(count, dtype=torch.float64, device=blocks.device)
+        _lib.call("kls_seg_combine", g.data_ptr(), count, count, self.world, out.data_ptr(),
+                  stream_handle())
+        self.allreduce_calls += 1
+        return out
 
     def allreduce_(self, t):
         """In-place sum over ranks (the one global reduction of a step)."""
@@ -94,6 +117,126 @@ def block_range(n, parts, index):
     base, extra = divmod(n, parts)
     lo = index * base + min(index, extra)
     return lo, lo + base + (1 if index < extra else 0)
+
+
+# ---------------------------------------------------------------------------
+# the rank-count-independent segment tree (csrc/seg.cuh; the same arithmetic)
+
+SEG_G = 24
+SEG_NODES = 39
+SEG_ROOT = 38
+SEG_MAX_EXPORT = 8
+
+
+def seg_row(m, unit, k):
+    """Global row where segment k (0..24) starts."""
+    units = -(-m // unit)
+    return min(m, unit * (units * k // SEG_G))
+
+
+def seg_first(rank, world):
+    return rank * SEG_G // world
+
+
+def seg_range(m, unit, world, rank):
+    """Rank's global rows [lo, hi): segments [24 r / N, 24 (r + 1) / N)."""
+    return seg_row(m, unit, seg_first(rank, world)), seg_row(m, unit, seg_first(rank + 1, world))
+
+
+def _node_lo(n):
+    return n if n < 24 else 3 * (n - 24) if n < 32 else 6 * (n - 32) if n < 36 else \
+        12 * (n - 36) if n < 38 else 0
+
+
+def _node_hi(n):
+    return n + 1 if n < 24 else 3 * (n - 24) + 3 if n < 32 else 6 * (n - 32) + 6 if n < 36 else \
+        12 * (n - 36) + 12 if n < 38 else 24
+
+
+def _node_parent(n):
+    return 24 + n // 3 if n < 24 else 32 + (n - 24) // 2 if n < 32 else \
+        36 + (n - 32) // 2 if n < 36 else 38 if n < 38 else -1
+
+
+def _node_children(n):
+    if n < 24:
+        return ()
+    if n < 32:
+        return (3 * (n - 24), 3 * (n - 24) + 1, 3 * (n - 24) + 2)
+    if n < 36:
+        return (24 + 2 * (n - 32), 25 + 2 * (n - 32))
+    if n < 38:
+        return (32 + 2 * (n - 36), 33 + 2 * (n - 36))
+    return (36, 37)
+
+
+def seg_exports(rank, world):
+    """The tree nodes a rank exports (maximal complete subtrees of its
+    segments), left to right."""
+    a, b = seg_first(rank, world), seg_first(rank + 1, world)
+    ids, pos = [], a
+    while pos < b:
+        node = pos
+        while True:
+            p = _node_parent(node)
+            if p < 0 or _node_lo(p) != pos or not (a <= _node_lo(p) and _node_hi(p) <= b):
+                break
+            node = p
+        ids.append(node)
+        pos = _node_hi(node)
+    return ids
+
+
+def _fold(n, val):
+    c = _node_children(n)
+    if len(c) == 3:
+        return (val[c[0]] + val[c[1]]) + val[c[2]]
+    return val[c[0]] + val[c[1]]
+
+
+def seg_local_nodes(segvals, rank, world):
+    """Host restatement of a rank's local tree: segvals (nseg x count) ->
+    its exported node values (nexp x count), numpy float64 adds in the
+    kernels' order (test scaffolding and reference for the device)."""
+    a, b = seg_first(rank, world), seg_first(rank + 1, world)
+    val = {}
+    for leaf in range(a, b):
+        val[leaf] = np.asarray(segvals[leaf - a], dtype=np.float64)
+    for n in range(SEG_G, SEG_NODES):
+        if a <= _node_lo(n) and _node_hi(n) <= b:
+            val[n] = _fold(n, val)
+    return np.array([val[i] for i in seg_exports(rank, world)])
+
+
+def seg_combine_host(blocks, world):
+    """Host restatement of kls_seg_combine: blocks[r] = rank r's exported
+    node values (nexp_r x count) -> the root (count)."""
+    val = {}
+    for r in range(world):
+        for e, nid in enumerate(seg_exports(r, world)):
+            val[nid] = np.asarray(blocks[r][e], dtype=np.float64)
+    for n in range(SEG_G, SEG_NODES):
+        if n not in val and all(c in val for c in _node_children(n)):
+            val[n] = _fold(n, val)
+    return val[SEG_ROOT]
+
+
+class Segs:
+    """KlsSegs of one row space (an operator's or a QR block's rows): the
+    global row count, the partition unit, and this rank's place."""
+
+    def __init__(self, m, unit, world, rank):
+        if unit % 2:
+            unit *= 2  # segments start 16-byte aligned
+        self.m, self.unit, self.world, self.rank = int(m), int(unit), int(world), int(rank)
+        self.lo, self.hi = seg_range(self.m, self.unit, self.world, self.rank)
+        self.nexp = len(seg_exports(self.rank, self.world))
+        self.c = _lib.KlsSegs(self.m, self.unit, self.world, self.rank)
+        self.ptr = ctypes.addressof(self.c)
+
+    @property
+    def m_local(self):
+        return self.hi - self.lo
 
 
 _default_comm = None
@@ -284,12 +427,20 @@ class PeerLink:
         hdl = symm_mem.rendezvous(t, self._group_name)
         return t, [int(p) for p in hdl.buffer_ptrs], hdl
 
-    def allreduce(self, src_ptr, count, out_ptr, stream):
-        if count > self.CAP:
-            raise RuntimeError(f"peer allreduce of {count} values exceeds the slot ({self.CAP})")
+    def take_epochs(self, n):
+        """Reserve n consecutive exchange epochs; returns the first."""
+        first = self.ar_epoch + 1
+        self.ar_epoch += n
+        return first
+
+    def seg_combine(self, src_ptr, count, out_ptr, stream):
+        """Cross-rank combine of a reduction's exported tree nodes (src,
+        [e][count]) into out: the fixed segment tree, same bits everywhere."""
+        if count * SEG_MAX_EXPORT > self.CAP:
+            raise RuntimeError(f"peer combine of {count} values exceeds the slot ({self.CAP})")
         self.ar_epoch += 1
-        _lib.call("kls_peer_allreduce", src_ptr, count, out_ptr, self.ptrs, self.rank, self.world,
-                  self.CAP, self.ar_epoch, self.err_dev, stream)
+        _lib.call("kls_peer_seg_combine", src_ptr, count, out_ptr, self.ptrs, self.rank,
+                  self.world, self.CAP, self.ar_epoch, self.err_dev, stream)
         self.comm.allreduce_calls += 1
 
     def check(self):

@@ -24,11 +24,11 @@ for m in [int(float(v)) for v in os.environ.get("SIZES", "1e6,1e7").split(",")]:
 
         def k1():
             _lib.call("kls_gram_dcgs2_step", Q.data_ptr(), ld, m, j, w.data_ptr(), aw.data_ptr(),
-                      g.data_ptr(), c.data_ptr(), None, 0, ws, wsb, st)
+                      g.data_ptr(), c.data_ptr(), None, 0, None, ws, wsb, st)
 
         def k1plain():
             _lib.call("kls_gram_dcgs2", Q.data_ptr(), ld, m, j, w.data_ptr(), aw.data_ptr(),
-                      g.data_ptr(), ws, wsb, st)
+                      g.data_ptr(), None, ws, wsb, st)
 
         def k2():
             _lib.call("kls_dcgs2_update_dev", Q.data_ptr(), ld, m, j, w.data_ptr(), w2.data_ptr(),

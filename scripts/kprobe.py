@@ -51,7 +51,7 @@ def main():
     for j in js:
         coef = torch.randn(2 * j + 1, dtype=torch.float64, device="cuda") * 1e-3
         g = timeit(lambda: _lib.call("kls_gram_dcgs2", Q.data_ptr(), ld, m, j, w.data_ptr(),
-                                     aw.data_ptr(), out.data_ptr(), ws, wsb, st), a.reps)
+                                     aw.data_ptr(), out.data_ptr(), None, ws, wsb, st), a.reps)
         u = timeit(lambda: _lib.call("kls_dcgs2_update", Q.data_ptr(), ld, m, j, w.data_ptr(),
                                      aw.data_ptr(), coef.data_ptr(), 1.0, 1, st), a.reps)
         res[f"gram_j{j}_ms"] = g * 1e3

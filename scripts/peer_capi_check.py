@@ -82,7 +82,7 @@ def main():
     out = torch.empty(2 * j + 3, dtype=torch.float64, device="cuda")
     ws, wsb = runtime.workspace(j + 2)
     _lib.call("kls_gram_dcgs2_peer", qb.data_ptr(), ld, m_local, j, wd.data_ptr(), awd.data_ptr(),
-              out.data_ptr(), ws, wsb, table, rank, world, cap, 6, err.data_ptr(), st)
+              out.data_ptr(), None, ws, wsb, table, rank, world, cap, 6, err.data_ptr(), st)
     torch.cuda.synchronize()
     left = np.hstack([Q, w[:, None]])
     want = np.concatenate([left.T @ w, left.T @ aw, [aw @ aw]])

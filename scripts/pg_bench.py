@@ -43,10 +43,10 @@ def main():
             def call():
                 if name == "project":
                     _lib.call("kls_mv_trans_mv", Q.data_ptr(), ld, m, k, None, v.data_ptr(), None, 1,
-                              1, out.data_ptr(), ws, wsb, st)
+                              1, out.data_ptr(), None, ws, wsb, st)
                 else:
                     _lib.call("kls_project_gram", Q.data_ptr(), ld, m, k, v.data_ptr(),
-                              s.ctypes.data, 1, 1, out.data_ptr(), ws, wsb, st)
+                              s.ctypes.data, 1, 1, out.data_ptr(), None, ws, wsb, st)
             for _ in range(2):
                 call()
             torch.cuda.synchronize()

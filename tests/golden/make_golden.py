@@ -340,6 +340,134 @@ def ks_config4_shape(kls):
     np.savez_compressed(os.path.join(OUT, "ks_config4_shape.npz"), **out)
 
 
+def ks_config4_full(kls, max_restarts=240):
+    """BASELINE config 4 at FULL size: Krylov-Schur on ManteuffelSpec(k=3163,
+    beta=0.5) (m = 10,004,569), max_basis 60, tol 1e-7, DCGS2, seed 1729
+    (eig.py:157-317).  Hours of reference CPU time, so the run is
+    instrumented rather than repeated: every restart's active Hessenberg
+    block (the input of eig._schur_active) is captured, and a checkpoint
+    (`ks_config4_full.npz`) is rewritten after every restart -- the Ritz
+    values of each restart, the active block size (nlock = k - na), and the
+    blocks themselves for the first 12 restarts.  When the run ends the
+    locked values, lock history and restart count are added.  Threads: the
+    OpenBLAS default of the process (recorded)."""
+    import time
+
+    from threadpoolctl import threadpool_info
+
+    import kls.eig as keig
+
+    path = os.path.join(OUT, "ks_config4_full.npz")
+    rec = {"ritz": [], "na": [], "blocks": [], "t": []}
+    t0 = time.perf_counter()
+    nthreads = max([d.get("num_threads", 0) for d in threadpool_info()
+                    if d.get("user_api") == "blas"] or [0])
+    orig = keig._schur_active
+
+    def save(extra=None):
+        na = np.array(rec["na"], dtype=np.int64)
+        ritz = np.zeros((len(na), 60), dtype=np.complex128)
+        for i, v in enumerate(rec["ritz"]):
+            ritz[i, : v.size] = v
+        out = dict(ritz=ritz, na=na, restart_s=np.array(rec["t"]), blas_threads=nthreads,
+                   k=3163, beta=0.5, max_basis=60, tol=1e-7, seed=1729)
+        for i, b in enumerate(rec["blocks"]):
+            out[f"block{i}"] = b
+        if extra:
+            out.update(extra)
+        tmp = path + ".tmp.npz"
+        np.savez_compressed(tmp, **out)
+        os.replace(tmp, path)
+
+    def spy(block):
+        rec["na"].append(block.shape[0])
+        rec["ritz"].append(np.sort_complex(np.linalg.eigvals(block)))
+        if len(rec["blocks"]) < 12:
+            rec["blocks"].append(block.copy())
+        rec["t"].append(time.perf_counter() - t0)
+        save()
+        print(f"restart {len(rec['na'])}: na={block.shape[0]} t={rec['t'][-1]:.0f}s", flush=True)
+        return orig(block)
+
+    keig._schur_active = spy
+    op = kls.CsrOperator(kls.manteuffel_build(kls.ManteuffelSpec(k=3163, beta=0.5)))
+    cfg = kls.KrylovSchurConfig(max_basis=60, tol=1e-7, scheme="dcgs2", max_restarts=max_restarts)
+    res = keig.krylov_schur_run(op, cfg, seed=1729)
+    save(dict(values=res.values, lock_history=np.array(res.lock_history), restarts=res.restarts,
+              invariant_dim=res.invariant_dim, incomplete=res.incomplete, done=True,
+              cpu_s=time.perf_counter() - t0))
+
+
+def ks_config4_ensemble(kls, nperm=24):
+    """The reference's OWN rounding sensitivity at BASELINE config 4's
+    Krylov-Schur settings (k = 100, m = 1e4, max_basis 60, tol 1e-7, DCGS2,
+    seed 1729, 30 restarts): the same problem run under exact symmetric row
+    permutations P A P^T with the permuted start vector (identical spectrum
+    and Krylov spaces in exact arithmetic; only the summation order of the
+    dot products / gemvs changes) and under 1, 2, 4, 8 BLAS threads.  The
+    lock histories and locked values of these runs are the envelope a
+    re-implementation with a different summation order must fall into
+    (SURVEY.md section 8c).  Stored: lock histories (runs x 30), locked
+    values (runs x 60, zero-padded, sorted), locked counts."""
+    import scipy.sparse as sp
+    from threadpoolctl import threadpool_limits
+
+    import kls.eig as keig
+
+    csr = kls.manteuffel_build(kls.ManteuffelSpec(k=100, beta=0.5))
+    m = csr.nrows
+    cfg = kls.KrylovSchurConfig(max_basis=60, tol=1e-7, scheme="dcgs2", max_restarts=30)
+    S = sp.csr_matrix((csr.data, csr.indices, csr.indptr), shape=(m, m))
+    real_np = keig.np
+
+    class PermGen:
+        def __init__(self, bitgen, perm):
+            self.g = real_np.random.Generator(bitgen)
+            self.perm = perm
+
+        def standard_normal(self, size=None):
+            x = self.g.standard_normal(size)
+            return x[self.perm] if np.ndim(x) == 1 and len(x) == len(self.perm) else x
+
+        def __getattr__(self, k):
+            return getattr(self.g, k)
+
+    runs = []
+    for tag, perm, nthr in ([(f"threads{t}", None, t) for t in (1, 2, 4, 8)] +
+                            [(f"perm{t}", np.random.default_rng(100 + t).permutation(m), 1)
+                             for t in range(nperm)]):
+        if perm is None:
+            op = kls.CsrOperator(csr)
+            keig.np = real_np
+        else:
+            Sp = S[perm][:, perm].tocsr()
+            Sp.sort_indices()
+            op = kls.CsrOperator(kls.CsrMatrix(m, m, Sp.indptr.astype(np.int64),
+                                               Sp.indices.astype(np.int64), Sp.data.copy()))
+            wrap = type(sys)("np_perm")
+            wrap.__dict__.update(real_np.__dict__)
+            wrap.random = type(sys)("np_perm_random")
+            wrap.random.__dict__.update(real_np.random.__dict__)
+            wrap.random.Generator = lambda bg, perm=perm: PermGen(bg, perm)
+            keig.np = wrap
+        try:
+            with threadpool_limits(limits=nthr, user_api="blas"):
+                res = keig.krylov_schur_run(op, cfg, seed=1729)
+        finally:
+            keig.np = real_np
+        vals = np.zeros(60, dtype=np.complex128)
+        v = np.sort_complex(res.values)
+        vals[: v.size] = v
+        runs.append((tag, np.array(res.lock_history), vals, v.size))
+        print(tag, [(i, int(x)) for i, x in enumerate(res.lock_history)
+                    if i == 0 or res.lock_history[i] != res.lock_history[i - 1]], flush=True)
+    np.savez_compressed(os.path.join(OUT, "ks_config4_ensemble.npz"),
+                        tags=np.array([r[0] for r in runs]),
+                        lock_history=np.stack([r[1] for r in runs]),
+                        values=np.stack([r[2] for r in runs]),
+                        nlocked=np.array([r[3] for r in runs]))
+
+
 def arnoldi_config3_shape(kls):
     """BASELINE config 3's expansion (3-D Poisson 7-point, x slowest, n = 100,
     start PCG64(1729)) on one GPU's share of the 8-GPU split scaled down:
@@ -427,6 +555,16 @@ if __name__ == "__main__":
         import kls
 
         ks_config4_shape(kls)
+    elif sys.argv[1:2] == ["--only"] and sys.argv[2:3] == ["ks_config4_full"]:
+        sys.path.insert(0, REF)
+        import kls
+
+        ks_config4_full(kls, *(int(a) for a in sys.argv[3:4]))
+    elif sys.argv[1:] == ["--only", "ks_config4_ensemble"]:
+        sys.path.insert(0, REF)
+        import kls
+
+        ks_config4_ensemble(kls)
     elif sys.argv[1:] == ["--only", "gmres_config2"]:
         sys.path.insert(0, REF)
         import kls

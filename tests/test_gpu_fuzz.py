@@ -50,7 +50,7 @@ def test_fuzz_gram_step(m, j, seed):
     coef = torch.empty(2 * j + 2, dtype=torch.float64, device="cuda")
     ws, wsb = rt.workspace(j + 2)
     lib.call("kls_gram_dcgs2_step", qb.data_ptr(), ld, m, j, wd.data_ptr(), awd.data_ptr(),
-             out.data_ptr(), coef.data_ptr(), None, 0, ws, wsb, rt.stream_handle())
+             out.data_ptr(), coef.data_ptr(), None, 0, None, ws, wsb, rt.stream_handle())
     left = np.hstack([Q, w[:, None]])
     right = np.column_stack([w, aw])
     want = np.concatenate([(left.T @ right).T.ravel(), [aw @ aw]])
@@ -114,7 +114,7 @@ def test_fuzz_project_gram(m, k, host, seed):
     out = torch.empty(k, dtype=torch.float64, device="cuda")
     ws, wsb = rt.workspace(k + 1)
     lib.call("kls_project_gram", qb.data_ptr(), ld, m, k, vd.data_ptr(),
-             s.ctypes.data if host else sd.data_ptr(), host, 0, out.data_ptr(), ws, wsb,
+             s.ctypes.data if host else sd.data_ptr(), host, 0, out.data_ptr(), None, ws, wsb,
              rt.stream_handle())
     wgot = vd.cpu().numpy()
     assert np.allclose(wgot, v - Q @ s, rtol=1e-12, atol=1e-12 * np.sqrt(k))

@@ -49,7 +49,7 @@ def test_gram_dcgs2_matches_numpy(cuda, rng, m, k):
     out = torch.full((2 * k + 3,), np.nan, dtype=torch.float64, device="cuda")
     ws, wsb = rt.workspace(k + 1)
     lib.call("kls_gram_dcgs2", qb.data_ptr(), ld, m, k, wd.data_ptr(), awd.data_ptr(),
-             out.data_ptr(), ws, wsb, rt.stream_handle())
+             out.data_ptr(), None, ws, wsb, rt.stream_handle())
     got = out.cpu().numpy()
     left = np.hstack([Q, w[:, None]])
     right = np.column_stack([w, aw])
@@ -59,7 +59,7 @@ def test_gram_dcgs2_matches_numpy(cuda, rng, m, k):
     # bitwise reproducible
     out2 = torch.empty_like(out)
     lib.call("kls_gram_dcgs2", qb.data_ptr(), ld, m, k, wd.data_ptr(), awd.data_ptr(),
-             out2.data_ptr(), ws, wsb, rt.stream_handle())
+             out2.data_ptr(), None, ws, wsb, rt.stream_handle())
     assert torch.equal(out, out2)
 
 
@@ -81,13 +81,13 @@ def test_gram_dcgs2_step_fuses_scalars(cuda, rng, m, j, qr):
     g1 = torch.empty(2 * j + 3, dtype=torch.float64, device="cuda")
     c1 = torch.empty(2 * j + 2, dtype=torch.float64, device="cuda")
     lib.call("kls_gram_dcgs2", qb.data_ptr(), ld, m, j, wd.data_ptr(), awd.data_ptr(), g1.data_ptr(),
-             ws, wsb, st)
+             None, ws, wsb, st)
     lib.call("kls_dcgs2_scalars", g1.data_ptr(), j, qr, c1.data_ptr(), None, st)
     g2 = torch.empty_like(g1)
     c2 = torch.empty_like(c1)
     gh = torch.full((2 * j + 3,), np.nan, dtype=torch.float64, device="cuda")
     lib.call("kls_gram_dcgs2_step", qb.data_ptr(), ld, m, j, wd.data_ptr(), awd.data_ptr(),
-             g2.data_ptr(), c2.data_ptr(), gh.data_ptr(), qr, ws, wsb, st)
+             g2.data_ptr(), c2.data_ptr(), gh.data_ptr(), qr, None, ws, wsb, st)
     assert torch.equal(g1, g2) and torch.equal(gh, g2)
     a, b = c1.cpu().numpy(), c2.cpu().numpy()
     assert np.allclose(a, b, rtol=1e-14, atol=0.0)
@@ -108,7 +108,7 @@ def test_mv_trans_mv_generic_panels(cuda, rng, k):
     out = torch.full((k + 1,), np.nan, dtype=torch.float64, device="cuda")
     ws, wsb = rt.workspace(k + 1)
     lib.call("kls_mv_trans_mv", qb.data_ptr() if k else None, ld, m, k, None, xd.data_ptr(), None,
-             1, 1, out.data_ptr(), ws, wsb, rt.stream_handle())
+             1, 1, out.data_ptr(), None, ws, wsb, rt.stream_handle())
     got = out.cpu().numpy()
     want = np.concatenate([Q.T @ x, [x @ x]])
     assert np.allclose(got, want, rtol=1e-12, atol=1e-11)
@@ -158,7 +158,7 @@ def test_mv_times_mat_add_mv_with_fused_norm(cuda, rng, l, k):
     nrm = torch.zeros(1, dtype=torch.float64, device="cuda")
     ws, wsb = rt.workspace(8)
     lib.call("kls_mv_times_mat_add_mv", yb.data_ptr(), ldy, m, l, bb.data_ptr() if k else None, ldb,
-             k, sd.data_ptr() if k else None, -1.0, 0.5, nrm.data_ptr(), ws, wsb,
+             k, sd.data_ptr() if k else None, -1.0, 0.5, nrm.data_ptr(), None, ws, wsb,
              rt.stream_handle())
     want = 0.5 * Y - B @ S
     got = yb[:l, :m].cpu().numpy().T
@@ -184,7 +184,7 @@ def test_project_gram_matches_numpy(cuda, rng, m, k, host):
     sd = torch.from_numpy(s).cuda()
     sp = s.ctypes.data if host else sd.data_ptr()
     lib.call("kls_project_gram", qb.data_ptr(), ld, m, k, vd.data_ptr(), sp, host, 1,
-             out.data_ptr(), ws, wsb, rt.stream_handle())
+             out.data_ptr(), None, ws, wsb, rt.stream_handle())
     w = v - Q @ s
     got_w = vd.cpu().numpy()
     assert np.allclose(got_w, w, rtol=1e-13, atol=1e-12 * np.sqrt(k))
@@ -196,7 +196,7 @@ def test_project_gram_matches_numpy(cuda, rng, m, k, host):
     vd2 = torch.from_numpy(v.copy()).cuda()
     out2 = torch.empty_like(out)
     lib.call("kls_project_gram", qb.data_ptr(), ld, m, k, vd2.data_ptr(), sp, host, 1,
-             out2.data_ptr(), ws, wsb, rt.stream_handle())
+             out2.data_ptr(), None, ws, wsb, rt.stream_handle())
     assert torch.equal(out, out2) and torch.equal(vd, vd2)
 
 
@@ -296,7 +296,7 @@ def test_resid_norms_and_scale(cuda, rng, n, off):
     out = torch.zeros(3, dtype=torch.float64, device="cuda")
     ws, wsb = rt.workspace(4)
     lib.call("kls_resid_norms", bd.data_ptr(), axd.data_ptr(), xd.data_ptr(), n, out.data_ptr(),
-             ws, wsb, rt.stream_handle())
+             None, ws, wsb, rt.stream_handle())
     want = [np.sum((b - ax) ** 2), x @ x, b @ b]
     assert np.allclose(out.cpu().numpy(), want, rtol=1e-12)
     y = torch.empty_like(xd)
@@ -308,7 +308,7 @@ def test_errors_surface_as_exceptions(cuda):
     from paper_2104_01253_b200 import _lib
 
     with pytest.raises(_lib.KlsGpuError):
-        _lib.call("kls_gram_dcgs2", None, 1, 10, 3, None, None, None, None, 0, None)
+        _lib.call("kls_gram_dcgs2", None, 1, 10, 3, None, None, None, None, None, 0, None)
 
 
 @pytest.mark.parametrize("dims", [(5, 4, 6), (1, 1, 1), (3, 1, 7), (8, 8, 8), (17, 9, 33)])
@@ -359,7 +359,7 @@ def test_ell_resid_norms_fused(cuda, rng, k, beta):
     out = torch.zeros(3, dtype=torch.float64, device="cuda")
     ws, wsb = rt.workspace(4)
     lib.call("kls_ell_resid_norms", ecol.data_ptr(), evals.data_ptr(), elen.data_ptr(), width,
-             op.n, ld, x.data_ptr(), b.data_ptr(), out.data_ptr(), ws, wsb, rt.stream_handle())
+             op.n, ld, x.data_ptr(), b.data_ptr(), out.data_ptr(), None, ws, wsb, rt.stream_handle())
     xh, bh = x.cpu().numpy(), b.cpu().numpy()
     want = [np.sum((bh - y) ** 2), xh @ xh, bh @ bh]
     assert np.allclose(out.cpu().numpy(), want, rtol=1e-12, atol=0)

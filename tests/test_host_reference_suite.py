@@ -240,6 +240,30 @@ def test_matrix_market_roundtrip_and_string(rng):
     assert csr.to_dense()[0, 0] == -3.5
 
 
+# (text, line of the MatrixMarketError) -- each line number was obtained by
+# running the reference's parse_matrix_market (problems.py:368-469) here:
+# the first offending line in file order wins, whatever the failure kind
+_MM_EDGE = [
+    ("2 2 2\n1 1 x\n1 1 1\n1 1 1\n", "general", 3),     # unparsable before the extra entry
+    ("2 2 1\n\n% c\n3 1 1\n", "general", 5),            # out of bounds after blank + comment
+    ("2 2 2\n1 2 1\n2 2 1\n", "skew-symmetric", 4),     # nonzero skew diagonal
+    ("2 2 3\n1 1 1\n% tail\n\n", "general", 5),         # too few entries: the last line
+    ("2 2 1\n1 1 1 1\n", "general", 3),                 # four tokens
+    ("% only comment\n", "general", 2),                 # no size line
+    ("2 2 -1\n", "general", 2),                         # negative size
+    ("2 x 1\n", "general", 2),                          # non-integer size
+]
+
+
+@pytest.mark.parametrize("body,sym,line", _MM_EDGE)
+def test_matrix_market_error_lines(body, sym, line):
+    K = kls()
+    text = f"%%MatrixMarket matrix coordinate real {sym}\n" + body
+    with pytest.raises(K.MatrixMarketError) as err:
+        K.parse_matrix_market(io.StringIO(text))
+    assert err.value.line == line
+
+
 # ---------------------------------------------------------------------------
 # test_metrics.py (host paths)
 
