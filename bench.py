@@ -34,7 +34,8 @@ sys.path.insert(0, ROOT)
 METRIC = "DCGS2 Arnoldi iters/sec + HBM GB/s (fp64) at 1/2/4/8 B200 vs CPU ref"
 UNIT = "iters/s"
 FULL_DIMS = (496, 512, 512)
-SAMPLE_DIMS = (31, 64, 128)  # 1/512 of the rows: ~5 s per expansion on 8 cores
+SAMPLE_DIMS = (124, 128, 128)  # 1/64 of the rows: the cpu_baseline leg's sample
+REF_SAMPLE_DIMS = (62, 64, 128)  # 1/256 of the rows: each --impl reference step
 NOMINAL_HBM_GBS = 8000.0
 FALLBACK_HBM_GBS = 6650.0
 
@@ -52,8 +53,13 @@ def parse():
                     help="matrix-free stencil (the reference's laplace3d) or the same "
                          "operator as a device-assembled CSR matrix")
     ap.add_argument("--sample-dims", default=",".join(map(str, SAMPLE_DIMS)))
+    ap.add_argument("--ref-sample-dims", default=",".join(map(str, REF_SAMPLE_DIMS)))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-configs", action="store_true",
+                    help="skip the configs 1, 2, 4, 5 block (N = 1 only)")
+    ap.add_argument("--traced", type=int, default=2,
+                    help="expansions of the separate traced pass (phase split, roofline)")
     return ap.parse_args()
 
 
@@ -71,36 +77,81 @@ def workload_name(dims, n, scheme, operator="stencil"):
 # CPU side: the reference implementation (or the oracle port) on host cores
 
 
-def cpu_reference_rate(sample_dims, n, scheme, reps=1):
-    """(iters/s at the sample size, kind, seconds per expansion)."""
-    import numpy as np
+def host_info():
+    """The host the CPU legs ran on: model, cores, RAM, numpy / BLAS."""
+    info = {"cpus": os.cpu_count()}
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    info["cpu_model"] = ln.split(":", 1)[1].strip()
+                    break
+        with open("/proc/meminfo") as f:
+            for ln in f:
+                if ln.startswith("MemTotal"):
+                    info["ram_gb"] = round(int(ln.split()[1]) / 2**20, 1)
+                    break
+    except OSError:
+        pass
+    try:
+        import numpy as np
+        from threadpoolctl import threadpool_info
 
+        info["numpy"] = np.__version__
+        blas = [d for d in threadpool_info() if d.get("user_api") == "blas"]
+        if blas:
+            info["blas"] = f"{blas[0].get('internal_api')} {blas[0].get('version')}"
+            info["blas_threads_default"] = blas[0].get("num_threads")
+    except Exception:
+        pass
+    return info
+
+
+def _ref_module():
+    """(module, kind): the unmodified reference from baseline/_ref, else None."""
     ref_dir = os.path.join(ROOT, "baseline", "_ref")
-    kind = "port"
     try:
         if os.path.isdir(os.path.join(ref_dir, "kls")):
-            sys.path.insert(0, ref_dir)
+            if ref_dir not in sys.path:
+                sys.path.insert(0, ref_dir)
             import kls  # the unmodified reference (pip-installed into baseline/_ref)
 
-            kind = "reference"
+            return kls, "reference"
     except Exception:
-        kind = "port"
+        pass
+    return None, "port"
+
+
+def cpu_reference_rate(sample_dims, n, scheme, reps=1, threads=None):
+    """(iters/s at the sample size, kind, seconds per expansion); threads
+    limits the BLAS pool (None: OpenBLAS default = all host cores)."""
+    import contextlib
+
+    import numpy as np
+
+    R, kind = _ref_module()
     m = sample_dims[0] * sample_dims[1] * sample_dims[2]
     start = np.random.Generator(np.random.PCG64(1729)).standard_normal(m)
-    times = []
-    for _ in range(reps):
-        if kind == "reference":
-            op = kls.laplace3d(*sample_dims)
-            t0 = time.perf_counter()
-            kls.arnoldi_expand(op, start, scheme, n)
-            times.append(time.perf_counter() - t0)
-        else:
-            import oracle  # CPU restatement (test infrastructure), baseline leg only
+    ctx = contextlib.nullcontext()
+    if threads is not None:
+        from threadpoolctl import threadpool_limits
 
-            fn = getattr(oracle, f"{scheme}_arnoldi")
-            t0 = time.perf_counter()
-            fn(lambda x: oracle.stencil7_matvec(x, sample_dims), start, n)
-            times.append(time.perf_counter() - t0)
+        ctx = threadpool_limits(limits=threads, user_api="blas")
+    times = []
+    with ctx:
+        for _ in range(reps):
+            if kind == "reference":
+                op = R.laplace3d(*sample_dims)
+                t0 = time.perf_counter()
+                R.arnoldi_expand(op, start, scheme, n)
+                times.append(time.perf_counter() - t0)
+            else:
+                import oracle  # CPU restatement (test infrastructure), baseline leg only
+
+                fn = getattr(oracle, f"{scheme}_arnoldi")
+                t0 = time.perf_counter()
+                fn(lambda x: oracle.stencil7_matvec(x, sample_dims), start, n)
+                times.append(time.perf_counter() - t0)
     return n / statistics.median(times), kind, times
 
 
@@ -109,9 +160,10 @@ def run_reference(args):
     if rank != 0:
         return 0
     dims = dims_of(args.dims)
-    sdims = dims_of(args.sample_dims)
+    sdims = dims_of(args.ref_sample_dims)
     m, ms = dims[0] * dims[1] * dims[2], sdims[0] * sdims[1] * sdims[2]
-    for _ in range(args.warmup):
+    # the CPU needs no warm-up beyond loading: at most one untimed sample
+    for _ in range(min(args.warmup, 1)):
         cpu_reference_rate(sdims, args.n, args.scheme)
     rate, kind, times = cpu_reference_rate(sdims, args.n, args.scheme, reps=max(args.steps, 1))
     value = rate * ms / m
@@ -132,10 +184,14 @@ def run_reference(args):
         "data": "synthetic: PCG64(1729) standard-normal start vector",
         "config": {"workload": workload_name(dims, args.n, args.scheme, args.operator), "m": m, "n": args.n,
                    "sample_rows": ms, "sample_dims": list(sdims),
-                   "extrapolation": "iters/s at the sample size x (sample rows / m)"},
+                   "extrapolation": "iters/s at the sample size x (sample rows / m): every "
+                                    "term of a step is linear in m",
+                   "measured_sample_ms_per_step": 1e3 * statistics.median(times)},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
                          "sample": f"{args.scheme} arnoldi_expand n={args.n} on laplace3d{sdims} "
-                                   f"({ms} rows), {len(times)} timed runs, OpenBLAS default threads"},
+                                   f"({ms} rows, 1/{m // ms} of m), {len(times)} timed runs, "
+                                   f"OpenBLAS default threads"},
+        "host": host_info(),
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -228,20 +284,255 @@ def ncu_traffic(kernel):
     return None
 
 
+def _events_time(fn, reps=1):
+    """Device seconds of reps calls of fn (CUDA events on the current stream,
+    synchronized on both sides) and fn's last result."""
+    import torch
+
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        out = fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) * 1e-3 / reps, out
+
+
+def _traced(fn):
+    """One call of fn with the per-kernel event tracer on: {kernel: (seconds,
+    algorithmic bytes, launches)} (a separate pass: the tracer times each
+    launch from Python, so it bypasses the one-call native step loop)."""
+    from paper_2104_01253_b200 import trace
+
+    rec = trace.start(events=True)
+    try:
+        fn()
+    finally:
+        trace.stop()
+    out = {}
+    for name in ("gram", "update", "project", "project_gram", "mtm", "apply", "resid_norms",
+                 "scale", "rotate"):
+        sec = rec.seconds(name)
+        if sec > 0:
+            out[name] = (sec, rec.bytes[name], rec.calls[name])
+    out["_allreduce"] = (rec.seconds("allreduce"), 0, rec.span_count("allreduce"))
+    out["_halo"] = (rec.seconds("halo"), 0, rec.span_count("halo"))
+    return out
+
+
+def _roofline(spans, peak, peak_src, note=None):
+    kern = max((k for k in spans if not k.startswith("_")), key=lambda k: spans[k][0])
+    sec, nbytes, calls = spans[kern]
+    achieved = nbytes / sec / 1e9
+    r = {"bound": "hbm", "kernel": kern, "achieved": achieved, "peak": peak, "unit": "GB/s",
+         "frac": achieved / peak, "peak_source": peak_src,
+         "frac_of_8TBs": achieved / NOMINAL_HBM_GBS,
+         "bytes_per_launch_avg": nbytes / max(calls, 1),
+         "launch_ms_avg": 1e3 * sec / max(calls, 1)}
+    if note:
+        r["note"] = note
+    return r
+
+
+# ---------------------------------------------------------------------------
+# BASELINE configs 1, 2, 4 and 5 (one GPU), each with its own roofline and a
+# bounded CPU baseline (the reference from baseline/_ref, else the oracle port)
+
+
+def _cpu_time(fn, reps=1, threads=None):
+    import contextlib
+
+    ctx = contextlib.nullcontext()
+    if threads is not None:
+        from threadpoolctl import threadpool_limits
+
+        ctx = threadpool_limits(limits=threads, user_api="blas")
+    ts = []
+    with ctx:
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            fn()
+            ts.append(time.perf_counter() - t0)
+    return statistics.median(ts)
+
+
+def config1(kls, peak, peak_src):
+    """2-D Poisson 100 x 100 (m = 1e4), n = 50, DCGS2 and CGS2 Arnoldi."""
+    import numpy as np
+
+    out = {}
+    op = kls.CsrOperator(kls.manteuffel_build(kls.ManteuffelSpec(k=100, beta=0.0)))
+    start = np.random.Generator(np.random.PCG64(1729)).standard_normal(op.n)
+    R, kind = _ref_module()
+    for scheme in ("dcgs2", "cgs2"):
+        fn = lambda: kls.arnoldi_expand(op, start, scheme, 50)  # noqa: E731
+        fn()
+        sec, _ = _events_time(fn, reps=20)
+        e = {"value": 50 / sec, "unit": "iters/s", "ms_per_expansion": 1e3 * sec}
+        e["roofline"] = _roofline(_traced(fn), peak, peak_src,
+                                  "latency-bound: Q (4 MB) sits in L2; the step is host/launch "
+                                  "latency, not bandwidth")
+        if kind == "reference":
+            rop = R.CsrOperator(R.manteuffel_build(R.ManteuffelSpec(k=100, beta=0.0)))
+            ct = _cpu_time(lambda: R.arnoldi_expand(rop, start, scheme, 50), reps=3)
+            ct1 = _cpu_time(lambda: R.arnoldi_expand(rop, start, scheme, 50), reps=3, threads=1)
+        else:
+            import oracle
+
+            ptr, idx, dat = oracle.manteuffel_csr(100, 0.0)
+            f = getattr(oracle, f"{scheme}_arnoldi")
+            ct = ct1 = _cpu_time(lambda: f(lambda x: oracle.csr_matvec(ptr, idx, dat, x), start, 50))
+        e["cpu_baseline"] = {"value": 50 / ct, "unit": "iters/s", "cores": os.cpu_count(),
+                             "kind": kind, "value_1thread": 50 / ct1,
+                             "sample": "the full workload (m = 1e4, n = 50), 3 runs"}
+        out[scheme] = e
+    return {"workload": "config 1: Arnoldi-QR, 2-D Poisson 5-point 100x100 (m=1e4), n=50, fp64",
+            **out}
+
+
+def config2(kls, peak, peak_src):
+    """Restarted GMRES(50), DCGS2, 1000 x 1000 convection-diffusion (m = 1e6),
+    rtol 1e-6 to convergence."""
+    import numpy as np
+    import torch
+
+    op = kls.manteuffel_operator(kls.ManteuffelSpec(k=1000, beta=0.5))
+    one = op.apply(torch.ones(op.m_local, dtype=torch.float64, device="cuda"))
+    b = one / kls.kernels.norm2(one, comm=op.comm, segs=op.segs)
+    out = {"workload": "config 2: GMRES(50) with DCGS2, 2-D convection-diffusion 1000x1000 "
+                       "(ManteuffelSpec(k=1000, beta=0.5), m=1e6), rtol 1e-6, fp64"}
+    for be in (True, False):
+        cfg = kls.GmresConfig(max_iters=10000, restart=50, rtol=1e-6, scheme="dcgs2",
+                              backward_errors=be)
+        fn = lambda: kls.gmres_solve(op, b, cfg)  # noqa: E731
+        fn()
+        sec, res = _events_time(fn)
+        e = {"value": res.iterations / sec, "unit": "iters/s", "iterations": res.iterations,
+             "converged": bool(res.converged), "seconds": sec}
+        if be:
+            e["roofline"] = _roofline(_traced(fn), peak, peak_src)
+        out["backward_errors" if be else "no_backward_errors"] = e
+    R, kind = _ref_module()
+    bh = b.cpu().numpy()
+    if kind == "reference":
+        rop = R.CsrOperator(R.manteuffel_build(R.ManteuffelSpec(k=1000, beta=0.5)))
+        fn = lambda: R.gmres_solve(rop, bh, R.GmresConfig(max_iters=100, restart=50,  # noqa: E731
+                                                          rtol=1e-6, scheme="dcgs2"))
+    else:
+        import oracle
+
+        ptr, idx, dat = oracle.manteuffel_csr(1000, 0.5)
+        fn = lambda: oracle.gmres(lambda x: oracle.csr_matvec(ptr, idx, dat, x), bh,  # noqa: E731
+                                  float(np.linalg.norm(dat)), 100, 50, 1e-6, "dcgs2")
+    ct = _cpu_time(fn)
+    out["backward_errors"]["cpu_baseline"] = {
+        "value": 100 / ct, "unit": "iters/s", "cores": os.cpu_count(), "kind": kind,
+        "sample": "gmres_solve on the same system, the first 100 iterations (2 restart cycles)"}
+    return out
+
+
+def config4(kls, peak, peak_src, restarts=20):
+    """Krylov-Schur, nonsymmetric convection-diffusion m = 1e7, max_basis 60,
+    DCGS2 basis: restart throughput over the first `restarts` restarts."""
+    import numpy as np
+
+    op = kls.manteuffel_operator(kls.ManteuffelSpec(k=3163, beta=0.5))
+    cfg = kls.KrylovSchurConfig(max_basis=60, tol=1e-7, scheme="dcgs2", max_restarts=restarts)
+    fn = lambda: kls.krylov_schur_run(op, cfg, seed=1729)  # noqa: E731
+    sec, res = _events_time(fn)
+    iters = 60 + 30 * (res.restarts - 1)  # the first expansion, then 30 steps per restart
+    out = {"workload": f"config 4: Krylov-Schur (max_basis 60, keep 30, tol 1e-7, DCGS2) on "
+                       f"ManteuffelSpec(k=3163, beta=0.5), m={op.n}; first {restarts} restarts",
+           "value": res.restarts / sec, "unit": "restarts/s", "arnoldi_iters_per_s": iters / sec,
+           "seconds": sec, "lock_history_tail": [int(x) for x in res.lock_history[-3:]]}
+    cfg1 = kls.KrylovSchurConfig(max_basis=60, tol=1e-7, scheme="dcgs2", max_restarts=3)
+    out["roofline"] = _roofline(_traced(lambda: kls.krylov_schur_run(op, cfg1, seed=1729)),
+                                peak, peak_src)
+    R, kind = _ref_module()
+    ks = 1000  # a 1/10-row sample of the same family, 2 restarts, scaled by rows
+    if kind == "reference":
+        rop = R.CsrOperator(R.manteuffel_build(R.ManteuffelSpec(k=ks, beta=0.5)))
+        ct = _cpu_time(lambda: R.krylov_schur_run(
+            rop, R.KrylovSchurConfig(max_basis=60, tol=1e-7, scheme="dcgs2", max_restarts=2),
+            seed=1729))
+        what = "reference krylov_schur_run, 2 restarts"
+    else:
+        import oracle
+
+        ptr, idx, dat = oracle.manteuffel_csr(ks, 0.5)
+        st = np.random.Generator(np.random.PCG64(1729)).standard_normal(ks * ks)
+        ct = _cpu_time(lambda: oracle.dcgs2_arnoldi(lambda x: oracle.csr_matvec(ptr, idx, dat, x),
+                                                    st, 90))
+        what = "oracle port: the 90 Arnoldi steps of 2 restarts (no Schur work)"
+    out["cpu_baseline"] = {"value": 2 / (ct * op.n / (ks * ks)), "unit": "restarts/s",
+                           "cores": os.cpu_count(), "kind": kind,
+                           "sample": f"{what} on ManteuffelSpec(k={ks}) (m={ks * ks}), "
+                                     f"{ct:.1f} s, scaled by rows to m={op.n}"}
+    return out
+
+
+def config5(kls, peak, peak_src, m=25_000_000, ns=(25, 50, 100, 200)):
+    """DCGS2 QR of a random-sparse tall-skinny block, m = 2.5e7 per GPU."""
+    import numpy as np
+    import torch
+
+    out = {"workload": "config 5: DCGS2 QR of a random-sparse tall-skinny matrix (density 1e-3, "
+                       "N(0,1) values, generated on the device), m=2.5e7 per GPU, n=25..200",
+           "unit": "columns/s"}
+    for n in ns:
+        g = torch.Generator(device="cuda")
+        g.manual_seed(1729)
+        A = torch.randn((n, m), generator=g, dtype=torch.float64, device="cuda")
+        A *= torch.rand((n, m), generator=g, device="cuda") < 1e-3
+
+        def qr():
+            st = kls.make_state("dcgs2", m, n)
+            for c in range(n):
+                st.push(A[c])
+            return st.finalize()
+
+        qr()
+        sec, _ = _events_time(qr)
+        nbytes = sum(8 * m * (2 * j + 6) for j in range(n))
+        e = {"value": n / sec, "seconds": sec, "hbm_gbs_algorithmic": nbytes / sec / 1e9}
+        if n == 100:
+            e["roofline"] = _roofline(_traced(qr), peak, peak_src)
+        out[f"n{n}"] = e
+        del A
+        torch.cuda.empty_cache()
+    R, kind = _ref_module()
+    ms, ns_ = 250_000, 100
+    rng = np.random.Generator(np.random.PCG64(2525))
+    A = np.zeros((ms, ns_))
+    for c in range(ns_):
+        rows = rng.choice(ms, size=int(round(1e-3 * ms)), replace=False)
+        A[rows, c] = rng.standard_normal(rows.size)
+    if kind == "reference":
+        ct = _cpu_time(lambda: R.qr_factorize(A, "dcgs2"))
+    else:
+        import oracle
+
+        ct = _cpu_time(lambda: oracle.dcgs2_qr(A))
+    out["n100"]["cpu_baseline"] = {"value": ns_ / (ct * m / ms), "unit": "columns/s",
+                                   "cores": os.cpu_count(), "kind": kind,
+                                   "sample": f"qr_factorize(dcgs2) of a {ms} x {ns_} matrix of the "
+                                             f"same family ({ct:.1f} s), scaled by rows to m={m}"}
+    return out
+
+
 def run_ours(args):
     import numpy as np
     import torch
-    import torch.distributed as dist
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2104_01253_b200 import runtime
+
+    comm = runtime.init_distributed()
+    world, rank = comm.world, comm.rank
+    local = torch.cuda.current_device()
 
     import paper_2104_01253_b200 as kls
-    from paper_2104_01253_b200 import _lib, runtime, trace
+    from paper_2104_01253_b200 import _lib
 
     dims = dims_of(args.dims)
     m = dims[0] * dims[1] * dims[2]
@@ -254,22 +545,16 @@ def run_ours(args):
     start_dev = start_host[lo:hi].to(torch.device("cuda", local))
     torch.cuda.synchronize()
 
-    def barrier():
-        if world > 1:
-            dist.barrier()
-
-    def max_over_ranks(x):
+    def host_reduce(x, op_name):
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        import torch.distributed as dist
 
-    def sum_over_ranks(x):
-        if world == 1:
-            return x
-        t = torch.tensor([float(x)], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t)
+        t = torch.tensor([float(x)], dtype=torch.float64)
+        if comm.backend() != "gloo":
+            t = t.cuda()
+        dist.all_reduce(t, op=dist.ReduceOp.MAX if op_name == "max" else dist.ReduceOp.SUM,
+                        group=comm.group)
         return float(t.item())
 
     def expansion(start):
@@ -279,31 +564,25 @@ def run_ours(args):
     for _ in range(args.warmup):
         expansion(start_dev)
     torch.cuda.synchronize()
-    barrier()
+    comm.barrier()
 
-    # ---- value: start resident in HBM -------------------------------------
-    rec = trace.start(events=True)
+    # ---- value: start resident in HBM, the path users get (no tracer) -------
     launches0 = _lib.launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
-        barrier()
+        comm.barrier()
         torch.cuda.synchronize()
         ev0.record()
         for _ in range(args.steps):
             H = expansion(start_dev)
         ev1.record()
         torch.cuda.synchronize()
-        barrier()
-    trace.stop()
+        comm.barrier()
     launches = _lib.launch_count() - launches0
-    sec = max_over_ranks(ev0.elapsed_time(ev1) * 1e-3)
+    sec = host_reduce(ev0.elapsed_time(ev1) * 1e-3, "max")
     iters = args.steps * args.n
     value = iters / sec
-    # per-kernel device time is read from the recorder spans below
-    ar_s, halo_s = rec.seconds("allreduce"), rec.seconds("halo")
-    local_bytes = rec.total_bytes()
-    total_bytes = sum_over_ranks(local_bytes)
-    total_launches = int(sum_over_ranks(launches))
+    total_launches = int(host_reduce(launches, "sum"))
 
     # ---- e2e: pinned host start, H2D inside the timed region ----------------
     e2e = None
@@ -311,7 +590,7 @@ def run_ours(args):
         expansion(start_host)  # warm the host path once
         torch.cuda.synchronize()
         x0 = dict(runtime.XFER)
-        barrier()
+        comm.barrier()
         t0 = time.perf_counter()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
@@ -319,62 +598,67 @@ def run_ours(args):
             H = expansion(start_host)
         e1.record()
         torch.cuda.synchronize()
-        barrier()
+        comm.barrier()
         wall = time.perf_counter() - t0
-        esec = max_over_ranks(max(e0.elapsed_time(e1) * 1e-3, wall))
+        esec = host_reduce(max(e0.elapsed_time(e1) * 1e-3, wall), "max")
         h2d = (runtime.XFER["h2d"] - x0["h2d"]) / args.steps
         d2h = (runtime.XFER["d2h"] - x0["d2h"]) / args.steps
         e2e = {"value": iters / esec, "unit": UNIT,
-               "h2d_bytes_per_step": int(sum_over_ranks(h2d)),
-               "d2h_bytes_per_step": int(sum_over_ranks(d2h)),
-               "path": "kls.arnoldi_expand(op, pinned host start) -> (V on device, H on host)"}
+               "h2d_bytes_per_step": int(host_reduce(h2d, "sum")),
+               "d2h_bytes_per_step": int(host_reduce(d2h, "sum")),
+               "path": "kls.arnoldi_expand(op, pinned host start) -> (V on device, H on host); "
+                       "d2h counts every step's 2j+3 scalars read from mapped pinned memory"}
 
-    # ---- collective latency (2j+3 = 203 doubles, back to back) ----------------
+    # ---- traced pass: per-kernel device time -> phase split and roofline ----
+    comm.barrier()
+    spans = _traced(lambda: [expansion(start_dev) for _ in range(max(args.traced, 1))])
+    t_iters = max(args.traced, 1) * args.n
+    traced_sec = sum(v[0] for k, v in spans.items() if not k.startswith("_"))
+    local_bytes = sum(v[1] for k, v in spans.items() if not k.startswith("_"))
+    total_bytes_per_iter = host_reduce(local_bytes, "sum") / t_iters
+    peak, peak_src = measured_peak()
+    roofline = _roofline(spans, peak, peak_src)
+    traffic = ncu_traffic(roofline["kernel"])
+    roofline["traffic"] = traffic.get("dram_bytes") if traffic else None
+    roofline["traffic_detail"] = traffic
+    roofline["share_of_step"] = (spans[roofline["kernel"]][0] / traced_sec) if traced_sec else None
+    roofline["timing"] = (f"CUDA events around every launch of a separate traced pass of "
+                          f"{max(args.traced, 1)} expansion(s) after the timed region (the tracer "
+                          f"bypasses the one-call native step loop, so it is kept out of `value`)")
+
+    # ---- collective latency (one step's 2j+3 = 203 doubles, back to back) ---
     coll = None
     if world > 1:
+        import torch.distributed as dist
+
         coll = {}
         n_ar, reps = 2 * args.n + 3, 200
-        src = torch.zeros(n_ar, dtype=torch.float64, device="cuda")
+        src = torch.zeros(runtime.SEG_MAX_EXPORT * n_ar, dtype=torch.float64, device="cuda")
         out = torch.zeros(n_ar, dtype=torch.float64, device="cuda")
         link = runtime.peer_link(op.comm)
         st = runtime.stream_handle()
         for name in ("peer", "nccl"):
             if name == "peer" and link is None:
                 continue
+            if name == "nccl" and comm.backend() != "nccl":
+                continue
             for rep in range(2):  # warm-up pass, timed pass
-                barrier()
+                comm.barrier()
                 torch.cuda.synchronize()
                 a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a0.record()
                 for _ in range(reps):
                     if name == "peer":
-                        link.allreduce(src.data_ptr(), n_ar, out.data_ptr(), st)
+                        link.seg_combine(src.data_ptr(), n_ar, out.data_ptr(), st)
                     else:
-                        dist.all_reduce(src)
+                        dist.all_reduce(out)
                 a1.record()
                 torch.cuda.synchronize()
-            coll[f"{name}_allreduce_us"] = max_over_ranks(a0.elapsed_time(a1) * 1e3 / reps)
+            key = "peer_seg_combine_us" if name == "peer" else "nccl_allreduce_us"
+            coll[key] = host_reduce(a0.elapsed_time(a1) * 1e3 / reps, "max")
         coll["doubles"] = n_ar
-        coll["note"] = ("the step's reduction runs fused into K1 (kls_gram_dcgs2_peer); these are "
-                        "standalone back-to-back latencies of the same payload")
-
-    # ---- roofline of the dominant kernel -------------------------------------
-    peak, peak_src = measured_peak()
-    spans = {name: rec.seconds(name) for name in ("gram", "update", "project", "project_gram", "mtm", "apply")}
-    kern = max(spans, key=spans.get)
-    k_s = spans[kern]
-    k_bytes = rec.bytes[kern]
-    k_calls = rec.calls[kern]
-    achieved = k_bytes / k_s / 1e9
-    traffic = ncu_traffic(kern)
-    roofline = {"bound": "hbm", "kernel": kern, "achieved": achieved, "peak": peak,
-                "unit": "GB/s", "frac": achieved / peak, "peak_source": peak_src,
-                "frac_of_8TBs": achieved / NOMINAL_HBM_GBS,
-                "bytes_per_launch_avg": k_bytes / max(k_calls, 1),
-                "launch_ms_avg": 1e3 * k_s / max(k_calls, 1),
-                "share_of_step": k_s / (sec * 1.0) if world == 1 else None,
-                "traffic": traffic.get("dram_bytes") if traffic else None,
-                "traffic_detail": traffic}
+        coll["note"] = ("the step's reduction runs fused into K1 (kls_gram_dcgs2_peer_step); "
+                        "these are standalone back-to-back latencies of the same payload")
 
     line = {
         "metric": METRIC,
@@ -393,15 +677,19 @@ def run_ours(args):
                    "scheme": args.scheme,
                    "operator": ("laplace3d 7-point, matrix-free" if args.operator == "stencil"
                                 else "laplace3d 7-point as device-assembled CSR (int32 cols)"),
-                   "parallelism": f"row-shard over {world} GPU(s), 1 allreduce/iteration",
+                   "parallelism": f"row-shard over {world} rank(s), 1 reduction/iteration, "
+                                  f"rank-count-independent segment tree"
+                                  + (", ranks share GPUs (CUDA-IPC peers)" if comm.shares_devices()
+                                     else ""),
                    "l2": "inputs larger than L2 (Q = %.1f GB)" % (8 * m * (args.n + 1) / 1e9)},
-        "hbm_gbs": total_bytes / sec / 1e9 / world,
-        "hbm_gbs_total": total_bytes / sec / 1e9,
-        "hbm_frac_of_8TBs": total_bytes / sec / 1e9 / world / NOMINAL_HBM_GBS,
-        "phase_ms_per_iter": {k: 1e3 * v / iters for k, v in spans.items() if v > 0},
-        "allreduce_us_per_iter": 1e6 * ar_s / iters if world > 1 else 0.0,
+        "hbm_gbs": total_bytes_per_iter * iters / sec / 1e9 / world,
+        "hbm_gbs_total": total_bytes_per_iter * iters / sec / 1e9,
+        "hbm_frac_of_8TBs": total_bytes_per_iter * iters / sec / 1e9 / world / NOMINAL_HBM_GBS,
+        "phase_ms_per_iter": {k: 1e3 * v[0] / t_iters for k, v in spans.items()
+                              if not k.startswith("_") and v[0] > 0},
+        "allreduce_us_per_iter": 1e6 * spans["_allreduce"][0] / t_iters if world > 1 else 0.0,
+        "halo_us_per_iter": 1e6 * spans["_halo"][0] / t_iters if world > 1 else 0.0,
         "collective_latency": coll,
-        "halo_us_per_iter": 1e6 * halo_s / iters if world > 1 else 0.0,
         "roofline": roofline,
         "e2e": e2e,
         "gpu_launches": total_launches,
@@ -409,19 +697,34 @@ def run_ours(args):
         "clocks": clk.summary(),
         "reductions_per_iter": 1 if args.scheme == "dcgs2" else 3,
     }
+    if world == 1 and not args.no_configs:
+        configs = {}
+        for name, fn in (("1", config1), ("2", config2), ("4", config4), ("5", config5)):
+            try:
+                configs[name] = fn(kls, peak, peak_src)
+            except Exception as exc:  # report, keep the headline line
+                configs[name] = {"error": f"{type(exc).__name__}: {exc}"}
+            torch.cuda.empty_cache()
+        line["configs"] = configs
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         sdims = dims_of(args.sample_dims)
         ms = sdims[0] * sdims[1] * sdims[2]
         rate, kind, times = cpu_reference_rate(sdims, args.n, args.scheme)
+        r1dims = dims_of(args.ref_sample_dims)
+        m1 = r1dims[0] * r1dims[1] * r1dims[2]
+        rate1, _, times1 = cpu_reference_rate(r1dims, args.n, args.scheme, threads=1)
         line["cpu_baseline"] = {
             "value": rate * ms / m, "unit": UNIT, "cores": os.cpu_count(), "kind": kind,
             "sample": f"{args.scheme} arnoldi_expand n={args.n} on laplace3d{sdims} ({ms} rows, "
-                      f"{times[0]:.1f} s), scaled by rows to m={m}; OpenBLAS default threads"}
+                      f"1/{m // ms} of m, {times[0]:.1f} s), scaled by rows to m={m}; OpenBLAS "
+                      f"default threads",
+            "value_1thread": rate1 * m1 / m,
+            "sample_1thread": f"the same on laplace3d{r1dims} ({m1} rows, {times1[0]:.1f} s) with "
+                              f"OPENBLAS threads = 1 (threadpoolctl)",
+            "host": host_info()}
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.barrier()
-        dist.destroy_process_group()
+    runtime.shutdown_distributed()
     return 0
 
 

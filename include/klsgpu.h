@@ -106,15 +106,18 @@ int kls_gram_dcgs2(const double* Q, int64_t ldq, int64_t m, int32_t j, const dou
  * (arnoldi.py:389-391 and 415-420; QR form ortho.py:371-375, 396-398):
  *   u = w - Q(:,0:j) c;  Q(:, j) = u / alpha;
  *   w = (divide ? aw / alpha : aw) - (Q(:,0:j) t(0:j) + Q(:,j) t_j)
- * coef (device) = [c(0:j), t(0:j+1)], 2j+1 doubles.  One pass over Q. */
+ * coef (device) = [c(0:j), t(0:j+1)], 2j+1 doubles.  One pass over Q.
+ * segs: the rows' layout (NULL: one rank) -- only its global row count is
+ * used, to pick the same kernel (the same per-row arithmetic) on every rank. */
 int kls_dcgs2_update(double* Q, int64_t ldq, int64_t m, int32_t j, double* w, const double* aw,
-                     const double* coef, double alpha, int32_t divide, void* stream);
+                     const double* coef, double alpha, int32_t divide, const KlsSegs* segs,
+                     void* stream);
 
 /* kls_dcgs2_update with the 2j+1 coefficients in HOST memory: they are
  * carried in the kernel launch (2j+1 <= 2048), so a step needs no H2D copy. */
 int kls_dcgs2_update_host(double* Q, int64_t ldq, int64_t m, int32_t j, double* w,
                           const double* aw, const double* coef_host, double alpha, int32_t divide,
-                          void* stream);
+                          const KlsSegs* segs, void* stream);
 
 /* Device-side scalar step (arnoldi.py:379-400): from g = [c, beta, s, s_piv,
  * aw.aw] (device) write coef = [c, s/alpha, t_piv, alpha] (device, 2j+2;
@@ -127,7 +130,7 @@ int kls_dcgs2_scalars(const double* g, int32_t j, int32_t qr, double* coef, doub
  * speculative step can be discarded). */
 int kls_dcgs2_update_dev(double* Q, int64_t ldq, int64_t m, int32_t j, const double* w,
                          double* w_out, const double* aw, const double* coef_alpha,
-                         int32_t divide, void* stream);
+                         int32_t divide, const KlsSegs* segs, void* stream);
 
 /* Y(:,0:l) <- scale*Y + sign*B(:,0:k) S — kernels.mv_times_mat_add_mv
  * (kernels.py:63-84) for l = 1 or 2; S is k x l column-major on the device.
@@ -221,6 +224,15 @@ int64_t kls_mant5_nnz(int64_t k, int64_t row_lo, int64_t row_hi);
 /* manteuffel_build (problems.py:208-245); diff = 1/h^2, conv = beta/(2h). */
 int kls_build_mant5_csr(int64_t k, int64_t row_lo, int64_t nrows, int64_t col_base, double diff,
                         double conv, int64_t* rowptr, int32_t* col, double* val, void* stream);
+/* Banded random operator of order m (config 5's Arnoldi variant, SURVEY.md
+ * §8d "random banded operator, bandwidth <= 1e3 so halos stay local"): row i
+ * holds d entries, one per equal slice of [max(0, i-band), min(m, i+band+1)),
+ * hashed column and value in [-1, 1) from (seed, i, slice) -- the host
+ * restatement oracle.band_random_coo + kls.CsrMatrix.from_coo
+ * (problems.py:99-117) gives the same CSR bit for bit.  d <= 2 band + 1. */
+int kls_build_band_csr(int64_t m, int64_t band, int32_t d, uint64_t seed, int64_t row_lo,
+                       int64_t nrows, int64_t col_base, int64_t* rowptr, int32_t* col,
+                       double* val, void* stream);
 
 /* ---- one-GPU step plan ------------------------------------------------------
  * The DCGS2 lookahead's per-step launches in one host call

@@ -129,6 +129,43 @@ def laplace3d_csr(nx, ny, nz):
     return _coo_to_csr(n, np.concatenate(rows), np.concatenate(cols), np.concatenate(vals))
 
 
+def band_random_coo(m, band, d, seed):
+    """Config 5's banded random operator (no reference counterpart: the
+    generator is this repo's): row i holds d entries, one per
+    equal slice of its window [max(0, i-band), min(m, i+band+1)), at column
+    slice_lo + (h >> 32) % slice_len with h = mix64(seed * G + i * H + k), value
+    (mix64(h ^ C) >> 11) * 2^-53 * 2 - 1.  uint64 arithmetic mod 2^64 -- the
+    restatement of csrc/build_ops.cu band_csr_kernel; the reference's
+    CsrMatrix.from_coo turns it into the golden CSR."""
+    M64 = np.uint64(0xFFFFFFFFFFFFFFFF)
+
+    def mix(x):
+        x = (x ^ (x >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        x = (x ^ (x >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        return x ^ (x >> np.uint64(31))
+
+    i = np.arange(m, dtype=np.int64)
+    lo = np.maximum(i - band, 0)
+    hi = np.minimum(i + band + 1, m)
+    w = hi - lo
+    rows, cols, vals = [], [], []
+    with np.errstate(over="ignore"):
+        for k in range(d):
+            a = lo + w * k // d
+            b = lo + w * (k + 1) // d
+            h = mix(np.uint64(seed) * np.uint64(0x9E3779B97F4A7C15)
+                    + i.astype(np.uint64) * np.uint64(0xD1B54A32D192ED03) + np.uint64(k)) & M64
+            c = a + ((h >> np.uint64(32)) % (b - a).astype(np.uint64)).astype(np.int64)
+            h2 = mix(h ^ np.uint64(0x5DEECE66D))
+            v = (h2 >> np.uint64(11)).astype(np.float64) * 2.0 ** -53 * 2.0 - 1.0
+            rows.append(i)
+            cols.append(c)
+            vals.append(v)
+    # row-major: row i's d entries, ascending columns
+    return (np.stack(rows, axis=1).ravel(), np.stack(cols, axis=1).ravel(),
+            np.stack(vals, axis=1).ravel())
+
+
 # ---------------------------------------------------------------------------
 # kernels (kernels.py:28-84)
 

@@ -236,7 +236,7 @@ class Engine:
             rec.note("update", 8 * self.ml * (j + 4))
         args = ("kls_dcgs2_update_dev", self.qptr, self.ld, self.ml, j, w.data_ptr(),
                 w_out.data_ptr(), aw.data_ptr(), self.cdev.data_ptr(), 1 if divide else 0,
-                self.st)
+                self.segp, self.st)
         if rec is not None and rec.events:
             with rec.span("update"):
                 _lib.call(*args)
@@ -273,11 +273,13 @@ class Engine:
         if coef.size <= _PACK:
             runtime.XFER["h2d"] += 8 * coef.size
             args = ("kls_dcgs2_update_host", self.qptr, self.ld, self.ml, j, w.data_ptr(),
-                    aw.data_ptr(), coef.ctypes.data, float(alpha), 1 if divide else 0, self.st)
+                    aw.data_ptr(), coef.ctypes.data, float(alpha), 1 if divide else 0, self.segp,
+                    self.st)
         else:
             dev = self.stage.push(coef)
             args = ("kls_dcgs2_update", self.qptr, self.ld, self.ml, j, w.data_ptr(),
-                    aw.data_ptr(), dev.data_ptr(), float(alpha), 1 if divide else 0, self.st)
+                    aw.data_ptr(), dev.data_ptr(), float(alpha), 1 if divide else 0, self.segp,
+                    self.st)
         if rec is not None and rec.events:
             with rec.span("update"):
                 _lib.call(*args)

@@ -58,11 +58,11 @@ SIGNATURES = {
     "kls_schur_move_front": (i64, [c_dp, c_dp, i64, c_dp, i64, c_dp]),
     "kls_schur_eigenvectors": (ctypes.c_int, [c_dp, c_dp, i64, i64, c_dp, i64, c_dp, c_dp, c_dp]),
     "kls_gram_dcgs2": (ctypes.c_int, [c_dp, i64, i64, i32, c_dp, c_dp, c_dp, c_dp, c_dp, sz, c_dp]),
-    "kls_dcgs2_update": (ctypes.c_int, [c_dp, i64, i64, i32, c_dp, c_dp, c_dp, f64, i32, c_dp]),
+    "kls_dcgs2_update": (ctypes.c_int, [c_dp, i64, i64, i32, c_dp, c_dp, c_dp, f64, i32, c_dp, c_dp]),
     "kls_dcgs2_scalars": (ctypes.c_int, [c_dp, i32, i32, c_dp, c_dp, c_dp]),
     "kls_dcgs2_update_dev": (ctypes.c_int, [c_dp, i64, i64, i32, c_dp, c_dp, c_dp, c_dp, i32,
-                                            c_dp]),
-    "kls_dcgs2_update_host": (ctypes.c_int, [c_dp, i64, i64, i32, c_dp, c_dp, c_dp, f64, i32, c_dp]),
+                                            c_dp, c_dp]),
+    "kls_dcgs2_update_host": (ctypes.c_int, [c_dp, i64, i64, i32, c_dp, c_dp, c_dp, f64, i32, c_dp, c_dp]),
     "kls_mv_times_mat_add_mv": (
         ctypes.c_int,
         [c_dp, i64, i64, i32, c_dp, i64, i32, c_dp, f64, f64, c_dp, c_dp, c_dp, sz, c_dp],
@@ -86,6 +86,8 @@ SIGNATURES = {
     "kls_build_lap7_csr": (ctypes.c_int, [i64, i64, i64, i64, i64, i64, c_dp, c_dp, c_dp, c_dp]),
     "kls_mant5_nnz": (i64, [i64, i64, i64]),
     "kls_build_mant5_csr": (ctypes.c_int, [i64, i64, i64, i64, f64, f64, c_dp, c_dp, c_dp, c_dp]),
+    "kls_build_band_csr": (ctypes.c_int, [i64, i64, i32, ctypes.c_uint64, i64, i64, i64, c_dp,
+                                          c_dp, c_dp, c_dp]),
     "kls_peer_seg_combine": (ctypes.c_int, [c_dp, i32, c_dp, c_dp, i32, i32, i32, ctypes.c_uint64,
                                             c_dp, c_dp]),
     "kls_gram_dcgs2_peer": (ctypes.c_int, [c_dp, i64, i64, i32, c_dp, c_dp, c_dp, c_dp, c_dp, sz,

@@ -20,7 +20,7 @@ import os
 import numpy as np
 import torch
 
-from . import _lib
+from . import _lib, runtime
 from . import ledger as _ledger
 from ._engine import Engine
 from .errors import BreakdownError, DimensionError, UnknownSchemeError
@@ -469,6 +469,9 @@ class _DelayedArnoldi(_BaseArnoldi):
         done, status, jstop = int(io[2]), int(io[3]), int(io[4])
         queued = done + (1 if status else 0)
         _lib.count_launches(3 * queued)  # update, operator, Gram (+ scalar step)
+        # the host read each step's 2j+3 scalars from mapped pinned memory
+        jq = np.arange(j0, j0 + queued, dtype=np.int64)
+        runtime.XFER["d2h"] += int(8 * np.sum(2 * jq + 3))
         m = self.m
         led = self.ledger
         js = np.arange(j0, j0 + done, dtype=np.int64)

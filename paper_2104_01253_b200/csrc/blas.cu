@@ -217,17 +217,17 @@ KLS_API int kls_tsgemm_inplace_cols(double* V, int64_t ldv, int64_t m, int32_t k
 
 KLS_API int kls_scale(const double* x, double* y, int64_t n, double alpha, int32_t mode,
                       void* stream) {
-  if (x == nullptr || y == nullptr || n < 0) return fail(KLS_EINVAL, "scale: bad arguments");
   if (n == 0) return KLS_OK;
+  if (x == nullptr || y == nullptr || n < 0) return fail(KLS_EINVAL, "scale: bad arguments");
   scale_kernel<<<grid_1d(n, 8), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(x, y, n, alpha,
                                                                                 mode);
   return check_launch("scale_kernel");
 }
 
 KLS_API int kls_sub(const double* a, const double* b, double* out, int64_t n, void* stream) {
+  if (n == 0) return KLS_OK;
   if (a == nullptr || b == nullptr || out == nullptr || n < 0)
     return fail(KLS_EINVAL, "sub: bad arguments");
-  if (n == 0) return KLS_OK;
   sub_kernel<<<grid_1d(n, 8), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(a, b, out, n);
   return check_launch("sub_kernel");
 }
@@ -235,7 +235,8 @@ KLS_API int kls_sub(const double* a, const double* b, double* out, int64_t n, vo
 KLS_API int kls_resid_norms(const double* b, const double* ax, const double* x, int64_t n,
                             double* out, const KlsSegs* segs, void* ws, size_t ws_bytes,
                             void* stream) {
-  if (b == nullptr || ax == nullptr || x == nullptr || out == nullptr || ws == nullptr || n < 0)
+  if ((n > 0 && (b == nullptr || ax == nullptr || x == nullptr)) || out == nullptr ||
+      ws == nullptr || n < 0)
     return fail(KLS_EINVAL, "resid_norms: bad arguments");
   seg::SimpleArgs a;
   int rc = seg::make_plan_simple(segs, n, kThreads, a, ws, ws_bytes, 3, out);

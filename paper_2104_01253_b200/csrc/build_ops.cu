@@ -99,6 +99,44 @@ __global__ void mant5_csr_kernel(int64_t row_lo, int64_t nrows, int64_t k, int64
   }
 }
 
+// Banded random operator (config 5's Arnoldi variant): row
+// i has exactly d entries, one in each of d equal slices of its window
+// [max(0, i - b), min(m, i + b + 1)) -- distinct and already ascending --
+// at a hashed column of the slice, with a hashed value in [-1, 1).  All
+// integer arithmetic is mod 2^64 and the value is (h >> 11) * 2^-53 * 2 - 1
+// (exact), so the host restatement (oracle.band_random_coo) produces the
+// same entries bit for bit.
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+__global__ void band_csr_kernel(int64_t m, int64_t band, int32_t d, uint64_t seed,
+                                int64_t row_lo, int64_t nrows, int64_t col_base,
+                                int64_t* __restrict__ rowptr, int32_t* __restrict__ col,
+                                double* __restrict__ val) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r <= nrows;
+       r += stride) {
+    rowptr[r] = r * d;
+    if (r == nrows) continue;
+    const int64_t i = row_lo + r;
+    const int64_t lo = i - band > 0 ? i - band : 0;
+    const int64_t hi = i + band + 1 < m ? i + band + 1 : m;
+    const int64_t w = hi - lo;
+    for (int k = 0; k < d; ++k) {
+      const int64_t a = lo + w * k / d, b = lo + w * (k + 1) / d;
+      const uint64_t h = mix64(seed * 0x9E3779B97F4A7C15ull + static_cast<uint64_t>(i) *
+                               0xD1B54A32D192ED03ull + static_cast<uint64_t>(k));
+      const int64_t c = a + static_cast<int64_t>((h >> 32) % static_cast<uint64_t>(b - a));
+      const uint64_t h2 = mix64(h ^ 0x5DEECE66Dull);
+      col[r * d + k] = static_cast<int32_t>(c - col_base);
+      val[r * d + k] = static_cast<double>(h2 >> 11) * 0x1.0p-53 * 2.0 - 1.0;
+    }
+  }
+}
+
 int grid_rows(int64_t n) {
   const int64_t b = ceil_div(n + 1, kThreads);
   return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(b, 16LL * sm_count())));
@@ -162,4 +200,18 @@ KLS_API int kls_build_mant5_csr(int64_t k, int64_t row_lo, int64_t nrows, int64_
   mant5_csr_kernel<<<grid_rows(nrows), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
       row_lo, nrows, k, col_base, diff, conv, rowptr, col, val);
   return check_launch("mant5_csr_kernel");
+}
+
+// CSR of rows [row_lo, row_lo + nrows) of the banded random operator of
+// order m (half bandwidth band >= d - 1, d entries per row, seed); columns
+// relative to the global row col_base; rowptr[r] = r * d.
+KLS_API int kls_build_band_csr(int64_t m, int64_t band, int32_t d, uint64_t seed, int64_t row_lo,
+                               int64_t nrows, int64_t col_base, int64_t* rowptr, int32_t* col,
+                               double* val, void* stream) {
+  if (m < 1 || d < 1 || band < 0 || 2 * band + 1 < d || (m < d) || row_lo < 0 || nrows < 0 ||
+      row_lo + nrows > m || rowptr == nullptr || (nrows > 0 && (col == nullptr || val == nullptr)))
+    return fail(KLS_EINVAL, "build_band_csr: bad arguments (need d <= min(m, 2 band + 1))");
+  band_csr_kernel<<<grid_rows(nrows), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+      m, band, d, seed, row_lo, nrows, col_base, rowptr, col, val);
+  return check_launch("band_csr_kernel");
 }

@@ -424,7 +424,8 @@ int launch_pg_reg_cols(PgArgs a, double* v, const double* s, bool host, size_t w
 KLS_API int kls_project_gram(const double* Q, int64_t ldq, int64_t m, int32_t k, double* v,
                              const double* s, int32_t s_on_host, int32_t xnorm, double* out,
                              const KlsSegs* segs, void* ws, size_t ws_bytes, void* stream) {
-  if (Q == nullptr || v == nullptr || s == nullptr || out == nullptr || ws == nullptr || m < 0 ||
+  if ((m > 0 && (Q == nullptr || v == nullptr)) || s == nullptr || out == nullptr ||
+      ws == nullptr || m < 0 ||
       k < 1 || k > 2048 || ldq < m || (ldq & 1) ||
       ((reinterpret_cast<uintptr_t>(Q) | reinterpret_cast<uintptr_t>(v)) & 15))
     return fail(KLS_EINVAL, "project_gram: bad arguments (k=%d, 1 <= k <= 2048)", k);

@@ -173,8 +173,11 @@ static int mv_trans_mv_impl(const double* Q, int64_t ldq, int64_t m, int32_t k,
                             size_t ws_bytes, void* stream, const peer::Peers* peers,
                             uint64_t epoch, int* err, double* coef = nullptr,
                             double* gout = nullptr, int32_t qr = 0) {
-  if (m < 0 || k < 0 || (k > 0 && (Q == nullptr || ldq < m)) || x0 == nullptr || out == nullptr ||
-      ws == nullptr || (nx != 1 && nx != 2) || (nx == 2 && x1 == nullptr))
+  // a rank may hold no rows (m = 0: empty tensors, null pointers); it still
+  // takes part in the reduction tree and the exchange
+  if (m < 0 || k < 0 || (k > 0 && ((m > 0 && Q == nullptr) || ldq < m)) ||
+      (m > 0 && x0 == nullptr) || out == nullptr || ws == nullptr || (nx != 1 && nx != 2) ||
+      (nx == 2 && m > 0 && x1 == nullptr))
     return fail(KLS_EINVAL, "mv_trans_mv: bad arguments (m=%lld k=%d nx=%d)", (long long)m, k, nx);
   if ((reinterpret_cast<uintptr_t>(x0) | reinterpret_cast<uintptr_t>(x1) |
        reinterpret_cast<uintptr_t>(bext) | reinterpret_cast<uintptr_t>(Q)) & 15)

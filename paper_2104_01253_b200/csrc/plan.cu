@@ -56,7 +56,8 @@ KLS_API int kls_dcgs2_queue_step(const KlsStepPlan* p, int32_t j, const double* 
                                  const double* x_out, const double* aw, double* aw_out,
                                  int32_t slot, int32_t gram) {
   if (p == nullptr || slot < 0 || slot > 1) return fail(KLS_EINVAL, "queue_step: bad plan or slot");
-  int rc = kls_dcgs2_update_dev(p->Q, p->ldq, p->m, j, w, w_out, aw, p->cdev, p->divide, p->stream);
+  int rc = kls_dcgs2_update_dev(p->Q, p->ldq, p->m, j, w, w_out, aw, p->cdev, p->divide,
+                                &p->segs, p->stream);
   if (rc) return rc;
   rc = apply_op(&p->op, x_out, aw_out, p->stream);
   if (rc) return rc;

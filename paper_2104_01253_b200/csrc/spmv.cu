@@ -456,9 +456,9 @@ __global__ void __launch_bounds__(kThreads) dense_gemv_kernel(const double* __re
 // extended vector [lo halo | local | hi halo].
 KLS_API int kls_csr_spmv(const int64_t* rowptr, const int32_t* col, const double* val,
                          int64_t nrows, const double* x, double* y, void* stream) {
+  if (nrows == 0) return KLS_OK;  // a rank without rows
   if (nrows < 0 || rowptr == nullptr || x == nullptr || y == nullptr)
     return fail(KLS_EINVAL, "csr_spmv: bad arguments");
-  if (nrows == 0) return KLS_OK;
   const int64_t blocks = ceil_div(nrows, 32 * kWarps);
   const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(blocks, 8LL * sm_count())));
   csr_spmv_kernel<<<grid, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(rowptr, col, val, nrows,
@@ -471,10 +471,10 @@ KLS_API int kls_csr_spmv(const int64_t* rowptr, const int32_t* col, const double
 // physical (Dirichlet) boundary.
 KLS_API int kls_stencil7(const double* x, const double* x_lo, const double* x_hi, double* y,
                          int64_t nx, int64_t ny, int64_t nz, void* stream) {
+  if (nx * ny * nz == 0 && nx >= 0 && ny >= 0 && nz >= 0) return KLS_OK;
   if (x == nullptr || y == nullptr || nx < 0 || ny < 0 || nz < 0)
     return fail(KLS_EINVAL, "stencil7: bad arguments");
   const int64_t n = nx * ny * nz;
-  if (n == 0) return KLS_OK;
   if (ny > INT32_MAX || nz > INT32_MAX) return fail(KLS_EINVAL, "stencil7: ny, nz must fit int32");
   static int env_chunk = -1;
   if (env_chunk < 0) {
@@ -528,10 +528,10 @@ KLS_API int kls_csr_to_ell(const int64_t* rowptr, const int32_t* col, const doub
 KLS_API int kls_ell_spmv(const int32_t* ecol, const double* eval, const uint8_t* elen,
                          int32_t width, int64_t nrows, int64_t ld, const double* x, double* y,
                          void* stream) {
+  if (nrows == 0) return KLS_OK;
   if (ecol == nullptr || eval == nullptr || elen == nullptr || x == nullptr || y == nullptr ||
       nrows < 0 || ld < nrows || width < 1 || width > 8)
     return fail(KLS_EINVAL, "ell_spmv: bad arguments");
-  if (nrows == 0) return KLS_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   static const bool plain = [] {
     const char* e = getenv("KLS_ELL");
@@ -558,8 +558,9 @@ KLS_API int kls_ell_resid_norms(const int32_t* ecol, const double* eval, const u
                                 int32_t width, int64_t nrows, int64_t ld, const double* x,
                                 const double* b, double* out, const KlsSegs* segs, void* ws,
                                 size_t ws_bytes, void* stream) {
-  if (ecol == nullptr || eval == nullptr || elen == nullptr || x == nullptr || b == nullptr ||
-      out == nullptr || ws == nullptr || nrows < 1 || ld < nrows || width < 1 || width > 8)
+  if ((nrows > 0 && (ecol == nullptr || eval == nullptr || elen == nullptr || x == nullptr ||
+                     b == nullptr)) ||
+      out == nullptr || ws == nullptr || nrows < 0 || ld < nrows || width < 1 || width > 8)
     return fail(KLS_EINVAL, "ell_resid_norms: bad arguments");
   seg::SimpleArgs a;
   int rc = seg::make_plan_simple(segs, nrows, kThreads, a, ws, ws_bytes, 3, out);

@@ -48,6 +48,7 @@ struct UpdParams {
   int32_t divide;      // aw / alpha (Arnoldi) or aw as is (QR)
   const double* alpha_dev;  // when set, alpha is read from device memory
   double* w_out;            // where w' goes (== w for the in-place update)
+  int64_t m_global;         // variant choice (the same on every rank)
 };
 
 template <int RP, bool CHECK>
@@ -130,7 +131,7 @@ __global__ void __launch_bounds__(kThreads, kUpdBlocksPerSm)
   pdl_trigger();
 }
 
-// Small-m K2 (m_local <= kUpdSmallRows): one 64-row block per CTA, the 8
+// Small-m K2 (global m <= kUpdSmallRows): one 64-row block per CTA, the 8
 // warps splitting the basis columns (k = w, w+8, ...) so every warp has all
 // its loads in flight at once; the warps' partial Q c and Q t are combined in
 // fixed warp order through shared memory, then the row arithmetic of
@@ -518,7 +519,10 @@ template <int NC>
 int launch_update(const UpdParams& p, const double* host_coef, cudaStream_t st) {
   CoefPack<NC> pk;
   if (NC > 0) std::memcpy(pk.v, host_coef, sizeof(double) * (2 * p.j + 1));
-  if (p.m <= kUpdSmallRows && p.j > 0 && update_tma()) {
+  // the small kernel sums a row's terms in another order than the streaming
+  // kernels, so the choice follows the GLOBAL row count: every rank of a
+  // sharded run (and a one-rank run) uses the same per-row arithmetic
+  if (p.m_global <= kUpdSmallRows && p.j > 0 && update_tma()) {
     const size_t smem = sizeof(double2) * static_cast<size_t>((p.j + kCols - 1) / kCols * kCols + 1);
     int rc = set_smem(reinterpret_cast<const void*>(dcgs2_update_small_kernel<NC>), smem);
     if (rc) return rc;
@@ -546,17 +550,22 @@ int launch_update(const UpdParams& p, const double* host_coef, cudaStream_t st) 
 }
 
 int update_common(double* Q, int64_t ldq, int64_t m, int32_t j, double* w, const double* aw,
-                  const double* coef, double alpha, int32_t divide, bool host, void* stream,
-                  const double* alpha_dev = nullptr, double* w_out = nullptr) {
-  if (Q == nullptr || w == nullptr || aw == nullptr || coef == nullptr || m < 0 || j < 0 ||
+                  const double* coef, double alpha, int32_t divide, bool host,
+                  const KlsSegs* segs, void* stream, const double* alpha_dev = nullptr,
+                  double* w_out = nullptr) {
+  if ((m > 0 && (Q == nullptr || w == nullptr || aw == nullptr)) || coef == nullptr || m < 0 ||
+      j < 0 ||
       ldq < m || (ldq & 1))
     return fail(KLS_EINVAL, "dcgs2_update: bad arguments");
   if (misaligned(Q) || misaligned(w) || misaligned(aw))
     return fail(KLS_EINVAL, "dcgs2_update: operands must be 16-byte aligned");
   if (w_out != nullptr && misaligned(w_out))
     return fail(KLS_EINVAL, "dcgs2_update: w_out must be 16-byte aligned");
+  seg::Layout L;
+  const int rc = seg::make_layout(segs, m, L);
+  if (rc) return rc;
   UpdParams p{Q, ldq, m, j, w, aw, host ? nullptr : coef, alpha, divide, alpha_dev,
-              w_out != nullptr ? w_out : w};
+              w_out != nullptr ? w_out : w, segs != nullptr ? segs->m : m};
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int nc = 2 * j + 1;
   if (!host) return launch_update<0>(p, nullptr, st);
@@ -603,8 +612,9 @@ int mtm_dispatch(const MtmParams& p, const double* host_s, const seg::SimpleArgs
 int mtm_common(double* Y, int64_t ldy, int64_t m, int32_t l, const double* B, int64_t ldb,
                int32_t k, const double* S, double sign, double scale, double* nrm_out,
                const KlsSegs* segs, void* ws, size_t ws_bytes, bool host, void* stream) {
-  if (Y == nullptr || m < 0 || k < 0 || (l != 1 && l != 2) || (l == 2 && (ldy < m || (ldy & 1))) ||
-      (k > 0 && (B == nullptr || S == nullptr || ldb < m || (ldb & 1))))
+  if ((m > 0 && Y == nullptr) || m < 0 || k < 0 || (l != 1 && l != 2) ||
+      (l == 2 && (ldy < m || (ldy & 1))) ||
+      (k > 0 && ((m > 0 && B == nullptr) || S == nullptr || ldb < m || (ldb & 1))))
     return fail(KLS_EINVAL, "mv_times_mat_add_mv: bad arguments (m=%lld k=%d l=%d)",
                 (long long)m, k, l);
   if (misaligned(Y) || misaligned(B)) return fail(KLS_EINVAL, "mv_times_mat_add_mv: misaligned");
@@ -642,16 +652,16 @@ int mtm_common(double* Y, int64_t ldy, int64_t m, int32_t l, const double* B, in
 // w' = aw/alpha - ...; divide == 0 the QR form w' = a - ....
 KLS_API int kls_dcgs2_update(double* Q, int64_t ldq, int64_t m, int32_t j, double* w,
                              const double* aw, const double* coef, double alpha, int32_t divide,
-                             void* stream) {
-  return update_common(Q, ldq, m, j, w, aw, coef, alpha, divide, false, stream);
+                             const KlsSegs* segs, void* stream) {
+  return update_common(Q, ldq, m, j, w, aw, coef, alpha, divide, false, segs, stream);
 }
 
 // Same with the coefficients in HOST memory: they ride in the kernel launch
 // (2j+1 <= 2048), so the step needs no separate H2D copy.
 KLS_API int kls_dcgs2_update_host(double* Q, int64_t ldq, int64_t m, int32_t j, double* w,
                                   const double* aw, const double* coef_host, double alpha,
-                                  int32_t divide, void* stream) {
-  return update_common(Q, ldq, m, j, w, aw, coef_host, alpha, divide, true, stream);
+                                  int32_t divide, const KlsSegs* segs, void* stream) {
+  return update_common(Q, ldq, m, j, w, aw, coef_host, alpha, divide, true, segs, stream);
 }
 
 // Same with everything on the device: coef = [c(0:j), t(0:j+1), alpha]
@@ -660,11 +670,11 @@ KLS_API int kls_dcgs2_update_host(double* Q, int64_t ldq, int64_t m, int32_t j, 
 // (w is left intact, so a speculative step can be discarded).
 KLS_API int kls_dcgs2_update_dev(double* Q, int64_t ldq, int64_t m, int32_t j, const double* w,
                                  double* w_out, const double* aw, const double* coef_alpha,
-                                 int32_t divide, void* stream) {
+                                 int32_t divide, const KlsSegs* segs, void* stream) {
   if (coef_alpha == nullptr || w_out == nullptr)
     return fail(KLS_EINVAL, "dcgs2_update_dev: null coefficients or output");
   return update_common(Q, ldq, m, j, const_cast<double*>(w), aw, coef_alpha, 0.0, divide, false,
-                       stream, coef_alpha + 2 * j + 1, w_out);
+                       segs, stream, coef_alpha + 2 * j + 1, w_out);
 }
 
 // Y(:, 0:l) <- scale * Y + sign * B(:, 0:k) S  with S (k x l, column-major,

@@ -208,6 +208,30 @@ class LinearOperator:
         return self._fro
 
 
+def _scratch_copy(op, x, peer_ok):
+    """A halo-capable copy of a plain local vector for a sharded apply (CGS2
+    applies the operator to a basis column, GMRES to its iterate).  With a
+    peer link the copy goes into one of TWO peer vectors used alternately:
+    before a rank overwrites the buffer of apply k it has passed apply k+1's
+    wait on its neighbours' halo flags, which they raise only after their
+    apply k -- so no neighbour still reads it.  Otherwise an NCCL halo
+    vector."""
+    link = runtime.peer_link(op.comm)
+    if link is None or not peer_ok:
+        if op._scratch is None:
+            op._scratch = op._plain_vector()
+        op._scratch.local.copy_(x)
+        return op._scratch
+    pair = op.__dict__.get("_peer_scratch")
+    if pair is None:
+        pair = op._peer_scratch = [PeerVector(link, op.m_local), PeerVector(link, op.m_local)]
+        op._peer_scratch_next = 0
+    v = pair[op._peer_scratch_next]
+    op._peer_scratch_next ^= 1
+    v.local.copy_(x)
+    return v
+
+
 class PeerVector:
     """A vector in NVLink symmetric memory: peers read its rows directly."""
 
@@ -511,11 +535,7 @@ class CsrOperator(LinearOperator):
 
     def apply_into(self, x, y, st=None):
         if not isinstance(x, (HaloVector, PeerVector)) and self._needs_halo():
-            # scratch copies take the NCCL path (see StencilLaplace3D)
-            if self._scratch is None:
-                self._scratch = self._plain_vector()
-            self._scratch.local.copy_(x)
-            x = self._scratch
+            x = _scratch_copy(self, x, bool(self._peer))
         super().apply_into(x, y, st)
 
     def _halo_plan(self):
@@ -524,15 +544,13 @@ class CsrOperator(LinearOperator):
         vectors over NVLink (decided collectively: all ranks take one path)."""
         c = self.comm
         link = runtime.peer_link(c)
-        mine = torch.tensor([self.row_lo - self.halo_lo, self.row_lo, self.row_hi,
-                             self.row_hi + self.halo_hi,
-                             1 if (link is not None and self._ell is not None) else 0],
-                            dtype=torch.int64, device=runtime.device())
-        allw = [torch.empty_like(mine) for _ in range(c.world)]
+        mine = (self.row_lo - self.halo_lo, self.row_lo, self.row_hi, self.row_hi + self.halo_hi,
+                1 if (link is not None and self._ell is not None) else 0)
         import torch.distributed as dist
 
-        dist.all_gather(allw, mine, group=c.group)
-        wins = [tuple(int(v) for v in w.cpu().tolist()) for w in allw]
+        allw = [None] * c.world
+        dist.all_gather_object(allw, mine, group=c.group)
+        wins = [tuple(int(v) for v in w) for w in allw]
         ok = all(w[4] for w in wins)
         for r, (nlo, lo, hi, nhi, _) in enumerate(wins):
             if nlo < lo and (r == 0 or nlo < wins[r - 1][1]):
@@ -649,12 +667,8 @@ class CsrOperator(LinearOperator):
                     # sum over the ELL entry columns (zero-padded, row-major
                     # per column): each a rank-count-independent dot
                     _, evals, _, width, ld = self._ell
-                    if self.comm.world > 1:  # the same number of dots on every rank
-                        wt = torch.tensor([width], dtype=torch.int64, device=evals.device)
-                        import torch.distributed as dist
-
-                        dist.all_reduce(wt, op=dist.ReduceOp.MAX, group=self.comm.group)
-                        width = int(wt.item())
+                    # the same number of dots on every rank
+                    width = self.comm.allreduce_max_int(width)
                     acc = 0.0
                     zero = torch.zeros(max(self.m_local, 2), dtype=torch.float64, device=evals.device)
                     for k in range(width):
@@ -840,12 +854,7 @@ class StencilLaplace3D(LinearOperator):
 
     def apply_into(self, x, y, st=None):
         if not isinstance(x, (HaloVector, PeerVector)) and self._needs_halo():
-            # scratch copies take the NCCL path: back-to-back applies on one
-            # scratch buffer would race a peer still reading the last one
-            if self._scratch is None:
-                self._scratch = self._plain_vector()
-            self._scratch.local.copy_(x)
-            x = self._scratch
+            x = _scratch_copy(self, x, True)
         super().apply_into(x, y, st)
 
     def _exchange(self, x):
@@ -976,6 +985,26 @@ def manteuffel_operator(spec, comm=None):
         _lib.call("kls_build_mant5_csr", k, lo, nrows, base, diff, conv, rp, cp, vp, st)
 
     return CsrOperator._device_built(k * k, k, nnz, build, comm)
+
+
+def band_random_operator(m, band=1000, per_row=7, seed=2525, comm=None):
+    """Config 5's Arnoldi operator (SURVEY.md §8d's alternative: a random
+    banded operator whose halos stay with the adjacent ranks): order m,
+    per_row entries per row spread over the band |i - j| <= band, hashed
+    columns and values in [-1, 1), assembled on the device
+    (kls_build_band_csr; host restatement oracle.band_random_coo, bitwise
+    equal through kls.CsrMatrix.from_coo)."""
+    if per_row > min(m, 2 * band + 1):
+        raise ValueError("per_row must be <= min(m, 2 band + 1)")
+    st = runtime.stream_handle()
+
+    def nnz(lo, hi):
+        return (hi - lo) * per_row
+
+    def build(lo, nrows, base, rp, cp, vp):
+        _lib.call("kls_build_band_csr", m, band, per_row, seed, lo, nrows, base, rp, cp, vp, st)
+
+    return CsrOperator._device_built(m, band, nnz, build, comm)
 
 
 # ---------------------------------------------------------------------------

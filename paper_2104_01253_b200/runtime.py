@@ -73,6 +73,54 @@ class Comm:
             self.rank, self.world = 0, 1
         self.allreduce_calls = 0
 
+    def backend(self):
+        import torch.distributed as dist
+
+        return dist.get_backend(self.group) if self.world > 1 else "none"
+
+    def barrier(self):
+        import torch.distributed as dist
+
+        if self.world > 1:
+            dist.barrier(group=self.group)
+
+    def shares_devices(self):
+        """True when two ranks of this comm drive the same GPU."""
+        if self.world == 1:
+            return False
+        if getattr(self, "_shares", None) is None:
+            import socket
+
+            import torch.distributed as dist
+
+            me = (socket.gethostname(), torch.cuda.current_device())
+            got = [None] * self.world
+            dist.all_gather_object(got, me, group=self.group)
+            self._shares = len(set(got)) < self.world
+        return self._shares
+
+    def allreduce_max_int(self, v):
+        """Max of a host integer over the ranks."""
+        if self.world == 1:
+            return int(v)
+        import torch.distributed as dist
+
+        dev = "cpu" if self.backend() == "gloo" else device()
+        t = torch.tensor([int(v)], dtype=torch.int64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
+        return int(t.item())
+
+    def allreduce_max_float(self, v):
+        """Max of a host float over the ranks."""
+        if self.world == 1:
+            return float(v)
+        import torch.distributed as dist
+
+        dev = "cpu" if self.backend() == "gloo" else device()
+        t = torch.tensor([float(v)], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
+        return float(t.item())
+
     def segs(self, m, unit=64):
         """The reduction layout of an m-row object split over this comm."""
         return Segs(m, unit, self.world, self.rank)
@@ -84,10 +132,16 @@ class Comm:
         peer path and as one rank."""
         import torch.distributed as dist
 
-        g = torch.zeros((self.world, SEG_MAX_EXPORT * count), dtype=torch.float64,
-                        device=blocks.device)
         mine = blocks[: SEG_MAX_EXPORT * count].contiguous()
-        dist.all_gather_into_tensor(g, mine, group=self.group)
+        if self.backend() == "gloo":  # host all_gather, then back to the device
+            parts = [torch.empty(SEG_MAX_EXPORT * count, dtype=torch.float64)
+                     for _ in range(self.world)]
+            dist.all_gather(parts, mine.cpu(), group=self.group)
+            g = torch.stack(parts).to(blocks.device)
+        else:
+            g = torch.zeros((self.world, SEG_MAX_EXPORT * count), dtype=torch.float64,
+                            device=blocks.device)
+            dist.all_gather_into_tensor(g, mine, group=self.group)
         out = torch.empty(count, dtype=torch.float64, device=blocks.device)
         _lib.call("kls_seg_combine", g.data_ptr(), count, count, self.world, out.data_ptr(),
                   stream_handle())
@@ -99,7 +153,12 @@ class Comm:
         if self.world > 1:
             import torch.distributed as dist
 
-            dist.all_reduce(t, group=self.group)
+            if self.backend() == "gloo" and t.is_cuda:
+                h = t.cpu()
+                dist.all_reduce(h, group=self.group)
+                t.copy_(h)
+            else:
+                dist.all_reduce(t, group=self.group)
             self.allreduce_calls += 1
         return t
 
@@ -375,35 +434,94 @@ def as_device_vector(x, n_local, lo=0, name="vector"):
 # NVLink peer link (symmetric memory)
 
 
-class PeerLink:
-    """Symmetric buffers of one process group, mapped into every peer GPU.
+class _CudaView:
+    """__cuda_array_interface__ of raw device memory (torch.as_tensor wraps
+    it without a copy)."""
 
-    Carries the one-shot allreduce of the per-step Gram scalars and the halo
-    flags of peer-read stencils (csrc/comm.cu).  Allocation and rendezvous
-    are collective: every rank must create the link / vectors in the same
-    order (they do: the solvers are SPMD).
+    def __init__(self, ptr, nbytes):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1",
+                                         "data": (int(ptr), False), "version": 3}
+
+
+class _IpcBuffer:
+    """A peer buffer allocated through the C-ABI (kls_peer_buffer_alloc,
+    zeroed cudaMalloc) and mapped into every rank by CUDA IPC handles
+    exchanged over the process group: works when ranks share a GPU (where
+    symmetric memory refuses) and for any host without a collective
+    allocator.  Collective."""
+
+    def __init__(self, comm, nbytes):
+        import torch.distributed as dist
+
+        lib = _lib.load()
+        hbytes = int(lib.kls_ipc_handle_bytes())
+        own = ctypes.c_void_p()
+        handle = (ctypes.c_char * hbytes)()
+        _lib.call("kls_peer_buffer_alloc", nbytes, ctypes.byref(own), handle)
+        handles = [None] * comm.world
+        dist.all_gather_object(handles, bytes(handle), group=comm.group)
+        self.own = own.value
+        self.opened = []
+        ptrs = []
+        for r, h in enumerate(handles):
+            if r == comm.rank:
+                ptrs.append(self.own)
+                continue
+            p = ctypes.c_void_p()
+            hb = (ctypes.c_char * hbytes).from_buffer_copy(h)
+            _lib.call("kls_peer_buffer_open", hb, ctypes.byref(p))
+            self.opened.append(p.value)
+            ptrs.append(p.value)
+        self.ptrs = ptrs
+        self.tensor = torch.as_tensor(_CudaView(self.own, nbytes), device=device())
+
+    def __del__(self):
+        try:
+            for p in self.opened:
+                _lib.call("kls_peer_buffer_close", p)
+            _lib.call("kls_peer_buffer_free", self.own)
+        except Exception:  # interpreter shutdown
+            pass
+
+
+class PeerLink:
+    """Peer buffers of one process group, mapped into every peer GPU.
+
+    Carries the one-shot combine of every reduction (the per-step Gram
+    scalars among them) and the halo flags of peer-read operators
+    (csrc/comm.cu).  Two allocators: torch symmetric memory (one rank per
+    GPU), or CUDA-IPC buffers from the C-ABI (kls_peer_buffer_alloc / open;
+    used when ranks share a GPU, or with KLS_PEER=ipc).  Allocation and
+    rendezvous are collective: every rank must create the link / vectors in
+    the same order (they do: the solvers are SPMD).
     """
 
-    CAP = 8192  # doubles per allreduce slot (2j+3 <= CAP)
+    CAP = 8192  # doubles per exchange slot (8 exported nodes x count <= CAP)
 
-    def __init__(self, comm):
-        import ctypes
-
+    def __init__(self, comm, mode="symm"):
         import torch.distributed as dist
-        import torch.distributed._symmetric_memory as symm_mem
 
         self.comm = comm
+        self.mode = mode
         self.rank, self.world = comm.rank, comm.world
         if self.world > 8:
             raise RuntimeError("peer link supports up to 8 ranks (one NVLink domain)")
         group = comm.group if comm.group is not None else dist.group.WORLD
         self._group_name = group.group_name
         nbytes = int(_lib.load().kls_peer_buffer_bytes(self.CAP))
-        self.buf = symm_mem.empty(nbytes, dtype=torch.uint8, device=device())
-        self.buf.zero_()
-        self.hdl = symm_mem.rendezvous(self.buf, self._group_name)
-        self.ptrs = (ctypes.c_void_p * self.world)(*[int(p) for p in self.hdl.buffer_ptrs])
-        self.mybuf = int(self.hdl.buffer_ptrs[self.rank])
+        if mode == "ipc":
+            self._ipc = _IpcBuffer(comm, nbytes)
+            self.buf = self._ipc.tensor
+            ptrs = self._ipc.ptrs
+        else:
+            import torch.distributed._symmetric_memory as symm_mem
+
+            self.buf = symm_mem.empty(nbytes, dtype=torch.uint8, device=device())
+            self.buf.zero_()
+            self.hdl = symm_mem.rendezvous(self.buf, self._group_name)
+            ptrs = [int(p) for p in self.hdl.buffer_ptrs]
+        self.ptrs = (ctypes.c_void_p * self.world)(*ptrs)
+        self.mybuf = int(ptrs[self.rank])
         self.err_host = torch.zeros(1, dtype=torch.int32, pin_memory=True)
         from ._engine import _mapped
 
@@ -411,18 +529,19 @@ class PeerLink:
         self.ar_epoch = 0
         self.halo_epoch = 0
         torch.cuda.synchronize()
-        dist.barrier(group=group)
+        comm.barrier()
 
     def symmetric_vector(self, n):
-        """A zeroed device vector in symmetric memory plus every rank's
+        """A zeroed device vector mapped into every peer plus every rank's
         pointer to its copy.  Collective; ranks may ask for different
         lengths (uneven row blocks): every copy gets the largest."""
-        import torch.distributed as dist
+        nmax = self.comm.allreduce_max_int(max(n, 2))
+        if self.mode == "ipc":
+            b = _IpcBuffer(self.comm, 8 * nmax)
+            return b.tensor.view(torch.float64), list(b.ptrs), b
         import torch.distributed._symmetric_memory as symm_mem
 
-        nmax = torch.tensor([max(n, 2)], dtype=torch.int64, device=device())
-        dist.all_reduce(nmax, op=dist.ReduceOp.MAX, group=self.comm.group)
-        t = symm_mem.empty(int(nmax.item()), dtype=torch.float64, device=device())
+        t = symm_mem.empty(nmax, dtype=torch.float64, device=device())
         t.zero_()
         hdl = symm_mem.rendezvous(t, self._group_name)
         return t, [int(p) for p in hdl.buffer_ptrs], hdl
@@ -450,18 +569,55 @@ class PeerLink:
 
 def peer_link(comm):
     """The comm's PeerLink, or None (single rank, disabled by KLS_PEER=0, or
-    symmetric memory unavailable, in which case NCCL carries the traffic)."""
+    no peer mapping possible, in which case NCCL carries the traffic).
+    Ranks sharing a GPU (or KLS_PEER=ipc) use CUDA-IPC buffers."""
     import os
 
-    if comm.world == 1 or os.environ.get("KLS_PEER", "1") == "0":
+    env = os.environ.get("KLS_PEER", "1")
+    if comm.world == 1 or env == "0":
         return None
     if getattr(comm, "_peer", None) is None and not getattr(comm, "_peer_failed", False):
+        mode = "ipc" if (env == "ipc" or comm.shares_devices()) else "symm"
         try:
-            comm._peer = PeerLink(comm)
+            comm._peer = PeerLink(comm, mode)
         except Exception as exc:  # transport selection only; compute is unchanged
+            if comm.backend() != "nccl":
+                raise
             import warnings
 
             warnings.warn(f"NVLink peer link unavailable ({exc}); using NCCL collectives")
             comm._peer_failed = True
             comm._peer = None
     return getattr(comm, "_peer", None)
+
+
+def init_distributed():
+    """One process per rank from torchrun's environment (RANK, LOCAL_RANK,
+    WORLD_SIZE, MASTER_*): the GPU is LOCAL_RANK % device count; NCCL when
+    every rank has its own GPU, gloo (bootstrap and host values only -- the
+    data path goes over CUDA-IPC peer buffers) when ranks share one.
+    Returns the default Comm (world 1 without torchrun)."""
+    import os
+
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    ndev = max(torch.cuda.device_count(), 1)
+    torch.cuda.set_device(local % ndev)
+    if world > 1 and not dist.is_initialized():
+        local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
+        if local_world > ndev:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local % ndev))
+    return comm()
+
+
+def shutdown_distributed():
+    import torch.distributed as dist
+
+    if dist.is_available() and dist.is_initialized():
+        c = comm()
+        c.barrier()
+        dist.destroy_process_group()

@@ -24,7 +24,7 @@ for m in [int(float(v)) for v in os.environ.get("SIZES", "1e4,1e5,1e6,1e7").spli
             _lib.call("kls_gram_dcgs2_step", Q.data_ptr(), ld, m, j, w.data_ptr(), aw.data_ptr(),
                       g.data_ptr(), c.data_ptr(), None, 0, None, ws, wsb, st)
             _lib.call("kls_dcgs2_update_dev", Q.data_ptr(), ld, m, j, w.data_ptr(), w2.data_ptr(),
-                      aw.data_ptr(), c.data_ptr(), 1, st)
+                      aw.data_ptr(), c.data_ptr(), 1, None, st)
 
         for _ in range(5):
             pair()

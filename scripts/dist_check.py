@@ -23,10 +23,10 @@ sys.path.insert(0, ROOT)
 
 
 def main():
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    rank, world = dist.get_rank(), dist.get_world_size()
+    from paper_2104_01253_b200 import runtime
+
+    comm = runtime.init_distributed()  # ranks may share GPUs (gloo + CUDA-IPC peers)
+    rank, world = comm.rank, comm.world
     import oracle
     import paper_2104_01253_b200 as kls
 
@@ -163,13 +163,11 @@ def main():
            and rep.n_matched == len(ks.values) and not ks.over_multiplicity
            and ks.vectors.shape[0] == op.m_local)
     res["ok"] = bool(ok)
-    flag = torch.tensor([1.0 if ok or rank != 0 else 0.0], device="cuda")
-    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+    flag = -comm.allreduce_max_float(-(1.0 if ok or rank != 0 else 0.0))
     if rank == 0:
         print(json.dumps(res), flush=True)
-    dist.barrier()
-    dist.destroy_process_group()
-    return 0 if flag.item() == 1.0 else 1
+    runtime.shutdown_distributed()
+    return 0 if flag == 1.0 else 1
 
 
 if __name__ == "__main__":

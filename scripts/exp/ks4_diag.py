@@ -4,8 +4,8 @@ beside the golden one.  torchrun --nproc-per-node N scripts/exp/ks4_diag.py"""
 import os, sys, json
 import numpy as np, torch, torch.distributed as dist
 sys.path.insert(0, "/root/repo")
-local = int(os.environ.get("LOCAL_RANK", "0")); torch.cuda.set_device(local)
-dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+from paper_2104_01253_b200 import runtime
+runtime.init_distributed()
 import paper_2104_01253_b200 as kls
 g4 = np.load("/root/repo/tests/golden/ks_config4_shape.npz")
 op4 = kls.CsrOperator(kls.manteuffel_build(kls.ManteuffelSpec(k=100, beta=0.5)))
@@ -17,4 +17,4 @@ if dist.get_rank() == 0:
         rel = np.abs(ks4.values - ref) / np.abs(ref); drift = np.abs(alt - ref) / np.abs(ref)
         out["max_rel"] = float(rel.max()); out["ratio_max"] = float(np.max(rel / np.maximum(1e-9, drift)))
     print(json.dumps(out))
-dist.destroy_process_group()
+runtime.shutdown_distributed()

@@ -32,7 +32,7 @@ for m in [int(float(v)) for v in os.environ.get("SIZES", "1e6,1e7").split(",")]:
 
         def k2():
             _lib.call("kls_dcgs2_update_dev", Q.data_ptr(), ld, m, j, w.data_ptr(), w2.data_ptr(),
-                      aw.data_ptr(), c.data_ptr(), 1, st)
+                      aw.data_ptr(), c.data_ptr(), 1, None, st)
 
         k1()
         torch.cuda.synchronize()

@@ -22,7 +22,7 @@ for it in range(6):
     if it == 3:
         e0.record()
     _lib.call("kls_dcgs2_update_dev", Q.data_ptr(), ld, m, j, w.data_ptr(), w2.data_ptr(),
-              aw.data_ptr(), c.data_ptr(), 1, st)
+              aw.data_ptr(), c.data_ptr(), 1, None, st)
 e1.record()
 torch.cuda.synchronize()
 us = e0.elapsed_time(e1) * 1e3 / 3

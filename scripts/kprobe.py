@@ -53,7 +53,7 @@ def main():
         g = timeit(lambda: _lib.call("kls_gram_dcgs2", Q.data_ptr(), ld, m, j, w.data_ptr(),
                                      aw.data_ptr(), out.data_ptr(), None, ws, wsb, st), a.reps)
         u = timeit(lambda: _lib.call("kls_dcgs2_update", Q.data_ptr(), ld, m, j, w.data_ptr(),
-                                     aw.data_ptr(), coef.data_ptr(), 1.0, 1, st), a.reps)
+                                     aw.data_ptr(), coef.data_ptr(), 1.0, 1, None, st), a.reps)
         res[f"gram_j{j}_ms"] = g * 1e3
         res[f"gram_j{j}_GBs"] = 8 * m * (j + 2) / g / 1e9
         res[f"update_j{j}_ms"] = u * 1e3

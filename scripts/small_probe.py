@@ -32,6 +32,6 @@ for m in [int(float(v)) for v in os.environ.get("SIZES", "1e4,1e5,1e6").split(",
                                          aw.data_ptr(), out.data_ptr(), coef.data_ptr(), None, 0,
                                          None, ws, wsb, st))
         t_upd = bench(lambda: _lib.call("kls_dcgs2_update_dev", Q.data_ptr(), ld, m, j, w.data_ptr(),
-                                        w2.data_ptr(), aw.data_ptr(), coef.data_ptr(), 1, st))
+                                        w2.data_ptr(), aw.data_ptr(), coef.data_ptr(), 1, None, st))
         print(json.dumps({"m": m, "j": j, "gram_us": round(t_gram, 2), "update_us": round(t_upd, 2),
                           "env": {k: os.environ.get(k) for k in ("KLS_GRAM", "KLS_UPDATE")}}), flush=True)

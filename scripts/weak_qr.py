@@ -16,7 +16,6 @@ import os
 import sys
 
 import torch
-import torch.distributed as dist
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
@@ -27,16 +26,15 @@ def main():
     ap.add_argument("--n", default="25,50,100,200")
     ap.add_argument("--density", type=float, default=1e-3)
     a = ap.parse_args()
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    rank = dist.get_rank() if world > 1 else 0
+    from paper_2104_01253_b200 import runtime
+
+    comm = runtime.init_distributed()
+    world, rank = comm.world, comm.rank
     import paper_2104_01253_b200 as kls
 
-    ml = a.m_per_gpu
-    m = ml * world
+    m = a.m_per_gpu * world
+    lo, hi = runtime.seg_range(m, 64, world, rank)  # this rank's rows (24-segment layout)
+    ml = hi - lo
     for n in (int(v) for v in a.n.split(",")):
         g = torch.Generator(device="cuda")
         g.manual_seed(1729 + 7919 * rank)
@@ -52,7 +50,7 @@ def main():
         run()
         torch.cuda.synchronize()
         if world > 1:
-            dist.barrier()
+            comm.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         led = kls.SyncLedger()
         e0.record()
@@ -61,12 +59,10 @@ def main():
         torch.cuda.synchronize()
         sec = e0.elapsed_time(e1) * 1e-3
         if world > 1:
-            t = torch.tensor([sec], device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            sec = float(t.item())
-            dist.barrier()
+            sec = comm.allreduce_max_float(sec)
+            comm.barrier()
         loo = kls.loss_of_orthogonality(Q)
-        bytes_per_gpu = sum(8 * ml * (2 * j + 6) for j in range(n))
+        bytes_per_gpu = sum(8 * (m / world) * (2 * j + 6) for j in range(n))
         if rank == 0:
             print(json.dumps({"config": 5, "gpus": world, "m_per_gpu": ml, "m": m, "n": n,
                               "seconds": sec, "columns_per_s": n / sec,
@@ -74,8 +70,7 @@ def main():
                               "reductions": led.reductions}), flush=True)
         del A, Q, R
         torch.cuda.empty_cache()
-    if world > 1:
-        dist.destroy_process_group()
+    runtime.shutdown_distributed()
 
 
 if __name__ == "__main__":

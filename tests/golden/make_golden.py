@@ -468,6 +468,38 @@ def ks_config4_ensemble(kls, nperm=24):
                         nlocked=np.array([r[3] for r in runs]))
 
 
+def band_random(kls):
+    """Config 5's Arnoldi variant: the banded random operator of
+    oracle.band_random_coo assembled by the reference's CsrMatrix.from_coo
+    (problems.py:99-117) -- golden CSR arrays for several shapes, edge and
+    interior rows -- and the reference's DCGS2 / CGS2 Arnoldi on it at
+    m = 50,000 (band 1000, 7 per row), 60 steps, start PCG64(1729)."""
+    sys.path.insert(0, os.path.dirname(os.path.dirname(OUT)))
+    import oracle
+
+    out = {}
+    for tag, (m, band, d, seed) in {"small": (37, 4, 3, 11), "edge": (1000, 999, 8, 5),
+                                    "mid": (50_000, 1000, 7, 2525)}.items():
+        r, c, v = oracle.band_random_coo(m, band, d, seed)
+        csr = kls.CsrMatrix.from_coo(m, m, r, c, v)
+        out[f"{tag}_shape"] = np.array([m, band, d, seed])
+        keep = slice(None) if m <= 1000 else np.r_[0:7000, csr.nnz - 7000:csr.nnz]
+        out[f"{tag}_indptr"] = csr.indptr if m <= 1000 else csr.indptr[::97]
+        out[f"{tag}_indices"], out[f"{tag}_data"] = csr.indices[keep], csr.data[keep]
+        out[f"{tag}_datasum"] = np.array([np.sum(csr.data), np.sum(csr.indices)])
+    m, band, d, seed = 50_000, 1000, 7, 2525
+    r, c, v = oracle.band_random_coo(m, band, d, seed)
+    op = kls.CsrOperator(kls.CsrMatrix.from_coo(m, m, r, c, v))
+    start = np.random.Generator(np.random.PCG64(1729)).standard_normal(m)
+    for scheme in ("dcgs2", "cgs2"):
+        led = kls.SyncLedger()
+        V, H = kls.arnoldi_expand(op, start, scheme, steps=60, ledger=led)
+        out[f"arnoldi_{scheme}_H"] = H
+        out[f"arnoldi_{scheme}_Vrows"] = V[::997]
+        out[f"arnoldi_{scheme}_reductions"] = led.reductions
+    np.savez_compressed(os.path.join(OUT, "band_random.npz"), **out)
+
+
 def arnoldi_config3_shape(kls):
     """BASELINE config 3's expansion (3-D Poisson 7-point, x slowest, n = 100,
     start PCG64(1729)) on one GPU's share of the 8-GPU split scaled down:
@@ -565,6 +597,11 @@ if __name__ == "__main__":
         import kls
 
         ks_config4_ensemble(kls)
+    elif sys.argv[1:] == ["--only", "band_random"]:
+        sys.path.insert(0, REF)
+        import kls
+
+        band_random(kls)
     elif sys.argv[1:] == ["--only", "gmres_config2"]:
         sys.path.insert(0, REF)
         import kls

@@ -73,7 +73,7 @@ def test_fuzz_update(m, j, divide, seed):
     wo = torch.empty_like(wd)
     coef = torch.from_numpy(np.concatenate([c, t, [alpha]])).cuda()
     lib.call("kls_dcgs2_update_dev", qb.data_ptr(), ld, m, j, wd.data_ptr(), wo.data_ptr(),
-             awd.data_ptr(), coef.data_ptr(), divide, rt.stream_handle())
+             awd.data_ptr(), coef.data_ptr(), divide, None, rt.stream_handle())
     q = (w - Q[:, :j] @ c) / alpha
     a = aw / alpha if divide else aw
     wn = a - (Q[:, :j] @ t[:j] + q * t[j])

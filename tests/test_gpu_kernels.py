@@ -131,7 +131,7 @@ def test_dcgs2_update_matches_numpy(cuda, rng, m, j, divide):
     awd = torch.from_numpy(aw).cuda()
     coef = torch.from_numpy(np.concatenate([c, t])).cuda()
     lib.call("kls_dcgs2_update", qb.data_ptr(), ld, m, j, wd.data_ptr(), awd.data_ptr(),
-             coef.data_ptr(), alpha, divide, rt.stream_handle())
+             coef.data_ptr(), alpha, divide, None, rt.stream_handle())
     u = w - Q[:, :j] @ c
     q = u / alpha
     a = aw / alpha if divide else aw
@@ -363,3 +363,49 @@ def test_ell_resid_norms_fused(cuda, rng, k, beta):
     xh, bh = x.cpu().numpy(), b.cpu().numpy()
     want = [np.sum((bh - y) ** 2), xh @ xh, bh @ bh]
     assert np.allclose(out.cpu().numpy(), want, rtol=1e-12, atol=0)
+
+
+@pytest.mark.parametrize("tag", ["small", "edge", "mid"])
+def test_device_built_band_random_matches_reference(cuda, rng, tag):
+    """kls_build_band_csr (config 5's Arnoldi operator) is bitwise the
+    reference's CsrMatrix.from_coo of the restated generator
+    (tests/golden/band_random.npz), and its product is CsrMatrix.matvec's."""
+    from paper_2104_01253_b200 import band_random_operator
+
+    g = golden("band_random.npz")
+    m, band, d, seed = (int(v) for v in g[f"{tag}_shape"])
+    dev = band_random_operator(m, band=band, per_row=d, seed=seed)
+    ptr = dev._rowptr.cpu().numpy()
+    col = dev._col.cpu().numpy()[: m * d]
+    val = dev._val.cpu().numpy()[: m * d]
+    if m <= 1000:
+        assert np.array_equal(ptr, g[f"{tag}_indptr"])
+        assert np.array_equal(col, g[f"{tag}_indices"])
+        assert np.array_equal(val, g[f"{tag}_data"])
+    else:
+        keep = np.r_[0:7000, m * d - 7000 : m * d]
+        assert np.array_equal(ptr[::97], g[f"{tag}_indptr"])
+        assert np.array_equal(col[keep], g[f"{tag}_indices"])
+        assert np.array_equal(val[keep], g[f"{tag}_data"])
+        assert np.array_equal(g[f"{tag}_datasum"], [np.sum(val), np.sum(col)])
+    r, c, v = oracle.band_random_coo(m, band, d, seed)
+    x = rng.standard_normal(m)
+    assert np.array_equal(dev.apply(x).cpu().numpy(), oracle.csr_matvec(ptr, c, v, x))
+
+
+@pytest.mark.parametrize("scheme", ["dcgs2", "cgs2"])
+def test_band_random_arnoldi_vs_reference(cuda, scheme):
+    """Config 5's Arnoldi variant at m = 50,000 (band 1000, 7 per row, 60
+    steps) against the reference's own run: H within 1e-10 relative, the same
+    reduction count, basis rows within 1e-10."""
+    import paper_2104_01253_b200 as K
+
+    g = golden("band_random.npz")
+    op = K.band_random_operator(50_000, band=1000, per_row=7, seed=2525)
+    start = np.random.Generator(np.random.PCG64(1729)).standard_normal(50_000)
+    led = K.SyncLedger()
+    V, H = K.arnoldi_expand(op, start, scheme, steps=60, ledger=led)
+    ref = g[f"arnoldi_{scheme}_H"]
+    assert np.max(np.abs(H - ref)) <= 1e-10 * np.max(np.abs(ref))
+    assert led.reductions == int(g[f"arnoldi_{scheme}_reductions"])
+    assert np.max(np.abs(V.cpu().numpy()[::997] - g[f"arnoldi_{scheme}_Vrows"])) <= 1e-10

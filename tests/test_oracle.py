@@ -132,3 +132,27 @@ def test_arnoldi_config3_shape(scheme):
     ref = g[f"{scheme}_H"]
     assert np.max(np.abs(H - ref)) <= 1e-13 * np.max(np.abs(ref))
     assert cnt.reductions == g[f"{scheme}_reductions"]
+
+
+@pytest.mark.parametrize("tag", ["small", "edge", "mid"])
+def test_band_random_restatement_vs_reference_from_coo(tag):
+    """oracle.band_random_coo through a CSR assembly equals the reference's
+    CsrMatrix.from_coo (problems.py:99-117) of the same entries
+    (tests/golden/band_random.npz): distinct ascending columns per row, so
+    the CSR is the COO in row-major order."""
+    g = golden("band_random.npz")
+    m, band, d, seed = (int(v) for v in g[f"{tag}_shape"])
+    r, c, v = oracle.band_random_coo(m, band, d, seed)
+    indptr = np.arange(m + 1, dtype=np.int64) * d
+    assert np.all(np.diff(c.reshape(m, d), axis=1) > 0)
+    assert np.all(np.abs(c - r) <= band)
+    if m <= 1000:
+        assert np.array_equal(g[f"{tag}_indptr"], indptr)
+        assert np.array_equal(g[f"{tag}_indices"], c)
+        assert np.array_equal(g[f"{tag}_data"], v)
+    else:
+        keep = np.r_[0:7000, m * d - 7000 : m * d]
+        assert np.array_equal(g[f"{tag}_indptr"], indptr[::97])
+        assert np.array_equal(g[f"{tag}_indices"], c[keep])
+        assert np.array_equal(g[f"{tag}_data"], v[keep])
+        assert np.array_equal(g[f"{tag}_datasum"], [np.sum(v), np.sum(c)])
