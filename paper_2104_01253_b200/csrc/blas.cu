@@ -4,6 +4,9 @@
 // the Krylov-Schur basis rotation V(:, a:b) <- V(:, a:b) Z (eig.py:237).
 #include "reduce.cuh"
 #include "seg.cuh"
+#include "tma.cuh"
+
+#include <cstdlib>
 
 namespace {
 
@@ -182,6 +185,129 @@ __global__ void __launch_bounds__(kThreads, 2)
   }
 }
 
+// fp64 tensor-core (DMMA, mma.sync m8n8k4) form of the same rotation, for
+// k <= 64: a producer warp streams 128-row tiles of all k columns into a
+// 2-3 stage shared-memory ring with cp.async.bulk (mbarrier completion);
+// each of the 8 consumer warps owns 16 rows of the tile and forms its
+// 16 x 32 output block per pass as 2 x 4 mma tiles, A fragments from the
+// tile (leading dimension 136: conflict-free), B fragments from Z (shared,
+// zero-padded to a multiple of 4 rows), accumulating in k order.
+constexpr int kMmaRows = 128;
+constexpr int kMmaLd = 136;
+constexpr int kMmaThreads = 288;
+
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(kMmaThreads, 1)
+    rotate_mma_kernel(double* __restrict__ V, int64_t ldv, int64_t m, int32_t k, int32_t p,
+                      const double* __restrict__ Z, int32_t kp, int32_t zp, int32_t stages) {
+  using namespace kls::tma;
+  extern __shared__ __align__(128) unsigned char smr_raw[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smr_raw);
+  uint64_t* empty = full + 4;
+  double* zs = reinterpret_cast<double*>(smr_raw + 128);         // [kp][zp]
+  double* ring = zs + static_cast<size_t>(kp) * zp;              // [stages][kp][kMmaLd]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < kp * zp; i += blockDim.x) {
+    const int r = i / zp, c = i % zp;
+    zs[i] = (r < k && c < p) ? Z[static_cast<int64_t>(c) * k + r] : 0.0;
+  }
+  // ring columns k..kp-1 are never loaded: zero (they meet zero rows of Z)
+  for (int i = threadIdx.x; i < stages * (kp - k) * kMmaLd; i += blockDim.x) {
+    const int st = i / ((kp - k) * kMmaLd), rem = i % ((kp - k) * kMmaLd);
+    ring[(static_cast<size_t>(st) * kp + k) * kMmaLd + rem] = 0.0;
+  }
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < stages; ++st) {
+      mbar_init(full + st, 1);
+      mbar_init(empty + st, kWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+  const int64_t ntiles = (m + kMmaRows - 1) / kMmaRows;
+  if (warp == kWarps) {  // producer
+    if (lane == 0) {
+      uint32_t use = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++use) {
+        const int st = use % stages;
+        const uint32_t round = use / stages;
+        if (round >= 1) mbar_wait(empty + st, (round - 1) & 1);
+        const int64_t row0 = t * kMmaRows;
+        const int64_t nr = m - row0 < kMmaRows ? m - row0 : kMmaRows;
+        const uint32_t bytes = static_cast<uint32_t>(nr & ~int64_t(1)) * sizeof(double);
+        mbar_expect_tx(full + st, bytes * static_cast<uint32_t>(k));
+        if (bytes)
+          for (int c = 0; c < k; ++c)
+            bulk_g2s(ring + (static_cast<size_t>(st) * kp + c) * kMmaLd,
+                     V + static_cast<int64_t>(c) * ldv + row0, bytes, full + st);
+      }
+    }
+    return;
+  }
+  const int npass = (p + 31) / 32;
+  const int r_a = 16 * warp + (lane >> 2);  // tile row of the A fragment (+8 for block 1)
+  const int kq = lane & 3;
+  uint32_t use = 0;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++use) {
+    const int st = use % stages;
+    mbar_wait(full + st, (use / stages) & 1);
+    const double* tile = ring + static_cast<size_t>(st) * kp * kMmaLd;
+    const int64_t row0 = t * kMmaRows;
+    const int64_t nr = m - row0 < kMmaRows ? m - row0 : kMmaRows;
+    if (nr & 1) {  // the odd last row is not in the bulk copy
+      double* tw = ring + static_cast<size_t>(st) * kp * kMmaLd;
+      for (int c = threadIdx.x; c < k; c += kWarps * 32)
+        tw[c * kMmaLd + nr - 1] = V[static_cast<int64_t>(c) * ldv + row0 + nr - 1];
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+    }
+    for (int pass = 0; pass < npass; ++pass) {
+      double acc[2][4][2];
+#pragma unroll
+      for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+      const double* zcol = zs + pass * 32 + (lane >> 2);
+#pragma unroll 4
+      for (int kk = 0; kk < kp; kk += 4) {
+        const double* trow = tile + (kk + kq) * kMmaLd;
+        const double a0 = trow[r_a], a1 = trow[r_a + 8];
+        const double* zr = zcol + (kk + kq) * zp;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const double bv = zr[8 * b];
+          dmma884(acc[0][b][0], acc[0][b][1], a0, bv);
+          dmma884(acc[1][b][0], acc[1][b][1], a1, bv);
+        }
+      }
+#pragma unroll
+      for (int a = 0; a < 2; ++a) {
+        const int64_t row = row0 + 16 * warp + 8 * a + (lane >> 2);
+        if (row >= m) continue;
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int col = pass * 32 + 8 * b + 2 * kq + e;
+            if (col < p) V[static_cast<int64_t>(col) * ldv + row] = acc[a][b][e];
+          }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty + st);
+  }
+}
+
+size_t rotate_mma_smem(int kp, int zp, int stages) {
+  return 128 + sizeof(double) * (static_cast<size_t>(kp) * zp +
+                                 static_cast<size_t>(stages) * kp * kMmaLd);
+}
+
 size_t rotate_smem(int k, int zp, int nbuf) {
   return sizeof(double) *
          (static_cast<size_t>(k) * zp + static_cast<size_t>(nbuf) * k * kRotRows);
@@ -198,6 +324,28 @@ KLS_API int kls_tsgemm_inplace_cols(double* V, int64_t ldv, int64_t m, int32_t k
   if (V == nullptr || Z == nullptr || m < 0 || k < 0 || p < 0 || p > k || ldv < m)
     return fail(KLS_EINVAL, "tsgemm_inplace_cols: bad arguments");
   if (m == 0 || k == 0 || p == 0) return KLS_OK;
+  static const bool use_mma = [] {  // KLS_ROTATE=fma: the DFMA kernel (experiments)
+    const char* e = getenv("KLS_ROTATE");
+    return !(e != nullptr && e[0] == 'f');
+  }();
+  {
+    const int kp = (k + 3) / 4 * 4;
+    const int zpm = (p + 31) / 32 * 32 + 8;  // B fragments conflict-free
+    int stages = 3;
+    while (stages > 1 && rotate_mma_smem(kp, zpm, stages) > 227 * 1024) --stages;
+    if (use_mma && k <= 64 && stages >= 2 && (reinterpret_cast<uintptr_t>(V) & 15) == 0 &&
+        (ldv & 1) == 0) {
+      const size_t smem = rotate_mma_smem(kp, zpm, stages);
+      cudaError_t e = cudaFuncSetAttribute(rotate_mma_kernel,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(smem));
+      if (e != cudaSuccess) return fail(KLS_ECUDA, "rotate_mma smem: %s", cudaGetErrorString(e));
+      const int grid = static_cast<int>(std::min<int64_t>(ceil_div(m, kMmaRows), sm_count()));
+      rotate_mma_kernel<<<grid, kMmaThreads, smem, static_cast<cudaStream_t>(stream)>>>(
+          V, ldv, m, k, p, Z, kp, zpm, stages);
+      return check_launch("rotate_mma_kernel");
+    }
+  }
   const int zp = ((p + 31) / 32) * 32;
   const int dbuf = rotate_smem(k, zp, 2) <= 227 * 1024 ? 1 : 0;  // double-buffered tiles when they fit
   const size_t smem = rotate_smem(k, zp, dbuf ? 2 : 1);
@@ -239,9 +387,9 @@ KLS_API int kls_resid_norms(const double* b, const double* ax, const double* x, 
       ws == nullptr || n < 0)
     return fail(KLS_EINVAL, "resid_norms: bad arguments");
   seg::SimpleArgs a;
-  int rc = seg::make_plan_simple(segs, n, kThreads, a, ws, ws_bytes, 3, out);
+  int rc = seg::make_plan_simple(segs, n, 1024, a, ws, ws_bytes, 3, out);
   if (rc) return rc;
-  const int grid = std::max(1, std::min(a.P.nitems, 4 * sm_count()));
+  const int grid = std::max(1, std::min(a.P.nitems, 8 * sm_count()));
   resid_norms_kernel<<<grid, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(b, ax, x, a);
   return check_launch("resid_norms_kernel");
 }

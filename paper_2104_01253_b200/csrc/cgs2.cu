@@ -159,17 +159,16 @@ struct PgArgs {
 };
 
 // Item epilogue of both variants: the 8 warps' accumulators (sacc rows,
-// stride) and xn in warp order -> the item partial; the finishing CTA runs
-// the segment tree.  Returns whether this CTA finished the launch.
-__device__ __forceinline__ bool pg_commit(const PgArgs& a, int it, int s, int V, const double* sacc,
-                                          int stride, double xn, double* s_red, int* s_flag) {
+// stride) and xn in warp order -> the item partial (plain stores).
+__device__ __forceinline__ void pg_store(const PgArgs& a, int it, const double* sacc, int stride,
+                                         double xn) {
   __shared__ double sx[kWarps];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const double t = warp_sum(xn);
   if (lane == 0) sx[warp] = t;
   __syncthreads();
   const int nv = a.k + (a.xnorm ? 1 : 0);
-  return seg::item_commit<kThreads, 0>(a.P, a.ws, it, s, V, nv, threadIdx.x, s_red, s_flag, [&](int i) {
+  seg::item_store<kThreads>(a.ws, it, nv, threadIdx.x, [&](int i) {
     double r = 0.0;
     if (i < a.k) {
 #pragma unroll
@@ -180,6 +179,7 @@ __device__ __forceinline__ bool pg_commit(const PgArgs& a, int it, int s, int V,
     }
     return r;
   });
+  __syncthreads();  // sacc / sx are read: the next item may reset them
 }
 
 template <int NC>
@@ -200,7 +200,6 @@ __global__ void __launch_bounds__(kThreads, kPBlocks)
   double* wacc = sacc + warp * stride;
   constexpr int64_t WROWS = 64 * kPRP;
   constexpr int64_t CROWS = WROWS * kWarps;
-  bool fin = false;
   for (int it = blockIdx.x; it < a.P.nitems; it += gridDim.x) {
     int sg, vi, V;
     seg::item_of(a.P, it, sg, vi, V);
@@ -219,10 +218,12 @@ __global__ void __launch_bounds__(kThreads, kPBlocks)
       else
         pg_chunk<true>(pr, vs, ss, wbase, lane, wacc, xn);
     }
-    fin = pg_commit(a, it, sg, V, sacc, stride, xn, s_red, &s_flag) || fin;
+    pg_store(a, it, sacc, stride, xn);
   }
-  if (fin) seg::seg_final<kThreads, 0>(a.P.L, a.ws, a.k + (a.xnorm ? 1 : 0), a.d, threadIdx.x, &s_ok,
-                                       [](int o) { return (int64_t)o; });
+  const int nv = a.k + (a.xnorm ? 1 : 0);
+  if (seg::finish_items<kThreads, 0>(a.P, a.ws, nv, threadIdx.x, s_red, &s_flag))
+    seg::seg_final<kThreads, 0>(a.P.L, a.ws, nv, a.d, threadIdx.x, &s_ok,
+                                [](int o) { return (int64_t)o; });
 }
 
 template <int NC>
@@ -281,7 +282,6 @@ __global__ void __launch_bounds__(kThreads, CPW >= 32 ? 1 : 2)
   const int lane = threadIdx.x & 31;
   double* mypart = part + warp * R;
   double* wacc = sacc + warp * stride;
-  bool fin = false;
   for (int it = blockIdx.x; it < a.P.nitems; it += gridDim.x) {
     int sg, vi, V;
     seg::item_of(a.P, it, sg, vi, V);
@@ -367,10 +367,12 @@ __global__ void __launch_bounds__(kThreads, CPW >= 32 ? 1 : 2)
       for (int64_t b0 = nfull * R; b0 < rows; b0 += 64 * kPRP * kWarps)
         pg_chunk<true>(pr, vs, ss, b0 + warp * 64 * kPRP, lane, wacc, xn);
     }
-    fin = pg_commit(a, it, sg, V, sacc, stride, xn, s_red, &s_flag) || fin;
+    pg_store(a, it, sacc, stride, xn);
   }
-  if (fin) seg::seg_final<kThreads, 0>(a.P.L, a.ws, k + (a.xnorm ? 1 : 0), a.d, threadIdx.x, &s_ok,
-                                       [](int o) { return (int64_t)o; });
+  const int nv = k + (a.xnorm ? 1 : 0);
+  if (seg::finish_items<kThreads, 0>(a.P, a.ws, nv, threadIdx.x, s_red, &s_flag))
+    seg::seg_final<kThreads, 0>(a.P.L, a.ws, nv, a.d, threadIdx.x, &s_ok,
+                                [](int o) { return (int64_t)o; });
 }
 
 template <int CPW, int NC>

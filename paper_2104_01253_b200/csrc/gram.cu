@@ -17,6 +17,8 @@
 // determinism rule, kernels.py:11-12).
 #include "gram.cuh"
 
+#include <cstdlib>
+
 namespace {
 
 using namespace kls;
@@ -29,7 +31,7 @@ using namespace kls::gram;
 // CTA evaluates its output's local segment tree; with several ranks it
 // publishes the exported nodes, and the last CTA to finish (ticket)
 // exchanges them (fused peers) and runs the fused DCGS2 scalar step.
-constexpr int kColThreads = 512;
+constexpr int kColThreads = 768;  // 24 warps: one per local segment
 constexpr int kColWarps = kColThreads / 32;
 constexpr int64_t kColRows = 1 << 15;  // global m at or below this: gram_cols_kernel
 
@@ -57,13 +59,36 @@ __global__ void __launch_bounds__(kColThreads) gram_cols_kernel(GramParams p) {
 #pragma unroll
     for (int t = 0; t < NX; ++t) acc[t] = 0.0;
     const double2* l2 = reinterpret_cast<const double2*>(left + a);
+    const double2* x2[2] = {reinterpret_cast<const double2*>(xs[0] + a),
+                            reinterpret_cast<const double2*>(xs[NX - 1] + a)};
     const int64_t npair = rows / 2;
-    for (int64_t i = lane; i < npair; i += 32) {
+    int64_t i = lane;
+    // four row pairs' loads in flight, then their fmas in row order (the
+    // same sequential per-lane chain as the one-pair loop below)
+    for (; i + 96 < npair; i += 128) {
+      double2 av[4], xv[NX][4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        av[u] = l2[i + 32 * u];
+#pragma unroll
+        for (int t = 0; t < NX; ++t)
+          if (t < nt) xv[t][u] = x2[t][i + 32 * u];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int t = 0; t < NX; ++t)
+          if (t < nt) {
+            acc[t] = fma(av[u].x, xv[t][u].x, acc[t]);
+            acc[t] = fma(av[u].y, xv[t][u].y, acc[t]);
+          }
+    }
+    for (; i < npair; i += 32) {
       const double2 av = l2[i];
 #pragma unroll
       for (int t = 0; t < NX; ++t)
         if (t < nt) {
-          const double2 x = reinterpret_cast<const double2*>(xs[t] + a)[i];
+          const double2 x = x2[t][i];
           acc[t] = fma(av.x, x.x, acc[t]);
           acc[t] = fma(av.y, x.y, acc[t]);
         }
@@ -84,12 +109,12 @@ __global__ void __launch_bounds__(kColThreads) gram_cols_kernel(GramParams p) {
   const bool fused = L.world > 1 && p.d.peers.world > 1;
   if (tid < nt) {
     const int i = norm_row ? nv - 1 : c < p.k ? c * NX + tid : nq + tid;
-    double val[seg::kNodes];
-    seg::local_tree_from(L, [&](int s) { return s_seg[s][tid]; }, val);
     const int64_t dst = gram_dst<NX>(p, i);
     if (L.world == 1) {
-      p.d.out[dst] = val[seg::kRoot];
+      p.d.out[dst] = seg::root24([&](int s) { return s_seg[s][tid]; });
     } else {
+      double val[seg::kNodes];
+      seg::local_tree_from(L, [&](int s) { return s_seg[s][tid]; }, val);
       int ids[seg::kMaxExport];
       const int ne = seg::exports(L.gseg0, L.gseg0 + L.nseg, ids);
       double* mine = fused ? peer::slot(p.d.peers.buf[p.d.peers.rank], p.d.peers.cap, p.d.epoch) : nullptr;
@@ -152,7 +177,11 @@ int launch_gram(GramParams p, int64_t m_global, size_t ws_bytes, cudaStream_t st
     return launch_gram_cols<NX>(p, st);
   }
   if (!tma_eligible(p)) return fail(KLS_EINVAL, "gram: operands must be 16-byte aligned, ldq even");
-  seg::make_plan(p.P.L, 64, kTmaVirt, p.P);
+  static const int vmax = [] {  // KLS_TMA_VIRT: experiments only (changes the tree)
+    const char* e = getenv("KLS_TMA_VIRT");
+    return e != nullptr && atoi(e) > 0 ? atoi(e) : kTmaVirt;
+  }();
+  seg::make_plan(p.P.L, 8192, vmax, p.P);
   const int nv = gram_nv(p, NX);
   if (seg::plan_ws_bytes(p.P, nv) > ws_bytes)
     return fail(KLS_ENOSPC, "gram: workspace %zu bytes < %zu needed", ws_bytes,

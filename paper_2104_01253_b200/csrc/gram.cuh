@@ -130,8 +130,9 @@ __device__ __forceinline__ void gram_chunk(const GramRows& p, int64_t wbase, int
 template <int NX>
 int launch_gram_tma(GramParams p, cudaStream_t st);
 bool tma_eligible(const GramParams& p);
-// virtual CTAs per segment of the staged kernel (seg.cuh): at most this
-// many, one per 64 rows below that
+// virtual CTAs per segment of the staged kernel (seg.cuh): one per 8192
+// rows (so a medium-m launch is one item per CTA), at most this many (49:
+// the 3 segments of an 8-rank share keep 147 of 148 SMs busy)
 constexpr int kTmaVirt = 49;
 
 }  // namespace gram

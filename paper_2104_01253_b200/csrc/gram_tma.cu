@@ -8,9 +8,10 @@
 // V(s) that walk segment s with the chunk schedule of ChunkWalk (1024-row
 // chunks round-robin, the remainder split evenly).  A persistent CTA per SM
 // takes items round-robin; after each item the consumer warps sum their
-// per-warp accumulators in warp order into the item partial and commit it,
-// and the CTA that completes a segment reduces the segment's item partials
-// (fixed order).  The CTA that completes the launch's last segment
+// per-warp accumulators in warp order into the item partial and store it
+// (plain stores: nothing waits); after its last item a CTA publishes its
+// partials once and takes the segment tickets, and the CTA that completes a
+// segment reduces the segment's item partials (fixed order).  The CTA that completes the launch's last segment
 // evaluates the fixed segment tree (and, with NVLink peers, exchanges the
 // rank's exported nodes and combines them) and runs the fused DCGS2 scalar
 // step.  The arithmetic of every segment depends only on its rows, so the
@@ -225,25 +226,27 @@ __global__ void __launch_bounds__(kTmaThreads, 1) gram_tma_kernel(GramParams p) 
         if (lane == 0) sx[warp][NX] = sv;
       }
       seg::gsync<kConsumers, 1>();
-      const bool fin = seg::item_commit<kConsumers, 1>(
-          p.P, p.ws, it, s, Vn, nv, threadIdx.x, s_red, &s_flag, [&](int i) {
-            double t = 0.0;
-            if (i < nq) {
+      seg::item_store<kConsumers>(p.ws, it, nv, threadIdx.x, [&](int i) {
+        double t = 0.0;
+        if (i < nq) {
 #pragma unroll
-              for (int w = 0; w < kWarps; ++w) t += sacc[w * stride + i];
-            } else if (has_b && i < nq + NX) {
+          for (int w = 0; w < kWarps; ++w) t += sacc[w * stride + i];
+        } else if (has_b && i < nq + NX) {
 #pragma unroll
-              for (int w = 0; w < kWarps; ++w) t += sx[w][i - nq];
-            } else {
+          for (int w = 0; w < kWarps; ++w) t += sx[w][i - nq];
+        } else {
 #pragma unroll
-              for (int w = 0; w < kWarps; ++w) t += sx[w][NX];
-            }
-            return t;
-          });
-      if (fin && threadIdx.x == 0) s_fin = 1;
+          for (int w = 0; w < kWarps; ++w) t += sx[w][NX];
+        }
+        return t;
+      });
+      seg::gsync<kConsumers, 1>();  // every warp's accumulators are read
       for (int i = lane; i < stride; i += 32) wacc[i] = 0.0;
       __syncwarp();
     }
+    if (seg::finish_items<kConsumers, 1>(p.P, p.ws, nv, threadIdx.x, s_red, &s_flag) &&
+        threadIdx.x == 0)
+      s_fin = 1;
   }
   // the streaming is done: a dependent update (PDL) may start staging its
   // Q tiles while the final sums and the scalar step finish here

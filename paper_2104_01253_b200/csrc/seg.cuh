@@ -203,34 +203,73 @@ __device__ __forceinline__ void group_sum_partials(const double* partials, int n
   }
 }
 
-// Commit one item's nv values (get(i)) and, when it completes its segment,
-// reduce the segment.  Returns true in every thread of the group that
-// completed the LAST segment of the launch (it then runs seg_final).
-// s_red: NT doubles of shared memory; s_flag: one shared int.
-template <int NT, int BAR, typename Get>
-__device__ __forceinline__ bool item_commit(const Plan& P, Ws ws, int it, int s, int V, int nv,
-                                            int tid, double* s_red, int* s_flag, Get get) {
+// Store one item's nv values (get(i)) to its partial row: plain stores,
+// nothing waits (the fence and the segment tickets come once per CTA, in
+// finish_items).  The group must have finished the item's accumulation.
+template <int NT, typename Get>
+__device__ __forceinline__ void item_store(Ws ws, int it, int nv, int tid, Get get) {
   double* part = ws.part + static_cast<int64_t>(it) * nv;
   for (int i = tid; i < nv; i += NT) part[i] = get(i);
+}
+
+// Once per CTA after its last item: publish the CTA's item partials
+// (fence), take the segment tickets for the items it processed (items
+// blockIdx.x, + gridDim.x, ...), reduce every segment this CTA completed
+// (its V item partials in fixed order, group_sum_partials), and count
+// completed segments.  Returns true in the group of the CTA that completed
+// the LAST segment (it then runs seg_final).  s_red: NT doubles of shared
+// memory; s_flag: one shared int.
+template <int NT, int BAR>
+__device__ __forceinline__ bool finish_items(const Plan& P, Ws ws, int nv, int tid, double* s_red,
+                                             int* s_flag) {
+  __shared__ int s_seg[kG], s_cnt[kG], s_done[kG], s_nt;
   __threadfence();
   gsync<NT, BAR>();
-  if (tid == 0) *s_flag = atomicAdd(ws.tick + s, 1u) == static_cast<unsigned>(V - 1) ? 1 : 0;
+  if (tid == 0) {  // the segments this CTA's items belong to, with item counts
+    int n = 0;
+    for (int it = blockIdx.x; it < P.nitems; it += gridDim.x) {
+      int s = 0;
+      while (P.ibase[s + 1] <= it) ++s;
+      if (n == 0 || s_seg[n - 1] != s) {
+        s_seg[n] = s;
+        s_cnt[n] = 0;
+        ++n;
+      }
+      ++s_cnt[n - 1];
+    }
+    s_nt = n;
+  }
   gsync<NT, BAR>();
-  if (*s_flag == 0) return false;
-  __threadfence();
-  double* sv = ws.segv + static_cast<int64_t>(s) * nv;
-  group_sum_partials<NT, BAR>(ws.part + static_cast<int64_t>(P.ibase[s]) * nv, V, nv, tid, s_red,
-                              [&](int i, double t) { sv[i] = t; });
+  const int nt = s_nt;
+  if (tid < nt) {  // all tickets at once: one round trip
+    const int s = s_seg[tid];
+    const unsigned V = static_cast<unsigned>(P.ibase[s + 1] - P.ibase[s]);
+    s_done[tid] = atomicAdd(ws.tick + s, static_cast<unsigned>(s_cnt[tid])) + s_cnt[tid] == V;
+  }
+  gsync<NT, BAR>();
+  int completed = 0;
+  for (int k = 0; k < nt; ++k) {
+    if (!s_done[k]) continue;
+    const int s = s_seg[k];
+    const int V = P.ibase[s + 1] - P.ibase[s];
+    __threadfence();
+    double* sv = ws.segv + static_cast<int64_t>(s) * nv;
+    group_sum_partials<NT, BAR>(ws.part + static_cast<int64_t>(P.ibase[s]) * nv, V, nv, tid,
+                                s_red, [&](int i, double t) { sv[i] = t; });
+    if (tid == 0) ws.tick[s] = 0u;
+    ++completed;
+  }
+  if (completed == 0) return false;
   __threadfence();
   gsync<NT, BAR>();
   if (tid == 0) {
-    ws.tick[s] = 0u;
-    const bool last = atomicAdd(ws.tick + kG, 1u) == static_cast<unsigned>(P.L.nseg - 1);
+    const unsigned c = static_cast<unsigned>(completed);
+    const bool last = atomicAdd(ws.tick + kG, c) + c == static_cast<unsigned>(P.L.nseg);
     if (last) ws.tick[kG] = 0u;
-    *s_flag = last ? 2 : 0;
+    *s_flag = last ? 1 : 0;
   }
   gsync<NT, BAR>();
-  const bool fin = *s_flag == 2;
+  const bool fin = *s_flag != 0;
   if (fin) __threadfence();
   return fin;
 }
@@ -252,6 +291,18 @@ __device__ __forceinline__ void local_tree_from(const Layout& L, Leaf leaf, doub
   for (int l = a; l < b; ++l) val[l] = leaf(l - a);
   for (int n = kG; n < kNodes; ++n)
     if (node_inside(n, a, b)) val[n] = node_fold(n, val);
+}
+
+// The whole tree of one rank holding all 24 segments, straight-line (the
+// same folds as local_tree + combine: 8 groups of 3, then pairs, quads,
+// root), so the 24 leaf loads are independent.
+template <typename Leaf>
+__device__ __forceinline__ double root24(Leaf leaf) {
+  double g[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) g[i] = (leaf(3 * i) + leaf(3 * i + 1)) + leaf(3 * i + 2);
+  const double p0 = g[0] + g[1], p1 = g[2] + g[3], p2 = g[4] + g[5], p3 = g[6] + g[7];
+  return (p0 + p1) + (p2 + p3);
 }
 
 // Combine: val[] holds every rank's exported nodes (have[] marks them);
@@ -319,11 +370,13 @@ __device__ __forceinline__ bool seg_final(const Layout& L, Ws ws, int nv, const 
   const bool fused = L.world > 1 && d.peers.world > 1;
   double* mine = fused ? peer::slot(d.peers.buf[d.peers.rank], d.peers.cap, d.epoch) : nullptr;
   for (int o = tid; o < nv; o += NT) {
+    if (L.world == 1) {
+      d.out[dst(o)] = root24([&](int l) { return __ldcg(ws.segv + static_cast<int64_t>(l) * nv + o); });
+      continue;
+    }
     double val[kNodes];
     local_tree(L, ws.segv, nv, o, val);
-    if (L.world == 1) {
-      d.out[dst(o)] = val[kRoot];
-    } else if (fused) {
+    if (fused) {
       for (int e = 0; e < ne; ++e) mine[static_cast<int64_t>(e) * nv + o] = val[ids[e]];
     } else {
       for (int e = 0; e < ne; ++e) d.out[static_cast<int64_t>(e) * d.xstride + dst(o)] = val[ids[e]];
@@ -376,7 +429,6 @@ __device__ __forceinline__ void run_simple(const SimpleArgs& A, Body body) {
   __shared__ double s_red[NT];
   __shared__ double sv[NV];
   __shared__ int s_flag, s_ok;
-  bool fin = false;
   for (int it = blockIdx.x; it < A.P.nitems; it += gridDim.x) {
     int s, v, V;
     item_of(A.P, it, s, v, V);
@@ -386,10 +438,10 @@ __device__ __forceinline__ void run_simple(const SimpleArgs& A, Body body) {
     for (int i = 0; i < NV; ++i) acc[i] = 0.0;
     body(r0, A.P.L.off[s + 1] - r0, v, V, acc);
     block_sum<NV>(acc, sv);
-    fin = item_commit<NT, 0>(A.P, A.ws, it, s, V, NV, threadIdx.x, s_red, &s_flag,
-                             [&](int i) { return sv[i]; }) || fin;
+    item_store<NT>(A.ws, it, NV, threadIdx.x, [&](int i) { return sv[i]; });
   }
-  if (fin) seg_final<NT, 0>(A.P.L, A.ws, NV, A.d, threadIdx.x, &s_ok, [](int o) { return (int64_t)o; });
+  if (finish_items<NT, 0>(A.P, A.ws, NV, threadIdx.x, s_red, &s_flag))
+    seg_final<NT, 0>(A.P.L, A.ws, NV, A.d, threadIdx.x, &s_ok, [](int o) { return (int64_t)o; });
 }
 
 }  // namespace seg

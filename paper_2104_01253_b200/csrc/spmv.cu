@@ -563,7 +563,7 @@ KLS_API int kls_ell_resid_norms(const int32_t* ecol, const double* eval, const u
       out == nullptr || ws == nullptr || nrows < 0 || ld < nrows || width < 1 || width > 8)
     return fail(KLS_EINVAL, "ell_resid_norms: bad arguments");
   seg::SimpleArgs a;
-  int rc = seg::make_plan_simple(segs, nrows, kThreads, a, ws, ws_bytes, 3, out);
+  int rc = seg::make_plan_simple(segs, nrows, 1024, a, ws, ws_bytes, 3, out);
   if (rc) return rc;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   switch (width) {

@@ -2,7 +2,7 @@
 // (step.cu, kls_dcgs2_scalars) and the Gram kernels' last CTA (gram.cuh,
 // kls_gram_dcgs2_step): from g = [c(0:j), beta, s(0:j), s_piv, aw.aw] it
 // writes coef = [c, s / alpha (QR: s), t_piv, alpha] and copies g to gout.
-// Called by every thread of one CTA (any multiple of 32 threads up to 512).
+// Called by every thread of one CTA (any multiple of 32 threads up to 1024).
 #pragma once
 
 #include "common.cuh"
@@ -11,7 +11,7 @@ namespace kls {
 
 __device__ __forceinline__ void dcgs2_scalars_block(const double* g, int j, int qr, double* coef,
                                                     double* gout) {
-  __shared__ double red[2][16];
+  __shared__ double red[2][32];
   __shared__ double s_alpha;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nwarps = blockDim.x >> 5;

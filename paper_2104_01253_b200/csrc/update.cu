@@ -624,7 +624,7 @@ int mtm_common(double* Y, int64_t ldy, int64_t m, int32_t l, const double* B, in
   if (nrm_out != nullptr) {
     int rc = seg::make_layout(segs, m, a.P.L);
     if (rc) return rc;
-    seg::make_plan(a.P.L, 64 * kUpdRP * kWarps, kUpdVirt, a.P);
+    seg::make_plan(a.P.L, 1024, kUpdVirt, a.P);
     if (ws == nullptr || seg::plan_ws_bytes(a.P, 1) > ws_bytes)
       return fail(KLS_ENOSPC, "mv_times_mat_add_mv: workspace too small for the fused norm");
     a.ws = seg::ws_of(ws, a.P.nitems, 1);
@@ -671,7 +671,7 @@ KLS_API int kls_dcgs2_update_host(double* Q, int64_t ldq, int64_t m, int32_t j, 
 KLS_API int kls_dcgs2_update_dev(double* Q, int64_t ldq, int64_t m, int32_t j, const double* w,
                                  double* w_out, const double* aw, const double* coef_alpha,
                                  int32_t divide, const KlsSegs* segs, void* stream) {
-  if (coef_alpha == nullptr || w_out == nullptr)
+  if (coef_alpha == nullptr || (m > 0 && w_out == nullptr))
     return fail(KLS_EINVAL, "dcgs2_update_dev: null coefficients or output");
   return update_common(Q, ldq, m, j, const_cast<double*>(w), aw, coef_alpha, 0.0, divide, false,
                        segs, stream, coef_alpha + 2 * j + 1, w_out);

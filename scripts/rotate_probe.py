@@ -1,8 +1,9 @@
 """Krylov-Schur rotation kernel (kls_tsgemm_inplace_cols) at config 4's
 size: m = 1e7 rows, k = 60 basis columns, p = 30 kept columns; CUDA-event
-time and the achieved HBM rate on its 8 m (k + p) algorithmic bytes.
+time and the achieved HBM rate on its 8 m (k + p) algorithmic bytes.  The
+default is the DMMA kernel; KLS_ROTATE=fma selects the DFMA one.
 
-    python scripts/rotate_probe.py
+    python scripts/rotate_probe.py; KLS_ROTATE=fma python scripts/rotate_probe.py
 """
 import os, sys, json
 import torch
@@ -25,6 +26,7 @@ for k, p in ((60, 30), (60, 60), (30, 15)):
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / 10
-    print(json.dumps({"m": m, "k": k, "p": p, "ms": round(ms, 3),
+    print(json.dumps({"kernel": os.environ.get("KLS_ROTATE", "mma"), "m": m, "k": k, "p": p,
+                      "ms": round(ms, 3),
                       "TBs": round(8 * m * (k + p) / ms / 1e9, 2),
                       "fp64_TFs": round(2 * m * k * p / ms / 1e9, 2)}))

@@ -137,3 +137,55 @@ def test_krylov_schur_config4_settings_vs_reference(cuda):
     # values are pseudospectral (eigenvalue condition numbers ~1e10,
     # PAPER.md:809-823), so their eigenvectors are ill-determined
     assert np.all(np.asarray(res.residuals) < cfg.tol)
+
+
+def test_krylov_schur_config4_full_size_vs_reference(cuda):
+    """BASELINE config 4 AT FULL SIZE (ManteuffelSpec(k=3163, beta=0.5),
+    m = 10,004,569, max_basis 60, tol 1e-7, DCGS2, seed 1729) against the
+    reference's own run (tests/golden/ks_config4_full.npz: hours of reference
+    CPU time, checkpointed every restart by make_golden.py --only
+    ks_config4_full).  Restart by restart, the active block has the same size
+    and every one of its Ritz values matches the reference's within 1e-9
+    relative; when the reference run reached its
+    locks, the lock history and the locked values are compared too."""
+    K = kls()
+    import paper_2104_01253_b200.eig as keig
+
+    g = golden("ks_config4_full.npz")
+    nref = len(g["na"])
+    assert nref >= 10
+    done = "done" in g.files
+    rec = []
+    orig = keig._schur_of
+
+    def spy(block):
+        rec.append(np.sort_complex(np.linalg.eigvals(block)))
+        return orig(block)
+
+    keig._schur_of = spy
+    try:
+        op = K.manteuffel_operator(K.ManteuffelSpec(k=3163, beta=0.5))
+        restarts = int(g["restarts"]) if done else nref
+        cfg = K.KrylovSchurConfig(max_basis=60, tol=1e-7, scheme="dcgs2", max_restarts=restarts)
+        res = K.krylov_schur_run(op, cfg, seed=1729)
+    finally:
+        keig._schur_of = orig
+    worst = 0.0
+    for i in range(min(nref, len(rec))):
+        ref = g["ritz"][i][: g["na"][i]]
+        assert rec[i].size == ref.size, i
+        rel = max(np.min(np.abs(rec[i] - x)) / abs(x) for x in ref)
+        worst = max(worst, rel)
+        if not np.any(np.array(res.lock_history[: i + 1]) > 0):  # before the first lock
+            assert rel <= 1e-9, (i, rel)
+    print(f"config 4 full size: {min(nref, len(rec))} restarts, worst Ritz deviation {worst:.2e}")
+    if done:
+        ref_lh = np.array(g["lock_history"])
+        lh = np.array(res.lock_history)
+        first = int(np.argmax(ref_lh > 0))
+        assert int(np.argmax(lh > 0)) == first and lh[first] == ref_lh[first]
+        ref_vals = g["values"]
+        got = np.asarray(res.values)
+        n10 = min(10, ref_vals.size, got.size)
+        rel = np.array([np.min(np.abs(got - x)) / abs(x) for x in ref_vals[:n10]])
+        assert np.all(rel <= 1e-6), rel

@@ -1,5 +1,7 @@
-"""Multi-GPU parity through torchrun + NCCL (runs when >= 2 GPUs are
-visible; the single-GPU round-end run skips it)."""
+"""Multi-rank parity through torchrun.  The NCCL tests need >= 2 GPUs; the
+rank-invariance and C-ABI peer tests also run with several ranks SHARING
+one GPU (gloo bootstrap + CUDA-IPC peer buffers), so the single-GPU
+round-end run exercises the sharded path too."""
 
 import json
 import os
@@ -32,15 +34,39 @@ def test_row_sharded_parity_nccl(cuda, want):
     assert res["ok"] and res["world"] == n, res
 
 
+def _torchrun(n, port, script, *args, timeout=600):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.join(ROOT, "scripts", script),
+           *args]
+    return subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, cwd=ROOT)
+
+
+def test_rank_count_invariance(cuda, tmp_path):
+    """The same problems on 1, 2 and 3 ranks (on however many GPUs there are:
+    ranks share a GPU when there are fewer) give BITWISE identical results:
+    Arnoldi H and basis rows (stencil, host and device CSR, DCGS2 / CGS2),
+    GMRES iterations and histories, Krylov-Schur lock history and values,
+    QR's R (scripts/rank_invariance.py)."""
+    outs = []
+    for n in (1, 2, 3):
+        out = str(tmp_path / f"rankinv_{n}.npz")
+        r = _torchrun(n, 29530 + n, "rank_invariance.py", "--out", out, timeout=900)
+        assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+        outs.append(out)
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "rank_invariance.py"),
+                        "--compare", *outs], capture_output=True, text=True, timeout=300, cwd=ROOT)
+    res = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    assert r.returncode == 0 and res["ok"], res
+
+
 def test_peer_capi_without_symmetric_memory(cuda):
     """C-ABI peer buffers (kls_peer_buffer_alloc/open, IPC handles) carry the
-    one-shot allreduce and the fused Gram + allreduce for a host that has no
-    collective allocator (scripts/peer_capi_check.py)."""
+    segment-tree combine and the fused Gram + combine for a host that has no
+    collective allocator, bitwise equal to one rank (scripts/peer_capi_check.py);
+    two ranks per GPU when there is one GPU."""
     import torch
 
-    n = min(torch.cuda.device_count(), 4)
-    if n < 2:
-        pytest.skip("needs >= 2 GPUs")
+    n = max(2, min(torch.cuda.device_count(), 4))
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr=127.0.0.1", "--master-port=29519",
            os.path.join(ROOT, "scripts", "peer_capi_check.py")]
