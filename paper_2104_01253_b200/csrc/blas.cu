@@ -333,7 +333,10 @@ KLS_API int kls_tsgemm_inplace_cols(double* V, int64_t ldv, int64_t m, int32_t k
     const int zpm = (p + 31) / 32 * 32 + 8;  // B fragments conflict-free
     int stages = 3;
     while (stages > 1 && rotate_mma_smem(kp, zpm, stages) > 227 * 1024) --stages;
-    if (use_mma && k <= 64 && stages >= 2 && (reinterpret_cast<uintptr_t>(V) & 15) == 0 &&
+    // measured at m = 1e7 (scripts/rotate_probe.py): DMMA 1.57 vs DFMA 2.24 ms
+    // at k = 60, p = 30; below k ~ 40 the DFMA kernel is faster (k = 30: 0.67
+    // vs 0.89 ms).  Both accumulate each output in k order: identical bits.
+    if (use_mma && k >= 40 && k <= 64 && stages >= 2 && (reinterpret_cast<uintptr_t>(V) & 15) == 0 &&
         (ldv & 1) == 0) {
       const size_t smem = rotate_mma_smem(kp, zpm, stages);
       cudaError_t e = cudaFuncSetAttribute(rotate_mma_kernel,
