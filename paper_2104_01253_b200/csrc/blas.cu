@@ -390,7 +390,7 @@ KLS_API int kls_resid_norms(const double* b, const double* ax, const double* x, 
       ws == nullptr || n < 0)
     return fail(KLS_EINVAL, "resid_norms: bad arguments");
   seg::SimpleArgs a;
-  int rc = seg::make_plan_simple(segs, n, 1024, a, ws, ws_bytes, 3, out);
+  int rc = seg::make_plan_simple(segs, n, 2048, a, ws, ws_bytes, 3, out);
   if (rc) return rc;
   const int grid = std::max(1, std::min(a.P.nitems, 8 * sm_count()));
   resid_norms_kernel<<<grid, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(b, ax, x, a);

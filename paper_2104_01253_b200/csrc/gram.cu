@@ -128,7 +128,10 @@ __global__ void __launch_bounds__(kColThreads) gram_cols_kernel(GramParams p) {
   }
   pdl_trigger();
   if (!fused && p.coef == nullptr) return;
-  __threadfence_system();
+  if (fused)
+    __threadfence_system();  // the exports in this rank's peer slot, before the exchange
+  else
+    __threadfence();
   __syncthreads();
   if (tid == 0) s_last = atomicAdd(p.ws.tick + seg::kG, 1u) == gridDim.x - 1;
   __syncthreads();

@@ -380,7 +380,7 @@ int stencil_variant() {
 // the grid (deterministic).  Saves the write of y and the re-read of y, x
 // and b by kls_resid_norms, and one launch per GMRES column.
 template <int W>
-__global__ void __launch_bounds__(kThreads, W >= 7 ? 2 : 3) ell_resid_norms_kernel(
+__global__ void __launch_bounds__(kThreads, W >= 7 ? 3 : 4) ell_resid_norms_kernel(
     const int32_t* __restrict__ ecol, const double* __restrict__ eval,
     const uint8_t* __restrict__ elen, int64_t ld, const double* __restrict__ x,
     const double* __restrict__ b, int width, const __grid_constant__ seg::SimpleArgs a) {
@@ -426,7 +426,8 @@ template <int W>
 int launch_ell_resid(const int32_t* ecol, const double* eval, const uint8_t* elen, int32_t width,
                      int64_t ld, const double* x, const double* b, const seg::SimpleArgs& a,
                      cudaStream_t st) {
-  const int grid = std::max(1, std::min(a.P.nitems, (W >= 7 ? 2 : 3) * sm_count()));
+  // one item per CTA up to 4 CTAs per SM (at m = 1e6 all 504 items resident)
+  const int grid = std::max(1, std::min(a.P.nitems, 4 * sm_count()));
   return launch_dependent(ell_resid_norms_kernel<W>, dim3(grid), dim3(kThreads), 0, st,
                           "ell_resid_norms_kernel", ecol, eval, elen, ld, x, b, width, a);
 }
@@ -563,7 +564,7 @@ KLS_API int kls_ell_resid_norms(const int32_t* ecol, const double* eval, const u
       out == nullptr || ws == nullptr || nrows < 0 || ld < nrows || width < 1 || width > 8)
     return fail(KLS_EINVAL, "ell_resid_norms: bad arguments");
   seg::SimpleArgs a;
-  int rc = seg::make_plan_simple(segs, nrows, 1024, a, ws, ws_bytes, 3, out);
+  int rc = seg::make_plan_simple(segs, nrows, 2048, a, ws, ws_bytes, 3, out);
   if (rc) return rc;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   switch (width) {
