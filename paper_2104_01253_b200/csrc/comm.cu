@@ -28,6 +28,7 @@
 
 #include <cstring>
 #include "stencil.cuh"
+#include "stencil_tma.cuh"
 
 namespace {
 
@@ -211,6 +212,16 @@ KLS_API int kls_stencil7_peer(const double* x, const double* x_lo, const double*
   const uint64_t* flag_hi = flags + (rank + 1 < kMaxPeers ? rank + 1 : rank);
   const int64_t xchunk = std::min<int64_t>(32, nx);
   dim3 grid;
+  if (stencil7_tma_ok(x, ny, nz) && stencil7_grid(nx, ny, nz, xchunk, grid, kTZ, kTY)) {
+    CUtensorMap map;
+    const int use_map = stencil7_tensor_map(x, nx, ny, nz, &map) ? 1 : 0;
+    TmaStencilArgs a{use_map, x, x_lo, x_hi, y, nx, static_cast<int32_t>(ny),
+                     static_cast<int32_t>(nz), static_cast<int32_t>(xchunk),
+                     x_lo != nullptr ? flag_lo : nullptr, x_hi != nullptr ? flag_hi : nullptr,
+                     epoch, err};
+    return launch_dependent(stencil7_tma_kernel, grid, dim3(kTThreads), 0,
+                            static_cast<cudaStream_t>(stream), "stencil7_tma_kernel", a, map);
+  }
   if (ny > INT32_MAX || nz > INT32_MAX || !stencil7_grid(nx, ny, nz, xchunk, grid, kSTZ, kSTY))
     return fail(KLS_EINVAL, "stencil7_peer: grid too large");
   stencil7_peer_kernel<<<grid, dim3(32, kSTY), 0, static_cast<cudaStream_t>(stream)>>>(

@@ -15,6 +15,7 @@
 #include "reduce.cuh"
 #include "seg.cuh"
 #include "stencil.cuh"
+#include "stencil_tma.cuh"
 #include "peer.cuh"
 
 #include <cstdlib>
@@ -362,13 +363,15 @@ __global__ void __launch_bounds__(32 * kSTY) stencil7_smem_kernel(
   pdl_trigger();
 }
 
-// stencil variant: 1 = shared-memory tiles (default), 0 = register march
-// (KLS_STENCIL=reg)
+
+// stencil variant: 2 = TMA-staged tiles (default), 1 = shared-memory tiles
+// with register prefetch (KLS_STENCIL=smem), 0 = register march
+// (KLS_STENCIL=reg); all bit-identical
 int stencil_variant() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("KLS_STENCIL");
-    v = (e && e[0] == 'r') ? 0 : 1;
+    v = (e && e[0] == 'r') ? 0 : (e && e[0] == 's') ? 1 : 2;
   }
   return v;
 }
@@ -483,7 +486,19 @@ KLS_API int kls_stencil7(const double* x, const double* x_lo, const double* x_hi
     env_chunk = e ? atoi(e) : 0;
   }
   dim3 grid;
-  if (stencil_variant() == 1) {
+  if (stencil_variant() == 2 && stencil7_tma_ok(x, ny, nz)) {
+    const int64_t xc = std::min<int64_t>(env_chunk > 0 ? env_chunk : 32, nx);
+    if (!stencil7_grid(nx, ny, nz, xc, grid, kTZ, kTY))
+      return fail(KLS_EINVAL, "stencil7: grid too large");
+    CUtensorMap map;
+    const int use_map = stencil7_tensor_map(x, nx, ny, nz, &map) ? 1 : 0;
+    TmaStencilArgs a{use_map, x, x_lo, x_hi, y, nx, static_cast<int32_t>(ny),
+                     static_cast<int32_t>(nz), static_cast<int32_t>(xc), nullptr, nullptr, 0,
+                     nullptr};
+    return launch_dependent(stencil7_tma_kernel, grid, dim3(kTThreads), 0,
+                            static_cast<cudaStream_t>(stream), "stencil7_tma_kernel", a, map);
+  }
+  if (stencil_variant() >= 1) {
     const int64_t xc = std::min<int64_t>(env_chunk > 0 ? env_chunk : 32, nx);
     if (!stencil7_grid(nx, ny, nz, xc, grid, kSTZ, kSTY))
       return fail(KLS_EINVAL, "stencil7: grid too large");

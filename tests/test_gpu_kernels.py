@@ -364,6 +364,13 @@ def test_ell_resid_norms_fused(cuda, rng, k, beta):
     xh, bh = x.cpu().numpy(), b.cpu().numpy()
     want = [np.sum((bh - y) ** 2), xh @ xh, bh @ bh]
     assert np.allclose(out.cpu().numpy(), want, rtol=1e-12, atol=0)
+    # the same rows per thread and the same segment tree as kls_resid_norms:
+    # bitwise the unfused product + norms (they used to differ)
+    yd = torch.from_numpy(y).cuda()
+    out2 = torch.zeros(3, dtype=torch.float64, device="cuda")
+    lib.call("kls_resid_norms", b.data_ptr(), yd.data_ptr(), x.data_ptr(), op.n, out2.data_ptr(),
+             None, ws, wsb, rt.stream_handle())
+    assert torch.equal(out, out2)
 
 
 @pytest.mark.parametrize("tag", ["small", "edge", "mid"])
