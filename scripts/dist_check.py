@@ -43,7 +43,7 @@ def main():
         op = kls.laplace3d(*dims)
         led = kls.SyncLedger()
         V, H = kls.arnoldi_expand(op, start, scheme, steps=30, ledger=led)
-        loo = kls.loss_of_orthogonality(V)
+        loo = kls.loss_of_orthogonality(V, segs=op.segs)
         if rank == 0:
             _, Hr, cnt = getattr(oracle, f"{scheme}_arnoldi")(
                 lambda x: oracle.stencil7_matvec(x, dims), start, 30)
@@ -59,7 +59,7 @@ def main():
         op = kls.laplace3d(62, 64, 64)
         led = kls.SyncLedger()
         V, H = kls.arnoldi_expand(op, start3, scheme, steps=100, ledger=led)
-        loo = kls.loss_of_orthogonality(V)
+        loo = kls.loss_of_orthogonality(V, segs=op.segs)
         ref = g[f"{scheme}_H"]
         err = float(np.max(np.abs(H - ref)) / np.max(np.abs(ref)))
         if rank == 0:
@@ -140,7 +140,7 @@ def main():
     for scheme in ("dcgs2", "cgs2"):
         led = kls.SyncLedger()
         Qd, R = kls.qr_factorize(A, scheme, ledger=led)
-        loo = kls.loss_of_orthogonality(Qd)
+        loo = kls.loss_of_orthogonality(Qd, segs=comm.segs(A.shape[0]))
         if rank == 0:
             _, Rr, cnt = getattr(oracle, f"{scheme}_qr")(A)
             err = float(np.max(np.abs(R - Rr)) / np.max(np.abs(Rr)))

@@ -61,7 +61,7 @@ def main():
         if world > 1:
             sec = comm.allreduce_max_float(sec)
             comm.barrier()
-        loo = kls.loss_of_orthogonality(Q)
+        loo = kls.loss_of_orthogonality(Q, segs=comm.segs(m))
         bytes_per_gpu = sum(8 * (m / world) * (2 * j + 6) for j in range(n))
         if rank == 0:
             print(json.dumps({"config": 5, "gpus": world, "m_per_gpu": ml, "m": m, "n": n,
