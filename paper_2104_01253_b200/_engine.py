@@ -332,6 +332,57 @@ class Engine:
                 _lib.call(*args)
         return self._finish(k)
 
+    def _reduce_into(self, count, launch, dst):
+        """Queue a reducing kernel whose `count` global results go to the
+        device tensor `dst` (world 1: written directly; otherwise exported
+        tree nodes, then the cross-rank combine) -- nothing waits."""
+        if self.world == 1:
+            launch(dst.data_ptr())
+            return
+        launch(self._out(count))
+        self._combine_into(count, dst.data_ptr(), dst)
+
+    def cgs2_chain(self, j, v):
+        """Cgs2State.push's three reductions for column v against Q(:, 0:j),
+        chained on the device with ONE host wait: s = Q^T v and v.v
+        (kls_mv_trans_mv), v <- v - Q s and c = Q^T v with s read from the
+        device (kls_project_gram), v <- v - Q c and ||v||^2 (the fused-norm
+        update, c from the device).  Each reduction is still a separate
+        global reduction (3 per step, the comparator's cost model); only the
+        host round trips between them are gone.  Returns host (s, ||v0||^2,
+        c, ||v||^2)."""
+        n1 = j + 1
+        g = self.gdev
+        rec = trace._active
+        gp = g.data_ptr()
+
+        def span(name, nbytes, fn):
+            if rec is None:
+                fn()
+            else:
+                rec.note(name, nbytes)
+                with rec.span(name):
+                    fn()
+
+        span("project", 8 * self.ml * (j + 1), lambda: self._reduce_into(n1, lambda o: _lib.call(
+            "kls_mv_trans_mv", self.qptr, self.ld, self.ml, j, None, v.data_ptr(), None, 1, 1, o,
+            self.segp, self.ws, self.wsb, self.st), g[:n1]))
+        span("project_gram", 8 * self.ml * (j + 2), lambda: self._reduce_into(j, lambda o: _lib.call(
+            "kls_project_gram", self.qptr, self.ld, self.ml, j, v.data_ptr(), gp, 0, 0, o,
+            self.segp, self.ws, self.wsb, self.st), g[n1 : n1 + j]))
+        span("mtm", 8 * self.ml * (j + 2), lambda: self._reduce_into(1, lambda o: _lib.call(
+            "kls_mv_times_mat_add_mv", v.data_ptr(), self.ld, self.ml, 1, self.qptr, self.ld, j,
+            gp + 8 * n1, -1.0, 1.0, o, self.segp, self.ws, self.wsb, self.st), g[n1 + j : n1 + j + 1]))
+        cnt = 2 * j + 2
+        h = self.stage.host_out[:cnt]
+        h.copy_(g[:cnt], non_blocking=True)
+        _lib.call("kls_stream_sync", self.st)
+        if self.peer is not None:
+            self.peer.check()
+        runtime.XFER["d2h"] += 8 * cnt
+        r = h.numpy().copy()
+        return r[:j], float(r[j]), r[n1 : n1 + j], float(r[n1 + j])
+
     def add_combination(self, y, x, k, coef):
         """y = x + Q(:, 0:k) coef (host coefficients ride in the launch)."""
         if y.data_ptr() != x.data_ptr():

@@ -564,6 +564,8 @@ class _ImmediateArnoldi(_BaseArnoldi):
         super().__init__(op, capacity, ledger, engine)
         e = self.eng
         self._v = torch.zeros(e.ld, dtype=torch.float64, device=e.vbuf.device)[: e.ml]
+        # KLS_CGS2_CHAIN=0: one host round trip per reduction (round 1's path)
+        self._chain = os.environ.get("KLS_CGS2_CHAIN", "1") != "0"
         self.last_coeffs = None
         self.last_alpha = None
         if start is not None:
@@ -590,18 +592,31 @@ class _ImmediateArnoldi(_BaseArnoldi):
         Q(:, 0:j); returns (coeffs, alpha) and leaves u = v - Q(s+c) in v."""
         e = self.eng
         m = self.m
-        r = e.project(j, v, xnorm=True)  # s = Q^T a and the local scale ||a||^2
-        s, scale2 = r[:j].copy(), float(r[j])
-        if not np.isfinite(scale2):
-            raise ValueError("non-finite column")
-        scale = float(np.sqrt(scale2))
-        self._rec(_ledger.MV_TRANS_MV, 2 * m * j)
-        c = e.subtract_and_project(v, j, s)  # one pass over Q for both
-        self._rec(_ledger.MV_TIMES_MAT_ADD_MV, 2 * m * j)
-        self._rec(_ledger.MV_TRANS_MV, 2 * m * j)
-        nrm2 = e.subtract_projection(v, j, c, want_norm=True)
-        self._rec(_ledger.MV_TIMES_MAT_ADD_MV, 2 * m * j)
-        self._rec(_ledger.MV_DOT, 2 * m)
+        if self._chain and j > 0:
+            # the three reductions queued back to back on the device, one
+            # host wait (Engine.cgs2_chain); the checks below then run in
+            # the reference's order on the same scalars
+            s, scale2, c, nrm2 = e.cgs2_chain(j, v)
+            if not np.isfinite(scale2):
+                raise ValueError("non-finite column")
+            scale = float(np.sqrt(scale2))
+            for kind in (_ledger.MV_TRANS_MV, _ledger.MV_TIMES_MAT_ADD_MV, _ledger.MV_TRANS_MV,
+                         _ledger.MV_TIMES_MAT_ADD_MV):
+                self._rec(kind, 2 * m * j)
+            self._rec(_ledger.MV_DOT, 2 * m)
+        else:
+            r = e.project(j, v, xnorm=True)  # s = Q^T a and the local scale ||a||^2
+            s, scale2 = r[:j].copy(), float(r[j])
+            if not np.isfinite(scale2):
+                raise ValueError("non-finite column")
+            scale = float(np.sqrt(scale2))
+            self._rec(_ledger.MV_TRANS_MV, 2 * m * j)
+            c = e.subtract_and_project(v, j, s)  # one pass over Q for both
+            self._rec(_ledger.MV_TIMES_MAT_ADD_MV, 2 * m * j)
+            self._rec(_ledger.MV_TRANS_MV, 2 * m * j)
+            nrm2 = e.subtract_projection(v, j, c, want_norm=True)
+            self._rec(_ledger.MV_TIMES_MAT_ADD_MV, 2 * m * j)
+            self._rec(_ledger.MV_DOT, 2 * m)
         alpha = float(np.sqrt(nrm2))
         self.last_coeffs, self.last_alpha = s + c, alpha
         if not alpha > _EPS * np.sqrt(m) * scale:
