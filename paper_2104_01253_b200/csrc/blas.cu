@@ -321,9 +321,10 @@ size_t rotate_smem(int k, int zp, int nbuf) {
 // they were.
 KLS_API int kls_tsgemm_inplace_cols(double* V, int64_t ldv, int64_t m, int32_t k, int32_t p,
                                     const double* Z, void* stream) {
+  if (m == 0 && k >= 0 && p >= 0 && p <= k) return KLS_OK;  // a rank without rows
   if (V == nullptr || Z == nullptr || m < 0 || k < 0 || p < 0 || p > k || ldv < m)
     return fail(KLS_EINVAL, "tsgemm_inplace_cols: bad arguments");
-  if (m == 0 || k == 0 || p == 0) return KLS_OK;
+  if (k == 0 || p == 0) return KLS_OK;
   static const bool use_mma = [] {  // KLS_ROTATE=fma: the DFMA kernel (experiments)
     const char* e = getenv("KLS_ROTATE");
     return !(e != nullptr && e[0] == 'f');

@@ -32,7 +32,7 @@ class _RowSpace:
 
     def __init__(self, m, comm=None):
         self.comm = comm if comm is not None else runtime.comm()
-        self.segs = self.comm.segs(m, 64)
+        self.segs = self.comm.segs(m, runtime.row_unit(m))
         self.row_lo, self.row_hi = self.segs.lo, self.segs.hi
         self.shape = (m, m)
 

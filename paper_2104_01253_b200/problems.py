@@ -85,7 +85,7 @@ class LinearOperator:
     def _partition(self):
         # rows follow the 24 global reduction segments (64-row units):
         # rank-count-independent reductions, DESIGN.md §6a
-        self.segs = self.comm.segs(self.n, 64)
+        self.segs = self.comm.segs(self.n, runtime.row_unit(self.n))
         self.row_lo, self.row_hi = self.segs.lo, self.segs.hi
 
     @property

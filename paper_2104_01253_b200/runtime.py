@@ -121,9 +121,17 @@ class Comm:
         dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
         return float(t.item())
 
-    def segs(self, m, unit=64):
-        """The reduction layout of an m-row object split over this comm."""
-        return Segs(m, unit, self.world, self.rank)
+    def segs(self, m, unit=None):
+        """The reduction layout of an m-row object split over this comm
+        (unit: row_unit(m) by default, a stencil passes its x-plane)."""
+        return Segs(m, row_unit(m) if unit is None else unit, self.world, self.rank)
+
+
+def row_unit(m):
+    """Partition unit of an m-row object: 64 rows, or fewer for small m so
+    that every one of the 24 segments gets rows (no rank without rows for
+    N <= 24); even, and a function of m only (rank-count independent)."""
+    return max(2, min(64, 2 * (m // 48)))
 
     def combine_(self, blocks, count):
         """NCCL path of a reduction's cross-rank combine: `blocks` (device,

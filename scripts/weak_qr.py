@@ -33,7 +33,7 @@ def main():
     import paper_2104_01253_b200 as kls
 
     m = a.m_per_gpu * world
-    lo, hi = runtime.seg_range(m, 64, world, rank)  # this rank's rows (24-segment layout)
+    lo, hi = runtime.seg_range(m, runtime.row_unit(m), world, rank)  # this rank's rows (24-segment layout)
     ml = hi - lo
     for n in (int(v) for v in a.n.split(",")):
         g = torch.Generator(device="cuda")
