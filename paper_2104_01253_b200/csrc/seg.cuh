@@ -364,6 +364,29 @@ __device__ __forceinline__ bool peer_exchange(const Dest& d, int tid, int* s_ok)
 // rank's peer slot (layout [e][nv]); emit(o, value).
 template <int NT, typename Emit>
 __device__ __forceinline__ void combine_from_slots(const Dest& d, int nv, int tid, Emit emit) {
+  const int W = d.peers.world;
+  if (W == 2 || W == 4 || W == 8) {
+    // each rank exports exactly its subtree root (a node of the binary part
+    // of the tree): all W remote loads in flight at once, then the balanced
+    // tree over them in rank order -- the same folds as combine_tree
+    for (int o = tid; o < nv; o += NT) {
+      double v[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+        if (r < W) v[r] = *(reinterpret_cast<const volatile double*>(
+                              peer::slot(d.peers.buf[r], d.peers.cap, d.epoch)) + o);
+      if (W == 8) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) v[r] = v[2 * r] + v[2 * r + 1];
+      }
+      if (W >= 4) {
+        v[0] = v[0] + v[1];
+        v[1] = v[2] + v[3];
+      }
+      emit(o, v[0] + v[1]);
+    }
+    return;
+  }
   for (int o = tid; o < nv; o += NT) {
     double val[kNodes];
     bool have[kNodes];
