@@ -38,7 +38,6 @@ constexpr int kRoot = 38;
 constexpr int kMaxExport = 8;   // nodes one rank exports (<= 4 for N <= 8)
 constexpr int kTickBytes = 256; // segment tickets [kG] + done ticket
 constexpr int kMaxVirt = 148;   // largest virtual grid of any segmented kernel
-constexpr int64_t kOneLevel = 16384;  // item partials one CTA sums at the end (finish_items)
 
 // ---- the static tree ------------------------------------------------------
 __host__ __device__ constexpr int node_lo(int n) {
@@ -226,30 +225,6 @@ __device__ __forceinline__ bool finish_items(const Plan& P, Ws ws, int nv, int t
   __shared__ int s_seg[kG], s_cnt[kG], s_done[kG], s_nt;
   __threadfence();
   gsync<NT, BAR>();
-  if (static_cast<int64_t>(P.nitems) * nv <= kOneLevel) {
-    // few partials (medium m): one ticket over all items, and the CTA that
-    // takes the last one sums every segment itself (the same fixed-order
-    // sums as below, one atomic round trip instead of two)
-    if (tid == 0) {
-      unsigned mine = 0;
-      for (int it = blockIdx.x; it < P.nitems; it += gridDim.x) ++mine;
-      const bool last = atomicAdd(ws.tick + kG, mine) + mine == static_cast<unsigned>(P.nitems);
-      if (last) ws.tick[kG] = 0u;
-      *s_flag = last ? 1 : 0;
-    }
-    gsync<NT, BAR>();
-    if (*s_flag == 0) return false;
-    __threadfence();
-    for (int s = 0; s < P.L.nseg; ++s) {
-      double* sv = ws.segv + static_cast<int64_t>(s) * nv;
-      group_sum_partials<NT, BAR>(ws.part + static_cast<int64_t>(P.ibase[s]) * nv,
-                                  P.ibase[s + 1] - P.ibase[s], nv, tid, s_red,
-                                  [&](int i, double t) { sv[i] = t; });
-    }
-    __threadfence();
-    gsync<NT, BAR>();
-    return true;
-  }
   if (tid == 0) {  // the segments this CTA's items belong to, with item counts
     int n = 0;
     for (int it = blockIdx.x; it < P.nitems; it += gridDim.x) {
