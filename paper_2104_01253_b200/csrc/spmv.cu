@@ -274,7 +274,15 @@ __global__ void __launch_bounds__(kThreads, ell_blocks<W>()) ell_spmv_pipe_kerne
     const int32_t* __restrict__ ecol, const double* __restrict__ eval,
     const uint8_t* __restrict__ elen, int64_t nrows, int64_t ld, XA x,
     double* __restrict__ y, PeerWait pw, int width) {
-  pdl_wait();  // x from the preceding update
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  // the first row's entries (the operator's own arrays, never written by
+  // the preceding kernels) are fetched before waiting for x: the loads
+  // overlap the predecessor's tail under PDL
+  EllRow<W> cur;
+  cur.n = 0;
+  if (i < nrows) ell_fetch<W>(cur, ecol, eval, elen, ld, i, width);
+  pdl_wait();  // x from the preceding update (and y free to overwrite)
   if (pw.flag_lo != nullptr || pw.flag_hi != nullptr) {
     __shared__ int s_ok;
     if (threadIdx.x == 0) {
@@ -287,11 +295,7 @@ __global__ void __launch_bounds__(kThreads, ell_blocks<W>()) ell_spmv_pipe_kerne
     __syncthreads();
     if (!s_ok) return;
   }
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= nrows) return;
-  EllRow<W> cur;
-  ell_fetch<W>(cur, ecol, eval, elen, ld, i, width);
   while (true) {
     const int64_t nx = i + stride;
     EllRow<W> nxt;
