@@ -35,7 +35,7 @@ METRIC = "DCGS2 Arnoldi iters/sec + HBM GB/s (fp64) at 1/2/4/8 B200 vs CPU ref"
 UNIT = "iters/s"
 FULL_DIMS = (496, 512, 512)
 SAMPLE_DIMS = (124, 128, 128)  # 1/64 of the rows: the cpu_baseline leg's sample
-REF_SAMPLE_DIMS = (62, 64, 128)  # 1/256 of the rows: each --impl reference step
+REF_SAMPLE_DIMS = (62, 128, 128)  # 1/128 of the rows: each --impl reference step (~8 s)
 NOMINAL_HBM_GBS = 8000.0
 FALLBACK_HBM_GBS = 6650.0
 
