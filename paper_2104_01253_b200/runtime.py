@@ -127,12 +127,6 @@ class Comm:
         return Segs(m, row_unit(m) if unit is None else unit, self.world, self.rank)
 
 
-def row_unit(m):
-    """Partition unit of an m-row object: 64 rows, or fewer for small m so
-    that every one of the 24 segments gets rows (no rank without rows for
-    N <= 24); even, and a function of m only (rank-count independent)."""
-    return max(2, min(64, 2 * (m // 48)))
-
     def combine_(self, blocks, count):
         """NCCL path of a reduction's cross-rank combine: `blocks` (device,
         >= 8 * count) holds this rank's exported tree nodes ([e][count]);
@@ -178,6 +172,13 @@ def row_unit(m):
         t = torch.from_numpy(arr.copy()).to(device())
         self.allreduce_(t)
         return t.cpu().numpy()
+
+
+def row_unit(m):
+    """Partition unit of an m-row object: 64 rows, or fewer for small m so
+    that every one of the 24 segments gets rows (no rank without rows for
+    N <= 24); even, and a function of m only (rank-count independent)."""
+    return max(2, min(64, 2 * (m // 48)))
 
 
 def block_range(n, parts, index):
@@ -343,11 +344,12 @@ class Workspace:
         self._old = []
         self._need = {}
 
-    def get(self, kmax):
+    def get(self, kmax, m=0):
         kmax = int(max(kmax, 8))
-        need = self._need.get(kmax)
+        key = (kmax, int(m))
+        need = self._need.get(key)
         if need is None:
-            need = self._need[kmax] = int(_lib.load().kls_workspace_bytes(0, kmax))
+            need = self._need[key] = int(_lib.load().kls_workspace_bytes(int(m), kmax))
         if self._buf is None or need > self._bytes:
             if self._buf is not None:
                 self._old.append(self._buf)
@@ -363,14 +365,15 @@ def workspace(kmax):
     return workspace_for(stream_handle(), kmax)
 
 
-def workspace_for(stream, kmax):
-    """(pointer, bytes) of the reduction workspace of `stream`.  Replaced
-    buffers stay alive, so a returned pointer remains valid."""
+def workspace_for(stream, kmax, m=0):
+    """(pointer, bytes) of the reduction workspace of `stream` for reductions
+    over m local rows with up to kmax basis columns.  Replaced buffers stay
+    alive, so a returned pointer remains valid."""
     key = (torch.cuda.current_device(), stream)
     ws = _workspaces.get(key)
     if ws is None:
         ws = _workspaces[key] = Workspace()
-    return ws.get(kmax)
+    return ws.get(kmax, m)
 
 
 class Staging:

@@ -246,3 +246,35 @@ def test_library_segment_layout_matches_host():
                 ids = (ctypes.c_int32 * 8)()
                 n = lib.kls_seg_exports(r, world, ids)
                 assert list(ids[:n]) == seg_exports(r, world)
+
+
+def _comm_worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2104_01253_b200.runtime import Comm
+
+        c = Comm()
+        t = torch.full((3,), float(rank + 1), dtype=torch.float64)
+        c.allreduce_(t)
+        out[rank] = (c.rank, c.world, t.tolist(), c.allreduce_calls,
+                     c.allreduce_max_int(rank), c.segs(1000).world)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_comm_collectives_gloo():
+    """runtime.Comm's own methods on gloo ranks (the NCCL fallback paths of
+    the reductions call allreduce_ / combine_ / allreduce_host)."""
+    from paper_2104_01253_b200.runtime import Comm
+
+    for name in ("allreduce_", "combine_", "allreduce_host", "allreduce_max_int", "segs", "barrier"):
+        assert callable(getattr(Comm, name, None)), name
+    world = 3
+    out = mp.Manager().dict()
+    mp.spawn(_comm_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    for r in range(world):
+        rank, w, t, calls, mx, sw = out[r]
+        assert (rank, w, calls, mx, sw) == (r, world, 1, world - 1, world)
+        assert t == [6.0, 6.0, 6.0]
