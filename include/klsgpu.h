@@ -252,8 +252,6 @@ typedef struct {
   const void* p0; /* ELL: ecol; CSR: rowptr; dense: a */
   const void* p1; /* ELL: eval; CSR: col */
   const void* p2; /* ELL: elen; CSR: val */
-  int64_t reach;  /* ELL: 1 + max |col - row| over the stored entries (the
-                     rows a product reaches on each side); 0 = unknown */
 } KlsOpDesc;
 typedef struct {
   double* Q;
@@ -294,27 +292,6 @@ typedef struct {
  * kls_dcgs2_host_step; stops at a breakdown.  See plan.cu for io. */
 int kls_dcgs2_run(const KlsRunState* s, int32_t j0, int32_t nsteps, int32_t cur, int32_t slot,
                   double* io);
-/* One DCGS2 lookahead step as ONE persistent launch (fused.cu): the update
- * of step j, the banded ELL product A w_out -> aw_out and the Gram pass of
- * step j + 1 with its fixed-tree reduction and device scalar step, chunk by
- * chunk with per-chunk halo flags; bitwise equal to the three launches of
- * kls_dcgs2_queue_step, which calls it when eligible (one rank, an ELL
- * operator with known reach <= 32768 rows, 65536 < m <= 2^25, j + 1 <= 256).
- * Replaces arnoldi.py:389-391 + 415-420, problems.py:127-136 and
- * arnoldi.py:362-370 + 414 of one step.  KLS_FUSED=0 disables it. */
-int kls_dcgs2_fused_step(const KlsStepPlan* plan, int32_t j, const double* w, double* w_out,
-                         const double* aw, double* aw_out, int32_t slot);
-/* Experiments: the same with per-chunk %globaltimer stamps (ns) in trace
- * (device int64[5 * chunks]: start, update done, halo ready, product done,
- * Gram pass done). */
-int kls_dcgs2_fused_step_traced(const KlsStepPlan* plan, int32_t j, const double* w,
-                                double* w_out, const double* aw, double* aw_out, int32_t slot,
-                                int64_t* trace);
-/* 1 when kls_dcgs2_fused_step applies to step j of the plan, else 0. */
-int kls_dcgs2_fused_eligible(const KlsStepPlan* plan, int32_t j);
-/* Non-zero (and cleared) when a fused step on this stream timed out waiting
- * for a neighbouring chunk; synchronizes the stream. */
-int kls_dcgs2_fused_error(void* stream);
 int kls_event_create(void** ev);
 int kls_event_destroy(void* ev);
 int kls_event_record(void* ev, void* stream);

@@ -75,7 +75,7 @@ class Engine:
             _lib.call("kls_event_create", ctypes.byref(ev))
             self.slot_ev.append(ev.value)
         self._plan = None  # kls_dcgs2_queue_step plan (one GPU), False when n/a
-        self.ws, self.wsb = runtime.workspace_for(self.st, capacity + 1, self.ml)
+        self.ws, self.wsb = runtime.workspace_for(self.st, capacity + 1)
         # the rows' reduction layout (rank-count-independent segment tree)
         self.segs = op.segs
         self.segp = op.segs.ptr
@@ -480,22 +480,10 @@ class Engine:
 
     def queue_step(self, plan, j, w, w_out, aw, aw_out, slot, gram):
         """Step j of the lookahead through the plan: w -> w_out (and column j),
-        A w_out -> aw_out, then (gram) Gram_{j+1} into `slot` -- one fused
-        launch when kls_dcgs2_fused_step applies, else three."""
+        A w_out -> aw_out, then (gram) Gram_{j+1} into `slot`."""
         _lib.call("kls_dcgs2_queue_step", ctypes.byref(plan), j, w.data_ptr(), w_out.local.data_ptr(),
                   w_out.ext_ptr, aw.data_ptr(), aw_out.data_ptr(), slot, 1 if gram else 0)
-        if not (gram and self.fused(plan, j)):
-            _lib.count_launches(2 if gram else 1)
-
-    def fused(self, plan, j):
-        """Whether step j of the plan runs as one fused launch (launch counts)."""
-        f = getattr(self, "_fused", None)
-        if f is None:
-            f = self._fused = {}
-        v = f.get(j)
-        if v is None:
-            v = f[j] = bool(_lib.load().kls_dcgs2_fused_eligible(ctypes.byref(plan), j))
-        return v
+        _lib.count_launches(2 if gram else 1)
 
     def check_capacity(self, n):
         if n > self.capacity:

@@ -42,10 +42,6 @@ SIGNATURES = {
     "kls_dcgs2_host_step": (ctypes.c_int, [c_dp, i32, i64, f64, c_dp, c_dp, i64, c_dp, c_dp, c_dp,
                                            c_dp, c_dp]),
     "kls_dcgs2_queue_step": (ctypes.c_int, [c_dp, i32, c_dp, c_dp, c_dp, c_dp, c_dp, i32, i32]),
-    "kls_dcgs2_fused_step": (ctypes.c_int, [c_dp, i32, c_dp, c_dp, c_dp, c_dp, i32]),
-    "kls_dcgs2_fused_step_traced": (ctypes.c_int, [c_dp, i32, c_dp, c_dp, c_dp, c_dp, i32, c_dp]),
-    "kls_dcgs2_fused_eligible": (ctypes.c_int, [c_dp, i32]),
-    "kls_dcgs2_fused_error": (ctypes.c_int, [c_dp]),
     "kls_event_create": (ctypes.c_int, [ctypes.POINTER(ctypes.c_void_p)]),
     "kls_event_destroy": (ctypes.c_int, [c_dp]),
     "kls_event_record": (ctypes.c_int, [c_dp, c_dp]),
@@ -113,8 +109,7 @@ _NO_LAUNCH = frozenset({"kls_version", "kls_last_error", "kls_device_sm_count", 
                         "kls_seg_rows", "kls_seg_exports",
                         "kls_event_destroy", "kls_event_record", "kls_event_sync",
                         "kls_hessenberg_reduce", "kls_schur_sweeps", "kls_schur_swap",
-                        "kls_schur_move_front", "kls_schur_eigenvectors",
-                        "kls_dcgs2_fused_eligible", "kls_dcgs2_fused_error"})
+                        "kls_schur_move_front", "kls_schur_eigenvectors"})
 
 
 class KlsSegs(ctypes.Structure):
@@ -127,7 +122,7 @@ class KlsOpDesc(ctypes.Structure):
     """include/klsgpu.h KlsOpDesc: an operator's apply as plain pointers."""
 
     _fields_ = [("kind", i32), ("width", i32), ("m", i64), ("n0", i64), ("n1", i64), ("n2", i64),
-                ("p0", c_dp), ("p1", c_dp), ("p2", c_dp), ("reach", i64)]
+                ("p0", c_dp), ("p1", c_dp), ("p2", c_dp)]
 
 
 class KlsHostBlas(ctypes.Structure):

@@ -468,9 +468,7 @@ class _DelayedArnoldi(_BaseArnoldi):
         _lib.call("kls_dcgs2_run", ctypes.byref(st), j0, nsteps, 0, self._slot, io.ctypes.data)
         done, status, jstop = int(io[2]), int(io[3]), int(io[4])
         queued = done + (1 if status else 0)
-        # update, operator, Gram (+ scalar step): one fused launch, or three
-        nf = sum(1 for jj in range(j0, j0 + queued) if jj + 2 < cap and e.fused(plan, jj))
-        _lib.count_launches(3 * queued - 2 * nf)
+        _lib.count_launches(3 * queued)  # update, operator, Gram (+ scalar step)
         # the host read each step's 2j+3 scalars from mapped pinned memory
         jq = np.arange(j0, j0 + queued, dtype=np.int64)
         runtime.XFER["d2h"] += int(8 * np.sum(2 * jq + 3))

@@ -15,7 +15,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 PKG = os.path.dirname(HERE)
 LIB = os.path.join(PKG, "libklsgpu.so")
-SOURCES = ["runtime.cu", "gram.cu", "gram_tma.cu", "update.cu", "spmv.cu", "blas.cu", "comm.cu", "build_ops.cu", "step.cu", "cgs2.cu", "host_step.cu", "plan.cu", "schur_host.cu", "seg.cu", "stencil_map.cu", "fused.cu"]
+SOURCES = ["runtime.cu", "gram.cu", "gram_tma.cu", "update.cu", "spmv.cu", "blas.cu", "comm.cu", "build_ops.cu", "step.cu", "cgs2.cu", "host_step.cu", "plan.cu", "schur_host.cu", "seg.cu", "stencil_map.cu"]
 HEADERS = ["step.cuh", "common.cuh", "reduce.cuh", "stencil.cuh", "gram.cuh", "tma.cuh", "peer.cuh", "seg.cuh", "stencil_tma.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 INCLUDE = os.path.join(os.path.dirname(PKG), "include")

@@ -184,12 +184,7 @@ int launch_gram(GramParams p, int64_t m_global, size_t ws_bytes, cudaStream_t st
     const char* e = getenv("KLS_TMA_VIRT");
     return e != nullptr && atoi(e) > 0 ? atoi(e) : kTmaVirt;
   }();
-  // the Arnoldi step's reduction (scalar step fused, Arnoldi form) at the
-  // fused step's sizes sums over the chunk tree the fused step uses
-  if (chunk_tree(m_global) && p.coef != nullptr && !p.qr)
-    chunk_plan(p.P.L, p.P);
-  else
-    seg::make_plan(p.P.L, 8192, vmax, p.P);
+  seg::make_plan(p.P.L, 8192, vmax, p.P);
   const int nv = gram_nv(p, NX);
   if (seg::plan_ws_bytes(p.P, nv) > ws_bytes)
     return fail(KLS_ENOSPC, "gram: workspace %zu bytes < %zu needed", ws_bytes,
@@ -199,14 +194,6 @@ int launch_gram(GramParams p, int64_t m_global, size_t ws_bytes, cudaStream_t st
 }
 
 }  // namespace
-
-bool kls::gram::chunk_tree_enabled() {
-  static const bool on = [] {
-    const char* e = getenv("KLS_CHUNK_TREE");
-    return !(e != nullptr && e[0] == '0');
-  }();
-  return on;
-}
 
 // Generic fused reduction: out = [Q(:, 0:k), bext]^T [x0 (, x1)]  (+ x_last^2).
 // Output is column-major with (k + (bext != NULL)) rows and nx columns, then
@@ -365,12 +352,9 @@ KLS_API int kls_gram_dcgs2_peer_step(const double* Q, int64_t ldq, int64_t m, in
 // segment values, for the widest reduction (a Gram panel, or CGS2's
 // k + 1 outputs).
 KLS_API size_t kls_workspace_bytes(int64_t m, int32_t kmax) {
+  (void)m;
   const int64_t panel = std::min<int64_t>(kmax, kPanel);
   const int64_t nv = std::max<int64_t>(2 * panel + 2 * 2 + 1, (int64_t)kmax + 1) + 8;
-  // chunk-item plans (chunk_tree): up to one item per 1024 local rows plus
-  // one short chunk per segment (m <= 0: rows unknown, the largest such plan)
-  if (m <= 0) m = kChunkTreeMax;
-  const int64_t chunks = m <= kChunkTreeMax ? ceil_div(m, kChunkRows) + seg::kG : 0;
-  const int64_t items = std::max<int64_t>((int64_t)seg::kG * seg::kMaxVirt, chunks);
+  const int64_t items = (int64_t)seg::kG * seg::kMaxVirt;
   return seg::kTickBytes + sizeof(double) * static_cast<size_t>((items + seg::kG) * nv);
 }

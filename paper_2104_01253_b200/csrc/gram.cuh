@@ -63,13 +63,7 @@ struct GramRows {
   int32_t xnorm;
 };
 
-// RW: read through the coherent path (operands this kernel wrote itself).
-template <bool CHECK, bool RW>
-__device__ __forceinline__ double2 gram_load(const double* col, int64_t r, int64_t m) {
-  return RW ? load_pair_rw<CHECK>(col, r, m) : load_pair<CHECK>(col, r, m);
-}
-
-template <int NX, int RP, bool CHECK, bool RW = false>
+template <int NX, int RP, bool CHECK>
 __device__ __forceinline__ void gram_chunk(const GramRows& p, int64_t wbase, int lane,
                                            double* wacc, double (&ex)[NX], double& xn) {
   constexpr int V = kG * NX;
@@ -78,14 +72,14 @@ __device__ __forceinline__ void gram_chunk(const GramRows& p, int64_t wbase, int
 #pragma unroll
   for (int t = 0; t < NX; ++t)
 #pragma unroll
-    for (int r = 0; r < RP; ++r) xv[t][r] = gram_load<CHECK, RW>(xs[t], wbase + 64 * r + 2 * lane, p.m);
+    for (int r = 0; r < RP; ++r) xv[t][r] = load_pair<CHECK>(xs[t], wbase + 64 * r + 2 * lane, p.m);
 
   if (p.bext != nullptr) {
 #pragma unroll
     for (int r = 0; r < RP; ++r) {
       // the DCGS2 call passes bext == x0 (the pending w): reuse the registers
       const double2 b = p.bext == p.x0 ? xv[0][r]
-                                        : gram_load<CHECK, RW>(p.bext, wbase + 64 * r + 2 * lane, p.m);
+                                        : load_pair<CHECK>(p.bext, wbase + 64 * r + 2 * lane, p.m);
 #pragma unroll
       for (int t = 0; t < NX; ++t) {
         ex[t] = fma(b.x, xv[t][r].x, ex[t]);
@@ -110,7 +104,7 @@ __device__ __forceinline__ void gram_chunk(const GramRows& p, int64_t wbase, int
       if (c < p.k) {
         const double* col = p.Q + static_cast<int64_t>(c) * p.ldq;
 #pragma unroll
-        for (int r = 0; r < RP; ++r) q[cc][r] = gram_load<CHECK, RW>(col, wbase + 64 * r + 2 * lane, p.m);
+        for (int r = 0; r < RP; ++r) q[cc][r] = load_pair<CHECK>(col, wbase + 64 * r + 2 * lane, p.m);
       } else {
 #pragma unroll
         for (int r = 0; r < RP; ++r) q[cc][r] = make_double2(0.0, 0.0);
@@ -140,24 +134,6 @@ bool tma_eligible(const GramParams& p);
 // rows (so a medium-m launch is one item per CTA), at most this many (49:
 // the 3 segments of an 8-rank share keep 147 of 148 SMs busy)
 constexpr int kTmaVirt = 49;
-
-// Global row counts whose DCGS2 Arnoldi-step reductions (Gram + scalar
-// step, Arnoldi form) use one item per 1024-row chunk (a segment's value is
-// the fixed-order sum of its chunk partials) instead of kTmaVirt-bounded
-// items: the tree of the fused DCGS2 step (fused.cu), which takes a chunk
-// through update, operator and Gram pass in one go.  Every other reduction
-// keeps the item tree.  Above kUpdSmallRows (the update's per-row order is the streaming
-// kernels' there) and up to 2^25 rows (chunk partials stay a few tens of MB).
-constexpr int64_t kChunkTreeMin = int64_t(1) << 16;
-constexpr int64_t kChunkTreeMax = int64_t(1) << 25;
-bool chunk_tree_enabled();  // KLS_CHUNK_TREE=0 turns it off (experiments)
-inline bool chunk_tree(int64_t m_global) {
-  return m_global > kChunkTreeMin && m_global <= kChunkTreeMax && chunk_tree_enabled();
-}
-constexpr int kChunkRows = 1024;
-inline void chunk_plan(const seg::Layout& L, seg::Plan& P) {
-  seg::make_plan(L, kChunkRows, 1 << 30, P);
-}
 
 }  // namespace gram
 }  // namespace kls

@@ -11,14 +11,6 @@
 
 using namespace kls;
 
-namespace kls {
-bool dcgs2_fused_ok(const KlsStepPlan* p, int32_t j);  // fused.cu
-}
-
-KLS_API int kls_dcgs2_fused_eligible(const KlsStepPlan* p, int32_t j) {
-  return dcgs2_fused_ok(p, j) ? 1 : 0;
-}
-
 static int apply_op(const KlsOpDesc* op, const double* x, double* y, void* stream) {
   switch (op->kind) {
     case KLS_OP_ELL:
@@ -64,11 +56,6 @@ KLS_API int kls_dcgs2_queue_step(const KlsStepPlan* p, int32_t j, const double* 
                                  const double* x_out, const double* aw, double* aw_out,
                                  int32_t slot, int32_t gram) {
   if (p == nullptr || slot < 0 || slot > 1) return fail(KLS_EINVAL, "queue_step: bad plan or slot");
-  if (gram && x_out == w_out && dcgs2_fused_ok(p, j)) {  // the three launches as one
-    int rc = kls_dcgs2_fused_step(p, j, w, w_out, aw, aw_out, slot);
-    if (rc) return rc;
-    return kls_event_record(p->event[slot], p->stream);
-  }
   int rc = kls_dcgs2_update_dev(p->Q, p->ldq, p->m, j, w, w_out, aw, p->cdev, p->divide,
                                 &p->segs, p->stream);
   if (rc) return rc;

@@ -247,9 +247,6 @@ __global__ void __launch_bounds__(kUThreads, 1)
 
   if (warp == kWarps) {
     if (lane == 0) {
-      // w, aw and Q(:, j-1) may be the preceding kernel's output (the fused
-      // step, fused.cu, writes all three): stream only after it completes
-      pdl_wait();
       uint32_t use = 0, xuse = 0;
       int64_t row, nr;
       for (ChunkWalk<kUR> cw(m64); cw.next(row, nr); ++xuse) {
@@ -273,7 +270,8 @@ __global__ void __launch_bounds__(kUThreads, 1)
     }
     return;
   }
-  // consumers: the coefficients come from the preceding kernel (PDL)
+  // consumers: the coefficients come from the preceding Gram kernel (PDL);
+  // the producer above streams Q, w and aw meanwhile (none of which it writes)
   pdl_wait();
   for (int k = threadIdx.x; k < jpad; k += kWarps * 32)
     sct[k] = k < p.j ? make_double2(coef[k], coef[p.j + k]) : make_double2(0.0, 0.0);

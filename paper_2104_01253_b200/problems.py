@@ -643,26 +643,9 @@ class CsrOperator(LinearOperator):
         if self._ell is not None:
             ecol, evals, elen, width, ld = self._ell
             return _lib.KlsOpDesc(kind=_lib.OP_ELL, width=width, m=self.m_local, n0=ld,
-                                  p0=ecol.data_ptr(), p1=evals.data_ptr(), p2=elen.data_ptr(),
-                                  reach=self._reach())
+                                  p0=ecol.data_ptr(), p1=evals.data_ptr(), p2=elen.data_ptr())
         return _lib.KlsOpDesc(kind=_lib.OP_CSR, m=self.m_local, p0=self._rowptr_p,
                               p1=self._col_p, p2=self._val_p)
-
-    def _reach(self):
-        """1 + max |col - row| over the stored ELL entries (one rank): how far
-        a row's product reaches, which bounds the fused step's halo waits."""
-        if getattr(self, "_reach_v", None) is None:
-            ecol, _, elen, width, ld = self._ell
-            m = self.m_local
-            rows = torch.arange(m, device=ecol.device, dtype=torch.int64)
-            n = elen[:m].to(torch.int64)
-            far = 0
-            for k in range(width):
-                d = (ecol[k * ld: k * ld + m].to(torch.int64) - rows).abs()
-                d = torch.where(n > k, d, torch.zeros_like(d))
-                far = max(far, int(d.max().item()) if m else 0)
-            self._reach_v = far + 1
-        return self._reach_v
 
     def to_dense(self, max_order=4000):
         if self.n > max_order:
