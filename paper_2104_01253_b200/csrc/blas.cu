@@ -190,10 +190,15 @@ __global__ void __launch_bounds__(kThreads, 2)
 // 2-3 stage shared-memory ring with cp.async.bulk (mbarrier completion);
 // each of the 8 consumer warps owns 16 rows of the tile and forms its
 // 16 x 32 output block per pass as 2 x 4 mma tiles, A fragments from the
-// tile (leading dimension 136: conflict-free), B fragments from Z (shared,
-// zero-padded to a multiple of 4 rows), accumulating in k order.
+// tile, B fragments from Z (shared, zero-padded to a multiple of 4 rows),
+// accumulating in k order.  A lane (k-quad q = lane & 3, row r = lane >> 2)
+// reads tile[(kk + q) * ld + r] and Z[(kk + q) * zp + r + 8 b]: with ld = 132
+// and zp = 36 (mod 32 doubles: 4 and 4) the four k-quads land 8 banks
+// apart, so the 64-bit fragment loads are conflict-free (ld = 136 / zp = 40
+// gave 2-way conflicts: 115 M replays at config 4's shape, ncu -- removing
+// them did not change the time: the kernel is bound elsewhere).
 constexpr int kMmaRows = 128;
-constexpr int kMmaLd = 136;
+constexpr int kMmaLd = 132;
 constexpr int kMmaThreads = 288;
 
 __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
@@ -331,7 +336,7 @@ KLS_API int kls_tsgemm_inplace_cols(double* V, int64_t ldv, int64_t m, int32_t k
   }();
   {
     const int kp = (k + 3) / 4 * 4;
-    const int zpm = (p + 31) / 32 * 32 + 8;  // B fragments conflict-free
+    const int zpm = (p + 31) / 32 * 32 + 4;  // B fragments conflict-free
     int stages = 3;
     while (stages > 1 && rotate_mma_smem(kp, zpm, stages) > 227 * 1024) --stages;
     // measured at m = 1e7 (scripts/rotate_probe.py): DMMA 1.57 vs DFMA 2.24 ms

@@ -12,7 +12,10 @@ from paper_2104_01253_b200 import _lib, runtime
 
 m = 10_004_569
 ld = runtime.pad_rows(m)
-for k, p in ((60, 30), (60, 60), (30, 15)):
+cases = ((60, 30), (60, 60), (30, 15))
+if os.environ.get("ROT_CASES"):  # e.g. ROT_CASES=60x30 (ncu captures)
+    cases = tuple(tuple(int(v) for v in c.split("x")) for c in os.environ["ROT_CASES"].split(","))
+for k, p in cases:
     V = torch.randn((k, ld), dtype=torch.float64, device="cuda")
     Z = torch.randn(k * p, dtype=torch.float64, device="cuda") / k
     st = runtime.stream_handle()
