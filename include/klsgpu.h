@@ -179,6 +179,14 @@ int kls_ell_resid_norms(const int32_t* ecol, const double* eval, const uint8_t* 
                         const double* b, double* out, const KlsSegs* segs, void* ws,
                         size_t ws_bytes, void* stream);
 
+/* y2 = A x2 (bit-identical to kls_ell_spmv) and the norms of
+ * kls_ell_resid_norms for (x, b) (bit-identical) in one pass over the
+ * entries of a one-rank ELL operator. */
+int kls_ell_apply_resid_norms(const int32_t* ecol, const double* eval, const uint8_t* elen,
+                              int32_t width, int64_t nrows, int64_t ld, const double* x2,
+                              double* y2, const double* x, const double* b, double* out,
+                              const KlsSegs* segs, void* ws, size_t ws_bytes, void* stream);
+
 /* Matrix-free 7-point Laplacian, bit-identical to StencilLaplace3D._matvec
  * (problems.py:296-305) on nx local x-planes of a (.., ny, nz) grid; x_lo /
  * x_hi are the neighbouring planes of other ranks (NULL at the boundary). */
@@ -292,6 +300,23 @@ typedef struct {
  * kls_dcgs2_host_step; stops at a breakdown.  See plan.cu for io. */
 int kls_dcgs2_run(const KlsRunState* s, int32_t j0, int32_t nsteps, int32_t cur, int32_t slot,
                   double* io);
+/* GMRES's per-column backward error (gmres.py:166-172) of an earlier column
+ * riding on a lookahead step: xj = x + Q(:, 0:q) y (y: q HOST doubles, read
+ * during the call) and out = [||b - A xj||^2, ||xj||^2, ||b||^2] (device). */
+typedef struct {
+  const double* x;
+  double* xj;
+  int32_t q;
+  const double* y;
+  const double* b;
+  double* out;
+} KlsBeCol;
+/* kls_dcgs2_queue_step (gram != 0 required for the Gram part as there) with
+ * the backward-error column fused into the update and the ELL product: the
+ * same bits as the separate launches, without their passes over Q and A. */
+int kls_dcgs2_queue_step_be(const KlsStepPlan* plan, int32_t j, const double* w, double* w_out,
+                            const double* x_out, const double* aw, double* aw_out, int32_t slot,
+                            int32_t gram, const KlsBeCol* be);
 int kls_event_create(void** ev);
 int kls_event_destroy(void* ev);
 int kls_event_record(void* ev, void* stream);

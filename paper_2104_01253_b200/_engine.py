@@ -485,6 +485,27 @@ class Engine:
                   w_out.ext_ptr, aw.data_ptr(), aw_out.data_ptr(), slot, 1 if gram else 0)
         _lib.count_launches(2 if gram else 1)
 
+    def queue_step_be(self, plan, j, w, w_out, aw, aw_out, slot, gram, job):
+        """queue_step with a GMRES backward-error column riding on it
+        (kls_dcgs2_queue_step_be): job = (x, xj, axj, y, b, out) computes
+        xj = x + Q(:, 0:len(y)) y and out = [||b - A xj||^2, ||xj||^2,
+        ||b||^2] inside the step's update and ELL product."""
+        x, xj, _, y, b, out = job
+        yc = np.ascontiguousarray(y, dtype=np.float64)
+        be = _lib.KlsBeCol(x=x.data_ptr(), xj=xj.data_ptr(), q=len(yc), y=yc.ctypes.data,
+                           b=b.data_ptr(), out=out.data_ptr())
+        trace.note("mtm", 16 * self.ml)
+        _lib.call("kls_dcgs2_queue_step_be", ctypes.byref(plan), j, w.data_ptr(),
+                  w_out.local.data_ptr(), w_out.ext_ptr, aw.data_ptr(), aw_out.data_ptr(), slot,
+                  1 if gram else 0, ctypes.byref(be))
+        _lib.count_launches(2 if gram else 1)
+
+    def be_fusable(self):
+        """Whether a GMRES backward-error column can ride on a lookahead step
+        (one rank, the step plan, an ELL operator)."""
+        plan = self.step_plan()
+        return plan is not None and plan.op.kind == _lib.OP_ELL
+
     def check_capacity(self, n):
         if n > self.capacity:
             raise DimensionError("expansion capacity exhausted")

@@ -42,6 +42,10 @@ SIGNATURES = {
     "kls_dcgs2_host_step": (ctypes.c_int, [c_dp, i32, i64, f64, c_dp, c_dp, i64, c_dp, c_dp, c_dp,
                                            c_dp, c_dp]),
     "kls_dcgs2_queue_step": (ctypes.c_int, [c_dp, i32, c_dp, c_dp, c_dp, c_dp, c_dp, i32, i32]),
+    "kls_dcgs2_queue_step_be": (ctypes.c_int, [c_dp, i32, c_dp, c_dp, c_dp, c_dp, c_dp, i32, i32,
+                                               c_dp]),
+    "kls_ell_apply_resid_norms": (ctypes.c_int, [c_dp, c_dp, c_dp, i32, i64, i64, c_dp, c_dp, c_dp,
+                                                 c_dp, c_dp, c_dp, c_dp, sz, c_dp]),
     "kls_event_create": (ctypes.c_int, [ctypes.POINTER(ctypes.c_void_p)]),
     "kls_event_destroy": (ctypes.c_int, [c_dp]),
     "kls_event_record": (ctypes.c_int, [c_dp, c_dp]),
@@ -138,6 +142,12 @@ class KlsStepPlan(ctypes.Structure):
     _fields_ = [("Q", c_dp), ("ldq", i64), ("m", i64), ("segs", KlsSegs), ("gdev", c_dp), ("cdev", c_dp),
                 ("gout", c_dp * 2), ("ws", c_dp), ("ws_bytes", sz), ("stream", c_dp),
                 ("event", c_dp * 2), ("divide", i32), ("qr", i32), ("op", KlsOpDesc)]
+
+
+class KlsBeCol(ctypes.Structure):
+    """include/klsgpu.h KlsBeCol (kls_dcgs2_queue_step_be)."""
+
+    _fields_ = [("x", c_dp), ("xj", c_dp), ("q", i32), ("y", c_dp), ("b", c_dp), ("out", c_dp)]
 
 
 class KlsRunState(ctypes.Structure):

@@ -185,6 +185,18 @@ class _BaseArnoldi:
         self.hcols = 0
         self.happy = False
         self.start_norm = None
+        # a GMRES backward-error column to run inside the next lookahead step
+        # (gmres.py sets it; _DelayedArnoldi._step_ahead runs it fused or,
+        # without the step plan, separately -- either way exactly once)
+        self._be_job = None
+
+    def _run_be_job(self, job):
+        """A GMRES backward-error column (x, x_j, scratch, y, b, out) through
+        the separate launches: x_j = x + V y, then its norms."""
+        if job is not None:
+            x, xj, axj, y, b, out = job
+            self.eng.add_combination(xj, x, len(y), y)
+            self.eng.apply_resid_norms(xj, axj, b, out)
 
     # -- views (device tensors for the basis, numpy for H) -------------------------
     @property
@@ -379,9 +391,14 @@ class _DelayedArnoldi(_BaseArnoldi):
         nxt = 1 - slot if j + 2 < self.capacity else None
         self.op.napply += 1
         plan = e.step_plan()
-        if plan is not None:  # one host call for the three launches
+        job, self._be_job = self._be_job, None
+        if plan is not None and job is not None and plan.op.kind == _lib.OP_ELL:
+            e.queue_step_be(plan, j, w.local, w2, aw, aw2, nxt or 0, nxt is not None, job)
+        elif plan is not None:  # one host call for the three launches
+            self._run_be_job(job)
             e.queue_step(plan, j, w.local, w2, aw, aw2, nxt or 0, nxt is not None)
         else:
+            self._run_be_job(job)
             e.update_ahead(j, w.local, w2.local, aw, divide=True)
             e.apply(w2, aw2)
             if nxt is not None:

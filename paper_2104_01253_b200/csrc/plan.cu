@@ -70,6 +70,46 @@ KLS_API int kls_dcgs2_queue_step(const KlsStepPlan* p, int32_t j, const double* 
   return rc;
 }
 
+namespace kls {
+int dcgs2_update_dev_comb(double* Q, int64_t ldq, int64_t m, int32_t j, const double* w,
+                          double* w_out, const double* aw, const double* coef_alpha,
+                          const KlsSegs* segs, void* stream, const double* x, double* xout,
+                          int32_t q, const double* y);  // update.cu
+}
+
+// kls_dcgs2_queue_step with GMRES's backward-error column of an earlier
+// step riding on it (gmres.py:166-172): the update also forms
+// be->xj = be->x + Q(:, 0:q) y from the Q tiles it streams, and on an ELL
+// operator the product of w_out and the norms [||b - A xj||^2, ||xj||^2,
+// ||b||^2] -> be->out are one pass over the entries.  Every value is
+// bit-identical to the separate launches (add_combination, the apply,
+// kls_ell_resid_norms); the column's two extra passes over Q and A go away.
+KLS_API int kls_dcgs2_queue_step_be(const KlsStepPlan* p, int32_t j, const double* w,
+                                    double* w_out, const double* x_out, const double* aw,
+                                    double* aw_out, int32_t slot, int32_t gram,
+                                    const KlsBeCol* be) {
+  if (p == nullptr || be == nullptr || slot < 0 || slot > 1)
+    return fail(KLS_EINVAL, "queue_step_be: bad arguments");
+  if (p->op.kind != KLS_OP_ELL)
+    return fail(KLS_EINVAL, "queue_step_be: needs an ELL operator");
+  int rc = dcgs2_update_dev_comb(p->Q, p->ldq, p->m, j, w, w_out, aw, p->cdev, &p->segs,
+                                 p->stream, be->x, be->xj, be->q, be->y);
+  if (rc) return rc;
+  rc = kls_ell_apply_resid_norms(static_cast<const int32_t*>(p->op.p0),
+                                 static_cast<const double*>(p->op.p1),
+                                 static_cast<const uint8_t*>(p->op.p2), p->op.width, p->op.m,
+                                 p->op.n0, x_out, aw_out, be->xj, be->b, be->out, &p->segs, p->ws,
+                                 p->ws_bytes, p->stream);
+  if (rc) return rc;
+  if (gram) {
+    rc = kls_gram_dcgs2_step(p->Q, p->ldq, p->m, j + 1, w_out, aw_out, p->gdev, p->cdev,
+                             p->gout[slot], p->qr, &p->segs, p->ws, p->ws_bytes, p->stream);
+    if (rc) return rc;
+    rc = kls_event_record(p->event[slot], p->stream);
+  }
+  return rc;
+}
+
 // The lookahead loop itself (arnoldi.py:349-423 per step, _step_ahead's
 // order): per step one queue_step, one wait on the step's scalars, the C++
 // host step; stops after nsteps, at a breakdown, or when the next Gram would

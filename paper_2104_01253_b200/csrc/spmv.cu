@@ -386,11 +386,15 @@ int stencil_variant() {
 // kernel accumulates ||b - y||^2, ||x||^2 and ||b||^2 and reduces them over
 // the grid (deterministic).  Saves the write of y and the re-read of y, x
 // and b by kls_resid_norms, and one launch per GMRES column.
-template <int W>
+// DUAL: the same pass also forms and stores y2 = A x2 (the step's operator
+// product, bit-identical to kls_ell_spmv) from the entries already in
+// registers -- the GMRES backward-error column riding on the step's apply.
+template <int W, bool DUAL = false>
 __global__ void __launch_bounds__(kThreads, W >= 7 ? 3 : 4) ell_resid_norms_kernel(
     const int32_t* __restrict__ ecol, const double* __restrict__ eval,
     const uint8_t* __restrict__ elen, int64_t ld, const double* __restrict__ x,
-    const double* __restrict__ b, int width, const __grid_constant__ seg::SimpleArgs a) {
+    const double* __restrict__ b, int width, const __grid_constant__ seg::SimpleArgs a,
+    const double* __restrict__ x2, double* __restrict__ y2) {
   pdl_wait();
   seg::run_simple<kThreads, 3>(a, [&](int64_t r0, int64_t rows, int vi, int V, double (&v)[3]) {
     const int64_t stride = static_cast<int64_t>(V) * kThreads;
@@ -415,6 +419,20 @@ __global__ void __launch_bounds__(kThreads, W >= 7 ? 3 : 4) ell_resid_norms_kern
           if (k < cur.n) r = __dadd_rn(r, p[k]);
         acc = __dadd_rn(p[0], r);
       }
+      if constexpr (DUAL) {
+        double p2[W];
+#pragma unroll
+        for (int k = 0; k < W; ++k) p2[k] = k < cur.n ? __dmul_rn(cur.v[k], __ldg(x2 + cur.c[k])) : 0.0;
+        double acc2 = 0.0;
+        if (cur.n > 0) {
+          double r2 = -0.0;
+#pragma unroll
+          for (int k = 1; k < W; ++k)
+            if (k < cur.n) r2 = __dadd_rn(r2, p2[k]);
+          acc2 = __dadd_rn(p2[0], r2);
+        }
+        y2[i] = acc2;
+      }
       const double bi = __ldcs(b + i);
       const double xi = __ldg(x + i);
       const double rr = bi - acc;
@@ -432,11 +450,15 @@ __global__ void __launch_bounds__(kThreads, W >= 7 ? 3 : 4) ell_resid_norms_kern
 template <int W>
 int launch_ell_resid(const int32_t* ecol, const double* eval, const uint8_t* elen, int32_t width,
                      int64_t ld, const double* x, const double* b, const seg::SimpleArgs& a,
-                     cudaStream_t st) {
+                     cudaStream_t st, const double* x2 = nullptr, double* y2 = nullptr) {
   // one item per CTA up to 4 CTAs per SM (at m = 1e6 all 504 items resident)
   const int grid = std::max(1, std::min(a.P.nitems, 4 * sm_count()));
+  if (x2 != nullptr)
+    return launch_dependent(ell_resid_norms_kernel<W, true>, dim3(grid), dim3(kThreads), 0, st,
+                            "ell_resid_norms_kernel", ecol, eval, elen, ld, x, b, width, a, x2, y2);
   return launch_dependent(ell_resid_norms_kernel<W>, dim3(grid), dim3(kThreads), 0, st,
-                          "ell_resid_norms_kernel", ecol, eval, elen, ld, x, b, width, a);
+                          "ell_resid_norms_kernel", ecol, eval, elen, ld, x, b, width, a,
+                          static_cast<const double*>(nullptr), static_cast<double*>(nullptr));
 }
 
 // dense y = A x, A row-major n x n (DenseOperator, problems.py:68-85):
@@ -592,6 +614,31 @@ KLS_API int kls_ell_resid_norms(const int32_t* ecol, const double* eval, const u
     case 7: return launch_ell_resid<7>(ecol, eval, elen, width, ld, x, b, a, st);
     case 8: return launch_ell_resid<8>(ecol, eval, elen, width, ld, x, b, a, st);
     default: return launch_ell_resid<4>(ecol, eval, elen, width, ld, x, b, a, st);
+  }
+}
+
+// The step's ELL product y2 = A x2 (bit-identical to kls_ell_spmv) and the
+// backward-error norms of kls_ell_resid_norms for x (bit-identical too) in
+// ONE pass over the operator's entries (GMRES, plan.cu).
+KLS_API int kls_ell_apply_resid_norms(const int32_t* ecol, const double* eval,
+                                      const uint8_t* elen, int32_t width, int64_t nrows,
+                                      int64_t ld, const double* x2, double* y2, const double* x,
+                                      const double* b, double* out, const KlsSegs* segs, void* ws,
+                                      size_t ws_bytes, void* stream) {
+  if ((nrows > 0 && (ecol == nullptr || eval == nullptr || elen == nullptr || x == nullptr ||
+                     b == nullptr || x2 == nullptr || y2 == nullptr)) ||
+      out == nullptr || ws == nullptr || nrows < 0 || ld < nrows || width < 1 || width > 8)
+    return fail(KLS_EINVAL, "ell_apply_resid_norms: bad arguments");
+  seg::SimpleArgs a;
+  int rc = seg::make_plan_simple(segs, nrows, 2048, a, ws, ws_bytes, 3, out);
+  if (rc) return rc;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  switch (width) {
+    case 5: return launch_ell_resid<5>(ecol, eval, elen, width, ld, x, b, a, st, x2, y2);
+    case 6: return launch_ell_resid<6>(ecol, eval, elen, width, ld, x, b, a, st, x2, y2);
+    case 7: return launch_ell_resid<7>(ecol, eval, elen, width, ld, x, b, a, st, x2, y2);
+    case 8: return launch_ell_resid<8>(ecol, eval, elen, width, ld, x, b, a, st, x2, y2);
+    default: return launch_ell_resid<4>(ecol, eval, elen, width, ld, x, b, a, st, x2, y2);
   }
 }
 

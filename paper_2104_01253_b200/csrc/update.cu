@@ -17,6 +17,7 @@
 
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 
 namespace {
 
@@ -213,9 +214,25 @@ constexpr int kUR = 1024;            // rows per chunk
 constexpr int kUStages = 4;
 constexpr int kUThreads = (kWarps + 1) * 32;
 
-template <int NC>
+// Optional second job of the streaming update (GMRES's per-column backward
+// error, gmres.py:166-172): xout = x + Q(:, 0:q) y for an earlier column's
+// least-squares y, formed from the same Q tiles (q <= j) with
+// mtm_chunk's per-row operation sequence (column groups of 4, one fma per
+// column, q and y read as 0 past column q within the last group), so xout
+// is bit-identical to kls_mv_times_mat_add_mv(x + Q y).
+constexpr int kCombMax = 64;
+struct CombPack {
+  const double* x;
+  double* xout;
+  int32_t q;
+  double y[kCombMax];
+};
+struct CombNone {};
+
+template <int NC, bool COMB = false>
 __global__ void __launch_bounds__(kUThreads, 1)
-    dcgs2_update_tma_kernel(UpdParams p, const __grid_constant__ CoefPack<NC> pk) {
+    dcgs2_update_tma_kernel(UpdParams p, const __grid_constant__ CoefPack<NC> pk,
+                            const __grid_constant__ typename std::conditional<COMB, CombPack, CombNone>::type cb) {
   using namespace kls::tma;
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
@@ -284,11 +301,12 @@ __global__ void __launch_bounds__(kUThreads, 1)
   uint32_t use = 0, xuse = 0;
   int64_t crow, nr;  // nr: a multiple of 64; rows past it are computed but not stored
   for (ChunkWalk<kUR> cw(m64); cw.next(crow, nr); ++xuse) {
-    double2 ac[RP], at[RP];
+    double2 ac[RP], at[RP], xc[RP];
 #pragma unroll
     for (int r = 0; r < RP; ++r) {
       ac[r] = make_double2(0.0, 0.0);
       at[r] = make_double2(0.0, 0.0);
+      xc[r] = make_double2(0.0, 0.0);
     }
     for (int g = 0; g < ng; ++g, ++use) {
       const int s = use % kUStages;
@@ -319,6 +337,20 @@ __global__ void __launch_bounds__(kUThreads, 1)
           at[r].y = fma(q[cc][r].y, ct.y, at[r].y);
         }
       }
+      if constexpr (COMB) {
+        if (g * kCols < cb.q) {  // mtm_chunk's groups over the first q columns
+#pragma unroll
+          for (int cc = 0; cc < kCols; ++cc) {
+            const bool in = g * kCols + cc < cb.q;
+            const double yv = in ? cb.y[g * kCols + cc] : 0.0;
+#pragma unroll
+            for (int r = 0; r < RP; ++r) {
+              xc[r].x = fma(in ? q[cc][r].x : 0.0, yv, xc[r].x);
+              xc[r].y = fma(in ? q[cc][r].y : 0.0, yv, xc[r].y);
+            }
+          }
+        }
+      }
     }
     const int xs = xuse & 1;
     mbar_wait(xfull + xs, (xuse >> 1) & 1);
@@ -344,10 +376,29 @@ __global__ void __launch_bounds__(kUThreads, 1)
       wn.y = ay - fma(qn.y, tj, at[r].y);
       *reinterpret_cast<double2*>(qout + row) = qn;
       *reinterpret_cast<double2*>(p.w_out + row) = wn;
+      if constexpr (COMB) {
+        const double2 xv = ld_stream2(cb.x + row);
+        *reinterpret_cast<double2*>(cb.xout + row) = make_double2(xv.x + xc[r].x, xv.y + xc[r].y);
+      }
     }
   }
-  if (m64 < p.m && blockIdx.x == gridDim.x - 1)
+  if (m64 < p.m && blockIdx.x == gridDim.x - 1) {
     upd_chunk<RP, true>(p, sct, tj, alpha, m64 + wrow, lane);
+    if constexpr (COMB) {  // the < 64 tail rows of xout, one per lane (warp 0)
+      if (warp == 0)
+        for (int64_t i = m64 + lane; i < p.m; i += 32) {
+          double a = 0.0;
+          for (int k0 = 0; k0 < cb.q; k0 += kCols)
+#pragma unroll
+            for (int cc = 0; cc < kCols; ++cc) {
+              const bool in = k0 + cc < cb.q;
+              a = fma(in ? __ldg(p.Q + static_cast<int64_t>(k0 + cc) * p.ldq + i) : 0.0,
+                      in ? cb.y[k0 + cc] : 0.0, a);
+            }
+          cb.xout[i] = __ldg(cb.x + i) + a;
+        }
+    }
+  }
   pdl_trigger();
 }
 
@@ -517,6 +568,7 @@ bool update_tma() {
 
 template <int NC>
 int launch_update(const UpdParams& p, const double* host_coef, cudaStream_t st) {
+  static_assert(NC >= 0, "");
   CoefPack<NC> pk;
   if (NC > 0) std::memcpy(pk.v, host_coef, sizeof(double) * (2 * p.j + 1));
   // the small kernel sums a row's terms in another order than the streaming
@@ -535,11 +587,11 @@ int launch_update(const UpdParams& p, const double* host_coef, cudaStream_t st) 
                        sizeof(double) * (static_cast<size_t>(kUStages) * kCols * kUR + 4 * kUR);
   if (update_tma() && p.j > 0 && p.m >= kUR && tsmem <= 227 * 1024 && !misaligned(p.Q) &&
       !misaligned(p.w) && !misaligned(p.aw) && (p.ldq % 2) == 0) {
-    int rc = set_smem(reinterpret_cast<const void*>(dcgs2_update_tma_kernel<NC>), tsmem);
+    int rc = set_smem(reinterpret_cast<const void*>(dcgs2_update_tma_kernel<NC, false>), tsmem);
     if (rc) return rc;
     const int grid = static_cast<int>(std::min<int64_t>((p.m + kUR - 1) / kUR, sm_count()));
     return launch_dependent(dcgs2_update_tma_kernel<NC>, dim3(grid), dim3(kUThreads), tsmem, st,
-                            "dcgs2_update_tma_kernel", p, pk);
+                            "dcgs2_update_tma_kernel", p, pk, CombNone{});
   }
   const size_t smem = sizeof(double2) * static_cast<size_t>((p.j + kCols - 1) / kCols * kCols + 1);
   int rc = set_smem(reinterpret_cast<const void*>(dcgs2_update_kernel<kUpdRP, NC>), smem);
@@ -697,3 +749,58 @@ KLS_API int kls_mv_times_mat_add_mv_host(double* Y, int64_t ldy, int64_t m, int3
   return mtm_common(Y, ldy, m, l, B, ldb, k, S_host, sign, scale, nrm_out, segs, ws, ws_bytes,
                     true, stream);
 }
+
+namespace kls {
+
+// The step update with GMRES's backward-error combination riding on it
+// (plan.cu, kls_dcgs2_queue_step_be): w -> w_out and q_j as
+// kls_dcgs2_update_dev, plus xout = x + Q(:, 0:q) y (y: q host doubles)
+// from the same Q tiles.  Falls back to the update followed by the separate
+// combination (copy + kls_mv_times_mat_add_mv_host, the same bits) where the
+// streaming kernel does not apply.
+int dcgs2_update_dev_comb(double* Q, int64_t ldq, int64_t m, int32_t j, const double* w,
+                          double* w_out, const double* aw, const double* coef_alpha,
+                          const KlsSegs* segs, void* stream, const double* x, double* xout,
+                          int32_t q, const double* y) {
+  if (x == nullptr || xout == nullptr || y == nullptr || q < 0 || q > j)
+    return fail(KLS_EINVAL, "dcgs2_update_comb: bad combination arguments");
+  const int64_t m_global = segs != nullptr ? segs->m : m;
+  const int jp = (j + kCols - 1) / kCols * kCols;
+  const size_t tsmem = 256 + sizeof(double2) * (jp + 1) +
+                       sizeof(double) * (static_cast<size_t>(kUStages) * kCols * kUR + 4 * kUR);
+  const bool fused = update_tma() && j > 0 && q <= kCombMax && m >= kUR &&
+                     m_global > kUpdSmallRows && tsmem <= 227 * 1024 && !misaligned(Q) &&
+                     !misaligned(w) && !misaligned(aw) && !misaligned(w_out) && !misaligned(x) &&
+                     !misaligned(xout) && (ldq % 2) == 0 && ldq >= m && coef_alpha != nullptr;
+  if (!fused) {
+    int rc = kls_dcgs2_update_dev(Q, ldq, m, j, w, w_out, aw, coef_alpha, 1, segs, stream);
+    if (rc) return rc;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (xout != x) {
+      const cudaError_t e = cudaMemcpyAsync(xout, x, sizeof(double) * m, cudaMemcpyDeviceToDevice, st);
+      if (e != cudaSuccess) return fail(KLS_ECUDA, "dcgs2_update_comb: copy: %s", cudaGetErrorString(e));
+    }
+    if (q == 0) return KLS_OK;
+    return kls_mv_times_mat_add_mv_host(xout, ldq, m, 1, Q, ldq, q, y, 1.0, 1.0, nullptr, segs,
+                                        nullptr, 0, stream);
+  }
+  seg::Layout L;
+  int rc = seg::make_layout(segs, m, L);
+  if (rc) return rc;
+  UpdParams p{Q, ldq, m, j, const_cast<double*>(w), aw, coef_alpha, 0.0, 1, coef_alpha + 2 * j + 1,
+              w_out, m_global};
+  CoefPack<0> pk;
+  CombPack cb;
+  cb.x = x;
+  cb.xout = xout;
+  cb.q = q;
+  for (int i = 0; i < kCombMax; ++i) cb.y[i] = i < q ? y[i] : 0.0;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  rc = set_smem(reinterpret_cast<const void*>(dcgs2_update_tma_kernel<0, true>), tsmem);
+  if (rc) return rc;
+  const int grid = static_cast<int>(std::min<int64_t>((m + kUR - 1) / kUR, sm_count()));
+  return launch_dependent(dcgs2_update_tma_kernel<0, true>, dim3(grid), dim3(kUThreads), tsmem, st,
+                          "dcgs2_update_tma_kernel", p, pk, cb);
+}
+
+}  // namespace kls

@@ -108,3 +108,62 @@ def test_gmres_config2_full_size_iteration_parity(cuda):
     assert dev[: 42 * 50].max() <= 1e-12
     assert np.array_equal(res.reduction_history, g["reduction_history"])
     assert led.reductions == int(g["reductions"])
+
+
+@pytest.mark.parametrize("k,restart", [(300, 20), (301, 7)])
+def test_fused_backward_errors_bitwise(cuda, monkeypatch, k, restart):
+    """Each drained column's x_j = x + V y and its norms ride on the next
+    step's update and ELL product (kls_dcgs2_queue_step_be): the backward
+    errors, residual history, ledger and apply count are BITWISE those of the
+    separate launches (KLS_FUSE_BE=0), on an even and an odd row count."""
+    K = kls()
+    op = K.manteuffel_operator(K.ManteuffelSpec(k=k, beta=0.5))
+    assert op._ell is not None and op.n > 65536
+    one = op.apply(np.ones(op.n)).cpu().numpy()
+    b = one / np.linalg.norm(one)
+    cfg = K.GmresConfig(max_iters=3 * restart + 3, restart=restart, rtol=1e-12, scheme="dcgs2",
+                        backward_errors=True)
+    out = {}
+    for fuse in ("1", "0"):
+        monkeypatch.setenv("KLS_FUSE_BE", fuse)
+        led = K.SyncLedger()
+        n0 = op.napply
+        res = K.gmres_solve(op, b, cfg, ledger=led)
+        out[fuse] = (res, led.reductions, op.napply - n0)
+    (r1, red1, n1), (r0, red0, n0) = out["1"], out["0"]
+    assert r1.iterations == r0.iterations == cfg.max_iters
+    assert np.array_equal(r1.residual_history, r0.residual_history)
+    assert np.array_equal(r1.backward_errors, r0.backward_errors)
+    assert np.all(np.isfinite(r1.backward_errors)) and np.all(r1.backward_errors > 0)
+    assert red1 == red0 and n1 == n0
+    assert np.array_equal(r1.x.cpu().numpy(), r0.x.cpu().numpy())
+
+
+def test_ell_apply_resid_norms_bitwise(cuda):
+    """kls_ell_apply_resid_norms = kls_ell_spmv (y2 = A x2) + kls_ell_resid_norms
+    (x, b), both bitwise, in one pass."""
+    import torch
+
+    from paper_2104_01253_b200 import _lib as lib
+    from paper_2104_01253_b200 import runtime as rt
+
+    K = kls()
+    op = K.band_random_operator(123_457, band=700, per_row=7, seed=5)
+    ecol, evals, elen, width, ld = op._ell
+    g = torch.Generator(device="cuda").manual_seed(3)
+    x, x2, bb = (torch.randn(op.n, dtype=torch.float64, device="cuda", generator=g) for _ in range(3))
+    st = rt.stream_handle()
+    ws, wsb = rt.workspace(8)
+    y_ref = torch.empty_like(x)
+    lib.call("kls_ell_spmv", ecol.data_ptr(), evals.data_ptr(), elen.data_ptr(), width, op.n, ld,
+             x2.data_ptr(), y_ref.data_ptr(), st)
+    n_ref = torch.zeros(3, dtype=torch.float64, device="cuda")
+    lib.call("kls_ell_resid_norms", ecol.data_ptr(), evals.data_ptr(), elen.data_ptr(), width, op.n,
+             ld, x.data_ptr(), bb.data_ptr(), n_ref.data_ptr(), op.segs.ptr, ws, wsb, st)
+    y2 = torch.full_like(x, float("nan"))
+    n2 = torch.zeros(3, dtype=torch.float64, device="cuda")
+    lib.call("kls_ell_apply_resid_norms", ecol.data_ptr(), evals.data_ptr(), elen.data_ptr(), width,
+             op.n, ld, x2.data_ptr(), y2.data_ptr(), x.data_ptr(), bb.data_ptr(), n2.data_ptr(),
+             op.segs.ptr, ws, wsb, st)
+    assert torch.equal(y2, y_ref)
+    assert torch.equal(n2, n_ref)
