@@ -204,7 +204,7 @@ static int mv_trans_mv_impl(const double* Q, int64_t ldq, int64_t m, int32_t k,
                             int32_t xnorm, double* out, const KlsSegs* segs, void* ws,
                             size_t ws_bytes, void* stream, const peer::Peers* peers,
                             uint64_t epoch, int* err, double* coef = nullptr,
-                            double* gout = nullptr, int32_t qr = 0) {
+                            double* gout = nullptr, int32_t qr = 0, int32_t qprefetch = 0) {
   // a rank may hold no rows (m = 0: empty tensors, null pointers); it still
   // takes part in the reduction tree and the exchange
   if (m < 0 || k < 0 || (k > 0 && ((m > 0 && Q == nullptr) || ldq < m)) ||
@@ -257,6 +257,7 @@ static int mv_trans_mv_impl(const double* Q, int64_t ldq, int64_t m, int32_t k,
     p.coef = last ? coef : nullptr;
     p.gout = gout;
     p.qr = qr;
+    p.qprefetch = qprefetch;
     if (peers != nullptr) p.d.peers = *peers;
     if (peers != nullptr && seg::kMaxExport * gram_nv(p, nx) > peers->cap)
       return fail(KLS_EINVAL, "mv_trans_mv: %d exported values exceed the peer slot (%d)",
@@ -329,6 +330,19 @@ KLS_API int kls_gram_dcgs2_step(const double* Q, int64_t ldq, int64_t m, int32_t
   return mv_trans_mv_impl(Q, ldq, m, j, w, w, aw, 2, 1, out, segs, ws, ws_bytes, stream, nullptr,
                           0, nullptr, coef, gout, qr);
 }
+
+namespace kls {
+// kls_gram_dcgs2_step for the step plan's K2 -> operator -> K1 chain
+// (plan.cu): the Gram kernel streams its first chunk's Q tiles before
+// waiting for the operator (GramParams::qprefetch).
+int gram_dcgs2_step_chain(const double* Q, int64_t ldq, int64_t m, int32_t j, const double* w,
+                          const double* aw, double* out, double* coef, double* gout, int32_t qr,
+                          const KlsSegs* segs, void* ws, size_t ws_bytes, void* stream) {
+  if (coef == nullptr) return fail(KLS_EINVAL, "gram_dcgs2_step: null coefficient buffer");
+  return mv_trans_mv_impl(Q, ldq, m, j, w, w, aw, 2, 1, out, segs, ws, ws_bytes, stream, nullptr,
+                          0, nullptr, coef, gout, qr, 1);
+}
+}  // namespace kls
 
 // The same fused with the peer exchange (kls_gram_dcgs2_peer): Gram pass,
 // global reduction and scalar step in one launch.

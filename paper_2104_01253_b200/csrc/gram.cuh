@@ -31,6 +31,12 @@ struct GramParams {
   double* coef;
   double* gout;
   int32_t qr;
+  // 1: the producer streams the first chunk's Q tiles before waiting for
+  // the preceding kernel -- only for launches whose predecessor writes none
+  // of Q (the step plan's K2 -> operator -> K1 chain: the operator writes
+  // Aw' only, and K2's q_j was complete before the operator passed its own
+  // griddepcontrol.wait, which precedes its trigger)
+  int32_t qprefetch;
 };
 
 constexpr int kG = 4;  // Q columns reduced together

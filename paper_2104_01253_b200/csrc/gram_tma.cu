@@ -40,7 +40,6 @@ constexpr int64_t kAlwaysBalance = int64_t(1) << 40;  // items: always split the
 
 template <int NX>
 __global__ void __launch_bounds__(kTmaThreads, 1) gram_tma_kernel(GramParams p) {
-  pdl_wait();  // x vectors / basis from the preceding kernels
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ double sx[kWarps][NX + 1];
   __shared__ double s_red[kTmaThreads];
@@ -93,6 +92,27 @@ __global__ void __launch_bounds__(kTmaThreads, 1) gram_tma_kernel(GramParams p) 
     if (lane == 0) {
       uint32_t use = 0;  // Q stage fills so far
       uint32_t xuse = 0;
+      int npre = 0;      // Q groups of the CTA's first chunk already in flight
+      if (p.qprefetch && blockIdx.x < p.P.nitems) {
+        int s, v, Vn;
+        seg::item_of(p.P, blockIdx.x, s, v, Vn);
+        const int64_t base = p.P.L.off[s];
+        const int64_t m64 = (p.P.L.off[s + 1] - base) & ~static_cast<int64_t>(63);
+        int64_t row, nr;
+        ChunkWalk<kR> cw(m64, Vn, v, kAlwaysBalance);
+        if (cw.next(row, nr)) {
+          const uint32_t bytes = static_cast<uint32_t>(nr) * sizeof(double);
+          npre = min(ng, kStages);
+          for (int g = 0; g < npre; ++g, ++use) {
+            const int ncols = min(kG, p.k - g * kG);
+            mbar_expect_tx(full + g, static_cast<uint32_t>(ncols) * bytes);
+            for (int cc = 0; cc < ncols; ++cc)
+              bulk_g2s(qring + (static_cast<size_t>(g) * kG + cc) * kR,
+                       p.Q + base + static_cast<int64_t>(g * kG + cc) * p.ldq + row, bytes, full + g);
+          }
+        }
+      }
+      pdl_wait();  // x vectors (and, without qprefetch, the basis) from the preceding kernels
       for (int it = blockIdx.x; it < p.P.nitems; it += gridDim.x) {
         int s, v, Vn;
         seg::item_of(p.P, it, s, v, Vn);
@@ -109,7 +129,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) gram_tma_kernel(GramParams p) 
           mbar_expect_tx(xfull + xs, static_cast<uint32_t>(nxb) * bytes);
           for (int t = 0; t < nxb; ++t)
             bulk_g2s(xbuf + (static_cast<size_t>(xs) * 3 + t) * kR, xsrc[t] + row, bytes, xfull + xs);
-          for (int g = 0; g < ng; ++g, ++use) {
+          for (int g = npre; g < ng; ++g, ++use) {
             const int st = use % kStages;
             const uint32_t round = use / kStages;
             if (round >= 1) mbar_wait(empty + st, (round - 1) & 1);
@@ -119,10 +139,12 @@ __global__ void __launch_bounds__(kTmaThreads, 1) gram_tma_kernel(GramParams p) 
               bulk_g2s(qring + (static_cast<size_t>(st) * kG + cc) * kR,
                        qb + static_cast<int64_t>(g * kG + cc) * p.ldq + row, bytes, full + st);
           }
+          npre = 0;
         }
       }
     }
   } else {
+    pdl_wait();  // the tail rows read x and Q directly
     double* wacc = sacc + warp * stride;
     const int64_t wrow = warp * (64 * kRPt);
     uint32_t use = 0;

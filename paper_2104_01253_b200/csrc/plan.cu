@@ -11,6 +11,16 @@
 
 using namespace kls;
 
+namespace kls {
+int gram_dcgs2_step_chain(const double* Q, int64_t ldq, int64_t m, int32_t j, const double* w,
+                          const double* aw, double* out, double* coef, double* gout, int32_t qr,
+                          const KlsSegs* segs, void* ws, size_t ws_bytes, void* stream);  // gram.cu
+int dcgs2_update_dev_comb(double* Q, int64_t ldq, int64_t m, int32_t j, const double* w,
+                          double* w_out, const double* aw, const double* coef_alpha,
+                          const KlsSegs* segs, void* stream, const double* x, double* xout,
+                          int32_t q, const double* y);  // update.cu
+}
+
 static int apply_op(const KlsOpDesc* op, const double* x, double* y, void* stream) {
   switch (op->kind) {
     case KLS_OP_ELL:
@@ -62,7 +72,7 @@ KLS_API int kls_dcgs2_queue_step(const KlsStepPlan* p, int32_t j, const double* 
   rc = apply_op(&p->op, x_out, aw_out, p->stream);
   if (rc) return rc;
   if (gram) {
-    rc = kls_gram_dcgs2_step(p->Q, p->ldq, p->m, j + 1, w_out, aw_out, p->gdev, p->cdev,
+    rc = gram_dcgs2_step_chain(p->Q, p->ldq, p->m, j + 1, w_out, aw_out, p->gdev, p->cdev,
                              p->gout[slot], p->qr, &p->segs, p->ws, p->ws_bytes, p->stream);
     if (rc) return rc;
     rc = kls_event_record(p->event[slot], p->stream);
@@ -70,12 +80,6 @@ KLS_API int kls_dcgs2_queue_step(const KlsStepPlan* p, int32_t j, const double* 
   return rc;
 }
 
-namespace kls {
-int dcgs2_update_dev_comb(double* Q, int64_t ldq, int64_t m, int32_t j, const double* w,
-                          double* w_out, const double* aw, const double* coef_alpha,
-                          const KlsSegs* segs, void* stream, const double* x, double* xout,
-                          int32_t q, const double* y);  // update.cu
-}
 
 // kls_dcgs2_queue_step with GMRES's backward-error column of an earlier
 // step riding on it (gmres.py:166-172): the update also forms
@@ -102,7 +106,7 @@ KLS_API int kls_dcgs2_queue_step_be(const KlsStepPlan* p, int32_t j, const doubl
                                  p->ws_bytes, p->stream);
   if (rc) return rc;
   if (gram) {
-    rc = kls_gram_dcgs2_step(p->Q, p->ldq, p->m, j + 1, w_out, aw_out, p->gdev, p->cdev,
+    rc = gram_dcgs2_step_chain(p->Q, p->ldq, p->m, j + 1, w_out, aw_out, p->gdev, p->cdev,
                              p->gout[slot], p->qr, &p->segs, p->ws, p->ws_bytes, p->stream);
     if (rc) return rc;
     rc = kls_event_record(p->event[slot], p->stream);
