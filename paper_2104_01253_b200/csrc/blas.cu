@@ -187,9 +187,10 @@ __global__ void __launch_bounds__(kThreads, 2)
 
 // fp64 tensor-core (DMMA, mma.sync m8n8k4) form of the same rotation, for
 // k <= 64: a producer warp streams 128-row tiles of all k columns into a
-// 2-3 stage shared-memory ring with cp.async.bulk (mbarrier completion);
-// each of the 8 consumer warps owns 16 rows of the tile and forms its
-// 16 x 32 output block per pass as 2 x 4 mma tiles, A fragments from the
+// 2-3 stage shared-memory ring with cp.async.bulk (mbarrier completion; its
+// 32 lanes issue the k one-column copies together); each of the MW consumer
+// warps (16 by default) owns 128 / MW rows of the tile and forms its
+// (128 / MW) x 32 output block per pass as MT x 4 mma tiles, A fragments from the
 // tile, B fragments from Z (shared, zero-padded to a multiple of 4 rows),
 // accumulating in k order.  A lane (k-quad q = lane & 3, row r = lane >> 2)
 // reads tile[(kk + q) * ld + r] and Z[(kk + q) * zp + r + 8 b]: with ld = 132
@@ -199,7 +200,10 @@ __global__ void __launch_bounds__(kThreads, 2)
 // them did not change the time: the kernel is bound elsewhere).
 constexpr int kMmaRows = 128;
 constexpr int kMmaLd = 132;
-constexpr int kMmaThreads = 288;
+// MW consumer warps (+ the producer), each owning MT = 16 / MW * 1 m-tiles
+// of 8 rows: 8 warps x 2 tiles or 16 warps x 1 tile per 128-row tile
+template <int MW>
+constexpr int mma_threads() { return (MW + 1) * 32; }
 
 __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
@@ -207,7 +211,8 @@ __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double
                : "d"(a), "d"(b));
 }
 
-__global__ void __launch_bounds__(kMmaThreads, 1)
+template <int MW>
+__global__ void __launch_bounds__(mma_threads<MW>(), 1)
     rotate_mma_kernel(double* __restrict__ V, int64_t ldv, int64_t m, int32_t k, int32_t p,
                       const double* __restrict__ Z, int32_t kp, int32_t zp, int32_t stages) {
   using namespace kls::tma;
@@ -229,34 +234,38 @@ __global__ void __launch_bounds__(kMmaThreads, 1)
   if (threadIdx.x == 0) {
     for (int st = 0; st < stages; ++st) {
       mbar_init(full + st, 1);
-      mbar_init(empty + st, kWarps);
+      mbar_init(empty + st, MW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncthreads();
   const int64_t ntiles = (m + kMmaRows - 1) / kMmaRows;
-  if (warp == kWarps) {  // producer
-    if (lane == 0) {
-      uint32_t use = 0;
-      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++use) {
-        const int st = use % stages;
-        const uint32_t round = use / stages;
+  constexpr int MT = 16 / MW;  // m-tiles per warp
+  if (warp == MW) {  // producer: a tile is k one-column copies of <= 1 KB,
+    // issued by all 32 lanes (one thread issuing them was the bound: ~50 ns
+    // per copy); lane 0 arms the stage's barrier before any copy lands
+    uint32_t use = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++use) {
+      const int st = use % stages;
+      const uint32_t round = use / stages;
+      const int64_t row0 = t * kMmaRows;
+      const int64_t nr = m - row0 < kMmaRows ? m - row0 : kMmaRows;
+      const uint32_t bytes = static_cast<uint32_t>(nr & ~int64_t(1)) * sizeof(double);
+      if (lane == 0) {
         if (round >= 1) mbar_wait(empty + st, (round - 1) & 1);
-        const int64_t row0 = t * kMmaRows;
-        const int64_t nr = m - row0 < kMmaRows ? m - row0 : kMmaRows;
-        const uint32_t bytes = static_cast<uint32_t>(nr & ~int64_t(1)) * sizeof(double);
         mbar_expect_tx(full + st, bytes * static_cast<uint32_t>(k));
-        if (bytes)
-          for (int c = 0; c < k; ++c)
-            bulk_g2s(ring + (static_cast<size_t>(st) * kp + c) * kMmaLd,
-                     V + static_cast<int64_t>(c) * ldv + row0, bytes, full + st);
       }
+      __syncwarp();
+      if (bytes)
+        for (int c = lane; c < k; c += 32)
+          bulk_g2s(ring + (static_cast<size_t>(st) * kp + c) * kMmaLd,
+                   V + static_cast<int64_t>(c) * ldv + row0, bytes, full + st);
     }
     return;
   }
   const int npass = (p + 31) / 32;
-  const int r_a = 16 * warp + (lane >> 2);  // tile row of the A fragment (+8 for block 1)
+  const int r_a = 8 * MT * warp + (lane >> 2);  // tile row of the A fragment (+8 per m-tile)
   const int kq = lane & 3;
   uint32_t use = 0;
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++use) {
@@ -267,32 +276,34 @@ __global__ void __launch_bounds__(kMmaThreads, 1)
     const int64_t nr = m - row0 < kMmaRows ? m - row0 : kMmaRows;
     if (nr & 1) {  // the odd last row is not in the bulk copy
       double* tw = ring + static_cast<size_t>(st) * kp * kMmaLd;
-      for (int c = threadIdx.x; c < k; c += kWarps * 32)
+      for (int c = threadIdx.x; c < k; c += MW * 32)
         tw[c * kMmaLd + nr - 1] = V[static_cast<int64_t>(c) * ldv + row0 + nr - 1];
-      asm volatile("bar.sync 1, 256;" ::: "memory");
+      asm volatile("bar.sync 1, %0;" ::"n"(MW * 32) : "memory");
     }
     for (int pass = 0; pass < npass; ++pass) {
-      double acc[2][4][2];
+      double acc[MT][4][2];
 #pragma unroll
-      for (int a = 0; a < 2; ++a)
+      for (int a = 0; a < MT; ++a)
 #pragma unroll
         for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
       const double* zcol = zs + pass * 32 + (lane >> 2);
 #pragma unroll 4
       for (int kk = 0; kk < kp; kk += 4) {
         const double* trow = tile + (kk + kq) * kMmaLd;
-        const double a0 = trow[r_a], a1 = trow[r_a + 8];
+        double av[MT];
+#pragma unroll
+        for (int a = 0; a < MT; ++a) av[a] = trow[r_a + 8 * a];
         const double* zr = zcol + (kk + kq) * zp;
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
           const double bv = zr[8 * b];
-          dmma884(acc[0][b][0], acc[0][b][1], a0, bv);
-          dmma884(acc[1][b][0], acc[1][b][1], a1, bv);
+#pragma unroll
+          for (int a = 0; a < MT; ++a) dmma884(acc[a][b][0], acc[a][b][1], av[a], bv);
         }
       }
 #pragma unroll
-      for (int a = 0; a < 2; ++a) {
-        const int64_t row = row0 + 16 * warp + 8 * a + (lane >> 2);
+      for (int a = 0; a < MT; ++a) {
+        const int64_t row = row0 + 8 * MT * warp + 8 * a + (lane >> 2);
         if (row >= m) continue;
 #pragma unroll
         for (int b = 0; b < 4; ++b)
@@ -339,19 +350,31 @@ KLS_API int kls_tsgemm_inplace_cols(double* V, int64_t ldv, int64_t m, int32_t k
     const int zpm = (p + 31) / 32 * 32 + 4;  // B fragments conflict-free
     int stages = 3;
     while (stages > 1 && rotate_mma_smem(kp, zpm, stages) > 227 * 1024) --stages;
-    // measured at m = 1e7 (scripts/rotate_probe.py): DMMA 1.57 vs DFMA 2.24 ms
+    // measured at m = 1e7 (scripts/rotate_probe.py): DMMA 1.35 vs DFMA 2.24 ms
     // at k = 60, p = 30; below k ~ 40 the DFMA kernel is faster (k = 30: 0.67
     // vs 0.89 ms).  Both accumulate each output in k order: identical bits.
     if (use_mma && k >= 40 && k <= 64 && stages >= 2 && (reinterpret_cast<uintptr_t>(V) & 15) == 0 &&
         (ldv & 1) == 0) {
       const size_t smem = rotate_mma_smem(kp, zpm, stages);
-      cudaError_t e = cudaFuncSetAttribute(rotate_mma_kernel,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+      // 16 consumer warps x 1 m-tile (4 per SM sub-partition to hide the
+      // DMMA and fragment-load latency): 1.35 ms at config 4's shape, against
+      // 1.45 with 8 warps x 2 tiles (KLS_ROT_WARPS=8, experiments)
+      static const int mw = [] {
+        const char* e = getenv("KLS_ROT_WARPS");
+        return e != nullptr && atoi(e) == 8 ? 8 : 16;
+      }();
+      const void* fn = mw == 16 ? reinterpret_cast<const void*>(rotate_mma_kernel<16>)
+                                : reinterpret_cast<const void*>(rotate_mma_kernel<8>);
+      cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            static_cast<int>(smem));
       if (e != cudaSuccess) return fail(KLS_ECUDA, "rotate_mma smem: %s", cudaGetErrorString(e));
       const int grid = static_cast<int>(std::min<int64_t>(ceil_div(m, kMmaRows), sm_count()));
-      rotate_mma_kernel<<<grid, kMmaThreads, smem, static_cast<cudaStream_t>(stream)>>>(
-          V, ldv, m, k, p, Z, kp, zpm, stages);
+      if (mw == 16)
+        rotate_mma_kernel<16><<<grid, mma_threads<16>(), smem, static_cast<cudaStream_t>(stream)>>>(
+            V, ldv, m, k, p, Z, kp, zpm, stages);
+      else
+        rotate_mma_kernel<8><<<grid, mma_threads<8>(), smem, static_cast<cudaStream_t>(stream)>>>(
+            V, ldv, m, k, p, Z, kp, zpm, stages);
       return check_launch("rotate_mma_kernel");
     }
   }
