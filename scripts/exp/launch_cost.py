@@ -46,5 +46,14 @@ for _ in range(N):
     f(ctypes.byref(plan), 25, w.data_ptr(), w2.data_ptr(), w2.data_ptr(), aw.data_ptr(), a2.data_ptr(), 0, 1)
 t1 = time.perf_counter()
 e1.record(); torch.cuda.synchronize()
+# the device alone: hold the stream with a sleep kernel while the host
+# queues the steps, then time them from an event recorded after the sleep
+torch.cuda._sleep(int(2e9 * (N * 20e-6 + 5e-3)))
+e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e2.record()
+for _ in range(N):
+    f(ctypes.byref(plan), 25, w.data_ptr(), w2.data_ptr(), w2.data_ptr(), aw.data_ptr(), a2.data_ptr(), 0, 1)
+e3.record(); torch.cuda.synchronize()
 print(json.dumps({"m": m, "host_us_per_step": round((t1 - t0) / N * 1e6, 2),
-                  "device_us_per_step": round(e0.elapsed_time(e1) * 1e3 / N, 2)}))
+                  "device_us_per_step_host_paced": round(e0.elapsed_time(e1) * 1e3 / N, 2),
+                  "device_us_per_step_prequeued": round(e2.elapsed_time(e3) * 1e3 / N, 2)}))
