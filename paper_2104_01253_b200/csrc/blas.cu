@@ -319,6 +319,132 @@ __global__ void __launch_bounds__(mma_threads<MW>(), 1)
   }
 }
 
+// The same rotation on 256-row tiles whose columns arrive in stages of 32
+// (kRot2Cols): a tile is two stages, each column copy 2 KB instead of 1 KB
+// -- half the bulk copies per byte (their issue and processing set the pace
+// of the 128-row kernel).  16 consumer warps own 16 rows each (two m-tiles);
+// every output still accumulates its k terms in ascending order: the same
+// bits as rotate_mma_kernel and the DFMA kernel.  ld = 260 (mod 32 = 4):
+// conflict-free fragment loads as with 132.
+constexpr int kRot2Rows = 256;
+constexpr int kRot2Ld = 260;
+constexpr int kRot2Cols = 32;
+constexpr int kRot2Warps = 16;
+constexpr int kRot2Threads = (kRot2Warps + 1) * 32;
+
+__global__ void __launch_bounds__(kRot2Threads, 1)
+    rotate_mma2_kernel(double* __restrict__ V, int64_t ldv, int64_t m, int32_t k, int32_t p,
+                       const double* __restrict__ Z, int32_t kp, int32_t zp, int32_t stages) {
+  using namespace kls::tma;
+  extern __shared__ __align__(128) unsigned char smr_raw[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smr_raw);
+  uint64_t* empty = full + 4;
+  double* zs = reinterpret_cast<double*>(smr_raw + 128);        // [kp][zp]
+  double* ring = zs + static_cast<size_t>(kp) * zp;             // [stages][kRot2Cols][kRot2Ld]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nch = (kp + kRot2Cols - 1) / kRot2Cols;  // column stages per tile
+  for (int i = threadIdx.x; i < kp * zp; i += blockDim.x) {
+    const int r = i / zp, c = i % zp;
+    zs[i] = (r < k && c < p) ? Z[static_cast<int64_t>(c) * k + r] : 0.0;
+  }
+  // stage columns past k are never loaded: zero (they meet zero rows of Z)
+  for (int i = threadIdx.x; i < stages * kRot2Cols * kRot2Ld; i += blockDim.x) ring[i] = 0.0;
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < stages; ++st) {
+      mbar_init(full + st, 1);
+      mbar_init(empty + st, kRot2Warps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+  const int64_t ntiles = (m + kRot2Rows - 1) / kRot2Rows;
+  if (warp == kRot2Warps) {  // producer: all 32 lanes issue a stage's column copies
+    uint32_t use = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      const int64_t row0 = t * kRot2Rows;
+      const int64_t nr = m - row0 < kRot2Rows ? m - row0 : kRot2Rows;
+      const uint32_t bytes = static_cast<uint32_t>(nr & ~int64_t(1)) * sizeof(double);
+      for (int h = 0; h < nch; ++h, ++use) {
+        const int st = use % stages;
+        const uint32_t round = use / stages;
+        const int c0 = h * kRot2Cols;
+        const int nc = min(kRot2Cols, k - c0);
+        if (lane == 0) {
+          if (round >= 1) mbar_wait(empty + st, (round - 1) & 1);
+          mbar_expect_tx(full + st, bytes * static_cast<uint32_t>(nc > 0 ? nc : 0));
+        }
+        __syncwarp();
+        if (bytes)
+          for (int c = lane; c < nc; c += 32)
+            bulk_g2s(ring + (static_cast<size_t>(st) * kRot2Cols + c) * kRot2Ld,
+                     V + static_cast<int64_t>(c0 + c) * ldv + row0, bytes, full + st);
+      }
+    }
+    return;
+  }
+  const int npass = (p + 31) / 32;
+  const int r_a = 16 * warp + (lane >> 2);  // tile row of the A fragment (+8 for the 2nd m-tile)
+  const int kq = lane & 3;
+  uint32_t use = 0;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int64_t row0 = t * kRot2Rows;
+    const int64_t nr = m - row0 < kRot2Rows ? m - row0 : kRot2Rows;
+    // npass > 1 (p > 32) would re-read the stages: this kernel takes p <= 32
+    double acc[2][4][2];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    for (int h = 0; h < nch; ++h, ++use) {
+      const int st = use % stages;
+      mbar_wait(full + st, (use / stages) & 1);
+      const double* tile = ring + static_cast<size_t>(st) * kRot2Cols * kRot2Ld;
+      const int c0 = h * kRot2Cols;
+      if (nr & 1) {  // the odd last row is not in the bulk copy
+        double* tw = ring + static_cast<size_t>(st) * kRot2Cols * kRot2Ld;
+        for (int c = threadIdx.x; c < min(kRot2Cols, k - c0); c += kRot2Warps * 32)
+          tw[c * kRot2Ld + nr - 1] = V[static_cast<int64_t>(c0 + c) * ldv + row0 + nr - 1];
+        asm volatile("bar.sync 1, %0;" ::"n"(kRot2Warps * 32) : "memory");
+      }
+      const int kend = min(kRot2Cols, kp - c0);
+      const double* zcol = zs + (lane >> 2);
+#pragma unroll 4
+      for (int kk = 0; kk < kend; kk += 4) {
+        const double* trow = tile + (kk + kq) * kRot2Ld;
+        const double a0 = trow[r_a], a1 = trow[r_a + 8];
+        const double* zr = zcol + (c0 + kk + kq) * zp;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const double bv = zr[8 * b];
+          dmma884(acc[0][b][0], acc[0][b][1], a0, bv);
+          dmma884(acc[1][b][0], acc[1][b][1], a1, bv);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + st);
+    }
+    (void)npass;
+#pragma unroll
+    for (int a = 0; a < 2; ++a) {
+      const int64_t row = row0 + 16 * warp + 8 * a + (lane >> 2);
+      if (row >= m) continue;
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int col = 8 * b + 2 * kq + e;
+          if (col < p) V[static_cast<int64_t>(col) * ldv + row] = acc[a][b][e];
+        }
+    }
+  }
+}
+
+size_t rotate_mma2_smem(int kp, int zp, int stages) {
+  return 128 + sizeof(double) * (static_cast<size_t>(kp) * zp +
+                                 static_cast<size_t>(stages) * kRot2Cols * kRot2Ld);
+}
+
 size_t rotate_mma_smem(int kp, int zp, int stages) {
   return 128 + sizeof(double) * (static_cast<size_t>(kp) * zp +
                                  static_cast<size_t>(stages) * kp * kMmaLd);
@@ -355,6 +481,25 @@ KLS_API int kls_tsgemm_inplace_cols(double* V, int64_t ldv, int64_t m, int32_t k
     // vs 0.89 ms).  Both accumulate each output in k order: identical bits.
     if (use_mma && k >= 40 && k <= 64 && stages >= 2 && (reinterpret_cast<uintptr_t>(V) & 15) == 0 &&
         (ldv & 1) == 0) {
+      static const bool rot2 = [] {  // KLS_ROT2=0: the 128-row kernel (experiments)
+        const char* e = getenv("KLS_ROT2");
+        return !(e != nullptr && e[0] == '0');
+      }();
+      if (rot2 && p <= 32) {
+        int st2 = 4;
+        while (st2 > 2 && rotate_mma2_smem(kp, zpm, st2) > 220 * 1024) --st2;
+        const size_t smem2 = rotate_mma2_smem(kp, zpm, st2);
+        if (smem2 <= 220 * 1024) {
+          cudaError_t e = cudaFuncSetAttribute(rotate_mma2_kernel,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               static_cast<int>(smem2));
+          if (e != cudaSuccess) return fail(KLS_ECUDA, "rotate_mma2 smem: %s", cudaGetErrorString(e));
+          const int grid2 = static_cast<int>(std::min<int64_t>(ceil_div(m, kRot2Rows), sm_count()));
+          rotate_mma2_kernel<<<grid2, kRot2Threads, smem2, static_cast<cudaStream_t>(stream)>>>(
+              V, ldv, m, k, p, Z, kp, zpm, st2);
+          return check_launch("rotate_mma2_kernel");
+        }
+      }
       const size_t smem = rotate_mma_smem(kp, zpm, stages);
       // 16 consumer warps x 1 m-tile (4 per SM sub-partition to hide the
       // DMMA and fragment-load latency): 1.35 ms at config 4's shape, against

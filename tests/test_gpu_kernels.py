@@ -263,7 +263,8 @@ def test_tsgemm_inplace(cuda, rng):
 
 @pytest.mark.parametrize("m,k,p", [(1, 1, 1), (127, 5, 3), (130, 60, 30), (10007, 37, 37),
                                    (100_003, 60, 33), (4099, 70, 65), (777, 100, 100),
-                                   (100_003, 100, 100), (1_000_003, 60, 30)])
+                                   (100_003, 100, 100), (1_000_003, 60, 30), (257, 64, 32),
+                                   (513, 41, 17), (300_001, 44, 32)])
 def test_tsgemm_inplace_cols(cuda, rng, m, k, p):
     """Krylov-Schur rotation V(:, :p) <- V(:, :k) Z(:, :p): ragged row tiles,
     column passes beyond 32, columns p..k-1 untouched; bitwise equal to the
