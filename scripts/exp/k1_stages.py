@@ -1,5 +1,7 @@
-"""K1 (kls_gram_dcgs2, the TMA-staged Gram pass) device time vs ring depth
-(KLS_K1_STAGES) at medium and headline m.  Prints one JSON line."""
+"""K1 (kls_gram_dcgs2, the TMA-staged Gram pass) device time at medium and
+headline m.  Prints one JSON line.  Used with a temporary KLS_K1_STAGES
+ring-depth knob (3-6 stages: within 2 %; the knob was removed and
+the ring stays at 4 stages)."""
 import json, os, sys
 import numpy as np, torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
