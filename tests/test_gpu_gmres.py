@@ -110,12 +110,14 @@ def test_gmres_config2_full_size_iteration_parity(cuda):
     assert led.reductions == int(g["reductions"])
 
 
-@pytest.mark.parametrize("k,restart", [(300, 20), (301, 7)])
+@pytest.mark.parametrize("k,restart", [(300, 20), (301, 7), (300, 80)])
 def test_fused_backward_errors_bitwise(cuda, monkeypatch, k, restart):
     """Each drained column's x_j = x + V y and its norms ride on the next
     step's update and ELL product (kls_dcgs2_queue_step_be): the backward
     errors, residual history, ledger and apply count are BITWISE those of the
-    separate launches (KLS_FUSE_BE=0), on an even and an odd row count."""
+    separate launches (KLS_FUSE_BE=0), on an even and an odd row count; with
+    restart 80 the columns past 64 coefficients take the update's fallback
+    (the separate combination inside kls_dcgs2_queue_step_be)."""
     K = kls()
     op = K.manteuffel_operator(K.ManteuffelSpec(k=k, beta=0.5))
     assert op._ell is not None and op.n > 65536
