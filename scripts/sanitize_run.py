@@ -22,6 +22,18 @@ ld = runtime.pad_rows(m)
 V = torch.randn((k + 1, ld), dtype=torch.float64, device="cuda")
 Z = torch.randn(k * p, dtype=torch.float64, device="cuda")
 _lib.call("kls_tsgemm_inplace_cols", V.data_ptr(), ld, m, k, p, Z.data_ptr(), runtime.stream_handle())
+# the 256-row rotation (p <= 32): ragged last tile, odd row count, two column stages
+m, k, p = 3001, 44, 30
+ld = runtime.pad_rows(m)
+V = torch.randn((k + 1, ld), dtype=torch.float64, device="cuda")
+Z = torch.randn(k * p, dtype=torch.float64, device="cuda")
+_lib.call("kls_tsgemm_inplace_cols", V.data_ptr(), ld, m, k, p, Z.data_ptr(), runtime.stream_handle())
+# GMRES with backward errors riding on the next step (combined update + dual
+# ELL kernel): ELL operator above 65536 rows, odd m, restart 7
+bop = kls.manteuffel_operator(kls.ManteuffelSpec(k=257))
+kls.gmres_solve(bop, rng.standard_normal(bop.n),
+                kls.GmresConfig(max_iters=16, restart=7, rtol=1e-14, scheme="dcgs2",
+                                backward_errors=True))
 # host Schur services (C++) on a 40 x 40 problem
 from paper_2104_01253_b200 import schur
 f = schur.hessenberg_real_schur(schur.hessenberg_reduce(rng.standard_normal((40, 40)))[0])
