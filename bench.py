@@ -273,7 +273,8 @@ def measured_peak():
 def ncu_traffic(kernel):
     """dram bytes per launch of `kernel` from the committed ncu --set full
     summary (profiles/ncu_summary.json), with the launch's algorithmic bytes."""
-    for name in ("ncu_summary_r02.json", "ncu_summary.json", "ncu_summary_cgs2.json"):
+    for name in ("ncu_summary_r02b.json", "ncu_summary_r02.json", "ncu_summary.json",
+                 "ncu_summary_cgs2.json"):
         try:
             with open(os.path.join(ROOT, "profiles", name)) as f:
                 d = json.load(f)
